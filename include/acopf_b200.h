@@ -1,0 +1,119 @@
+/* C ABI of the B200 ACOPF callback evaluator (libacopf_b200.so).
+ *
+ * Drop-in boundary for the reference's callback path.  The
+ * reference binds these callbacks through Python (`opfkit.nlp.NlpProblem`,
+ * pkg/src/opfkit/nlp.py:26-49); the Python package in this repo binds this
+ * header through ctypes and rebuilds the same NlpProblem, and INTEGRATION.md
+ * shows the equivalent ctypes stub a maintainer would add to opfkit.
+ *
+ * Entry point -> reference interface it replaces:
+ *   acopf_topo_create      _Engine.__init__ packing + _build_patterns   (acopf.py:77-195)
+ *   acopf_batch_create     composer._Builder.assemble: build_acopf per stage (composer.py:199-203)
+ *   acopf_batch_stage_sizes  NlpProblem.n/m_eq/m_ineq + nnz of each stage (acopf.py:392-410)
+ *   acopf_batch_set_layout   composite offsets, coupling rows        (composer.py:206-242)
+ *   acopf_batch_eval       objective/gradient/constraints/jacobian/lagrangian_hessian
+ *                          of every stage at once, device buffers     (acopf.py:266-373,
+ *                                                                     composer.py:256-311)
+ *   acopf_batch_eval_host  same with host buffers (H2D + eval + D2H on the handle's stream)
+ *   acopf_batch_pattern    CSR indptr/indices of J or H (stage or composite) -- the fixed
+ *                          pattern scipy would produce (acopf.py:308-311, 370-373)
+ *   acopf_last_error       error text (Python raises DeviceError / Disconnected ...)
+ *
+ * Conventions: plain pointers and sizes, no exceptions across the ABI.  Every
+ * function returns 0 on success and nonzero on failure; the message is in
+ * acopf_last_error() (thread-local).  Device pointers are CUDA global memory on
+ * the handle's device.  Evaluation is stream-ordered on the given stream
+ * (NULL = the handle's own stream); one handle must not be evaluated
+ * concurrently from two streams (it owns one objective scratch buffer).
+ */
+#ifndef ACOPF_B200_H
+#define ACOPF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct acopf_topo acopf_topo;
+typedef struct acopf_batch acopf_batch;
+
+/* what-mask bits for acopf_batch_eval */
+#define ACOPF_OBJ 1u
+#define ACOPF_GRAD 2u
+#define ACOPF_CONS 4u
+#define ACOPF_JAC 8u
+#define ACOPF_HESS 16u
+#define ACOPF_ALL 31u
+
+/* objective modes for acopf_batch_set_layout */
+#define ACOPF_OBJ_PER_STAGE 0   /* obj[slot_s] = f_s (independent points)            */
+#define ACOPF_OBJ_WEIGHTED 1    /* obj[0] = ((0 + w_0 f_0) + w_1 f_1) + ... (composite) */
+#define ACOPF_OBJ_TERMS 2       /* obj[slot_s] = w_s f_s, summed by the caller (sharded) */
+
+const char* acopf_last_error(void);
+int acopf_version(void);
+
+/* One packed topology (active buses, live branches and generators) in the
+ * reference's per-unit conventions.  fo/to: bus slots per live branch; adm:
+ * 8 doubles per branch (gff, bff, gft, bft, gtf, btf, gtt, btt), branch-major;
+ * rated: 1 when rate_a > 0; gbus: bus slot per live generator; gs/bs: per unit. */
+int acopf_topo_create(int32_t nb, int32_t nbr, int32_t ng, const int32_t* fo, const int32_t* to,
+                      const double* adm, const uint8_t* rated, const int32_t* gbus,
+                      const double* gs, const double* bs, acopf_topo** out);
+int acopf_topo_destroy(acopf_topo* t);
+
+/* A batch of stages on one device.  Stage s uses topology stage_topo[s] minus
+ * the branches removed_idx[removed_ptr[s] .. removed_ptr[s+1]) (topology-local
+ * branch indices), loads set stage_load[s] (pd/qd, nb values each, at
+ * load_off[set]) and cost set stage_cost[s] (ca/cb/cc, ng values each, at
+ * cost_off[set]), objective weight weight[s]. */
+int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos, int32_t n_stages,
+                       const int32_t* stage_topo, const int64_t* removed_ptr, const int32_t* removed_idx,
+                       const int32_t* stage_load, const int64_t* load_off, int64_t n_load_values,
+                       const double* pd, const double* qd, const int32_t* stage_cost,
+                       const int64_t* cost_off, int64_t n_cost_values, const double* ca,
+                       const double* cb, const double* cc, const double* weight, acopf_batch** out);
+int acopf_batch_destroy(acopf_batch* b);
+
+/* Per stage, 6 values: n, m_eq, m_ineq, nnz of the J equality rows, nnz of the
+ * J inequality rows, nnz of H. */
+int acopf_batch_stage_sizes(const acopf_batch* b, int64_t* out6);
+
+/* Output placement of every stage inside the caller's flat buffers (6 int64
+ * per stage: var_off, eq_row, ineq_row, jeq_base, jineq_base, h_base), the
+ * objective mode and slots, and the coupling rows: cons row, position of the
+ * row's 2 J values, x index of the child (a) and base (b) quantity, and
+ * whether the base column sorts first (J values -1, +1) or not (+1, -1). */
+int acopf_batch_set_layout(acopf_batch* b, const int64_t* offsets6, int32_t obj_mode,
+                           const int32_t* obj_slot, int64_t n_coupling, const int64_t* cp_row,
+                           const int64_t* cp_jpos, const int64_t* cp_a, const int64_t* cp_b,
+                           const int8_t* cp_base_first);
+
+/* Evaluate the requested callbacks of every stage at (x, obj_factor, mult).
+ * Unrequested outputs may be NULL.  All pointers are device pointers. */
+int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const double* mult,
+                     uint32_t what, double* obj, double* grad, double* cons, double* jval,
+                     double* hval, void* stream);
+
+/* Same, host pointers; sizes of the flat buffers in doubles.  Copies in,
+ * evaluates and copies out on the handle's stream, then synchronises. */
+int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double obj_factor,
+                          const double* mult, int64_t nm, uint32_t what, double* obj, int64_t nobj,
+                          double* grad, int64_t ngrad, double* cons, int64_t ncons, double* jval,
+                          int64_t nj, double* hval, int64_t nh);
+
+/* CSR pattern of one stage (stage >= 0; rows: that stage's constraints or
+ * variables; columns stage-local) or of the whole laid-out batch (stage = -1,
+ * needs set_layout; n_rows/n_cols are the flat sizes).  which: 0 = J, 1 = H.
+ * indptr has rows+1 entries (int64), indices nnz entries (int32). */
+int acopf_batch_pattern(const acopf_batch* b, int32_t stage, int32_t which, int64_t n_rows,
+                        int64_t* indptr, int32_t* indices);
+
+/* Kernel launches issued by this handle since creation (evidence counter). */
+int64_t acopf_batch_launches(const acopf_batch* b);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,575 @@
+// C ABI of libacopf_b200.so: batch planning on the host, device residency,
+// and the evaluation launch.  See include/acopf_b200.h for the contract.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/acopf_b200.h"
+#include "eval_kernel.cuh"
+#include "planner.hpp"
+
+using namespace acopf;
+
+namespace {
+thread_local std::string g_err;
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    } catch (...) {
+        g_err = "unknown error";
+        return 1;
+    }
+}
+
+// RAII device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { if (p) cudaFree(p); }
+    template <class T>
+    T* upload(const std::vector<T>& v) {
+        n = std::max<size_t>(sizeof(T) * v.size(), 16);
+        cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+        if (!v.empty()) cuda_check(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "H2D");
+        return static_cast<T*>(p);
+    }
+    void* alloc(size_t bytes) {
+        n = std::max<size_t>(bytes, 16);
+        cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+        // setup-time zeroing on the legacy stream: synchronise so it cannot land
+        // after work later queued on the handle's non-blocking stream
+        cuda_check(cudaMemset(p, 0, n), "cudaMemset");
+        cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+        return p;
+    }
+};
+
+struct StageInfo {
+    int topo = 0;
+    std::vector<int> removed;        // topology-local branch ids, sorted
+    std::vector<int> removed_rated;  // their rated indices (sorted), rated only
+    std::vector<int> removed_rowsz;
+    int64_t pd_off = 0, cost_off = 0;
+    double w = 1.0;
+    std::vector<int> table;          // per tile: table index in the blob list
+    // sizes
+    int64_t n = 0, m_eq = 0, m_ineq = 0, nnz_jeq = 0, nnz_jin = 0, nnz_h = 0, hpg_local = 0;
+    std::vector<int> tile_off;       // per tile 4 offsets (P, Q, VA, VM), stage-local
+};
+}  // namespace
+
+struct acopf_topo {
+    Topo t;
+};
+
+struct acopf_batch {
+    int device = 0;
+    std::vector<const Topo*> topos;
+    std::vector<std::vector<int>> base_table;            // topo -> per tile -> table id
+    std::vector<TileTable> tables;
+    std::map<std::pair<int, std::pair<std::vector<int>, int>>, int> patch_cache;
+    std::vector<StageInfo> stages;
+    std::vector<double> pd, qd, ca, cb, cc;
+    // layout
+    bool laid_out = false, uploaded = false;
+    std::vector<int32_t> obj_slot;
+    std::vector<int64_t> off6;
+    std::vector<int64_t> cp_row, cp_jpos, cp_a, cp_b;
+    std::vector<int8_t> cp_first;
+    int obj_mode = 0, n_obj = 0;
+    // device
+    cudaStream_t stream = nullptr;
+    DevBuf d_topo, d_stage, d_work, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
+    DevBuf d_cprow, d_cpj, d_cpa, d_cpb, d_cpf, d_objterms, d_counter;
+    std::vector<std::unique_ptr<DevBuf>> topo_bufs;
+    EvalParams params{};
+    size_t smem = 0;
+    int64_t launches = 0;
+    // host staging for eval_host
+    DevBuf h_x, h_m, h_obj, h_g, h_c, h_j, h_h;
+
+    ~acopf_batch() {
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+static void upload(acopf_batch* b) {
+        cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
+        const int S = (int)b->stages.size();
+        const int64_t n_coupling = (int64_t)b->cp_row.size();
+        const int obj_mode = b->obj_mode;
+        if (!b->stream) cuda_check(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "stream");
+
+        // topologies
+        std::vector<DTopo> dt;
+        b->topo_bufs.clear();
+        for (const Topo* T : b->topos) {
+            DTopo d{};
+            d.nb = T->nb; d.nbr = T->nbr; d.ng = T->ng; d.nr = T->nr;
+            auto up = [&](const auto& v) {
+                b->topo_bufs.emplace_back(new DevBuf());
+                return b->topo_bufs.back()->upload(v);
+            };
+            d.fo = up(T->fo); d.to = up(T->to); d.adm = up(T->adm); d.ridx = up(T->ridx);
+            d.gs = up(T->gs); d.bs = up(T->bs); d.gen_ptr = up(T->gen_ptr); d.gen_list = up(T->gen_list);
+            std::vector<long long> foff(T->foff.begin(), T->foff.end());
+            d.foff = up(foff);
+            d.rowsz = up(T->rowsz);
+            std::vector<int> leaf;
+            for (size_t l = 0; l < T->leaf_start.size(); ++l) { leaf.push_back(T->leaf_start[l]); leaf.push_back(T->leaf_len[l]); }
+            d.leaf = up(leaf);
+            d.nleaf = (int)T->leaf_start.size();
+            dt.push_back(d);
+        }
+        // blob of tile tables
+        std::vector<uint8_t> blob;
+        std::vector<int64_t> table_off(b->tables.size());
+        size_t max_q = 64;
+        for (size_t i = 0; i < b->tables.size(); ++i) {
+            table_off[i] = (int64_t)blob.size();
+            b->tables[i].serialise(blob);
+            max_q = std::max(max_q, (size_t)b->tables[i].nQ());
+        }
+        // stages, removed lists, work items (bus tiles first, stage-major)
+        std::vector<DStage> ds(S);
+        std::vector<int> rem, remsz;
+        std::vector<DWork> work;
+        int n_obj = 0;
+        for (int s = 0; s < S; ++s) {
+            const StageInfo& st = b->stages[s];
+            const Topo& T = *b->topos[st.topo];
+            DStage& d = ds[s];
+            const int64_t* o = &b->off6[6 * s];
+            d.var_off = o[0]; d.eq_row = o[1]; d.ineq_row = o[2];
+            d.jeq_base = o[3]; d.jineq_base = o[4]; d.h_base = o[5];
+            d.hpg_local = st.hpg_local;
+            d.pd_off = st.pd_off;
+            d.cost_off = st.cost_off;
+            d.rem_off = (long long)rem.size();
+            d.nrem = (int)st.removed_rated.size();
+            rem.insert(rem.end(), st.removed_rated.begin(), st.removed_rated.end());
+            remsz.insert(remsz.end(), st.removed_rowsz.begin(), st.removed_rowsz.end());
+            d.topo = st.topo;
+            d.obj_slot = b->obj_slot[s];
+            d.w = st.w;
+            max_q = std::max(max_q, T.leaf_start.size());
+            for (size_t t = 0; t < st.table.size(); ++t) {
+                DWork w{};
+                w.stage = s;
+                w.blob_off = table_off[st.table[t]];
+                w.jP = st.tile_off[4 * t + 0]; w.jQ = st.tile_off[4 * t + 1];
+                w.hA = st.tile_off[4 * t + 2]; w.hV = st.tile_off[4 * t + 3];
+                work.push_back(w);
+            }
+        }
+        const int n_bus = (int)work.size();
+        for (int s = 0; s < S; ++s) {
+            const Topo& T = *b->topos[b->stages[s].topo];
+            int nch = std::max(1, (T.ng + GEN_CHUNK - 1) / GEN_CHUNK);
+            for (int c = 0; c < nch; ++c) {
+                DWork w{};
+                w.stage = s;
+                w.jP = c;
+                work.push_back(w);
+            }
+            n_obj++;
+        }
+        const int n_gen = (int)work.size() - n_bus;
+        const int n_cp = (int)((n_coupling + CP_CHUNK - 1) / CP_CHUNK);
+        b->n_obj = n_obj;
+
+        EvalParams& P = b->params;
+        P = EvalParams{};
+        P.topos = b->d_topo.upload(dt);
+        P.stages = b->d_stage.upload(ds);
+        P.work = b->d_work.upload(work);
+        P.blob = b->d_blob.upload(blob);
+        P.pd = b->d_pd.upload(b->pd);
+        P.qd = b->d_qd.upload(b->qd);
+        P.ca = b->d_ca.upload(b->ca);
+        P.cb = b->d_cb.upload(b->cb);
+        P.cc = b->d_cc.upload(b->cc);
+        P.rem_ridx = b->d_rem.upload(rem);
+        P.rem_rowsz = b->d_remsz.upload(remsz);
+        P.cp_row = reinterpret_cast<const long long*>(b->d_cprow.upload(b->cp_row));
+        P.cp_jpos = reinterpret_cast<const long long*>(b->d_cpj.upload(b->cp_jpos));
+        P.cp_a = reinterpret_cast<const long long*>(b->d_cpa.upload(b->cp_a));
+        P.cp_b = reinterpret_cast<const long long*>(b->d_cpb.upload(b->cp_b));
+        P.cp_base_first = reinterpret_cast<const signed char*>(b->d_cpf.upload(b->cp_first));
+        P.ncp = n_coupling;
+        P.n_bus_work = n_bus;
+        P.n_gen_work = n_gen;
+        P.n_cp_work = n_cp;
+        P.n_obj = n_obj;
+        P.obj_mode = obj_mode;
+        P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
+        P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
+        b->smem = sizeof(double) * max_q;
+        if (b->smem > 48 * 1024)
+            cuda_check(cudaFuncSetAttribute(acopf_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)b->smem), "cudaFuncSetAttribute");
+        b->uploaded = true;
+}
+
+
+
+extern "C" {
+
+const char* acopf_last_error(void) { return g_err.c_str(); }
+int acopf_version(void) { return 1; }
+
+int acopf_topo_create(int32_t nb, int32_t nbr, int32_t ng, const int32_t* fo, const int32_t* to,
+                      const double* adm, const uint8_t* rated, const int32_t* gbus, const double* gs,
+                      const double* bs, acopf_topo** out) {
+    return guard([&] {
+        if (nb < 0 || nbr < 0 || ng < 0) throw std::runtime_error("negative size");
+        auto* h = new acopf_topo();
+        Topo& T = h->t;
+        T.nb = nb; T.nbr = nbr; T.ng = ng;
+        T.fo.assign(fo, fo + nbr);
+        T.to.assign(to, to + nbr);
+        T.adm.assign(adm, adm + 8 * (size_t)nbr);
+        T.ridx.assign(nbr, -1);
+        int r = 0;
+        for (int k = 0; k < nbr; ++k) {
+            if (fo[k] < 0 || fo[k] >= nb || to[k] < 0 || to[k] >= nb) { delete h; throw std::runtime_error("branch bus slot out of range"); }
+            if (rated[k]) T.ridx[k] = r++;
+        }
+        T.gbus.assign(gbus, gbus + ng);
+        for (int g = 0; g < ng; ++g)
+            if (gbus[g] < 0 || gbus[g] >= nb) { delete h; throw std::runtime_error("generator bus slot out of range"); }
+        T.gs.assign(gs, gs + nb);
+        T.bs.assign(bs, bs + nb);
+        T.finalize();
+        *out = h;
+    });
+}
+
+int acopf_topo_destroy(acopf_topo* t) {
+    delete t;
+    return 0;
+}
+
+int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos, int32_t n_stages,
+                       const int32_t* stage_topo, const int64_t* removed_ptr, const int32_t* removed_idx,
+                       const int32_t* stage_load, const int64_t* load_off, int64_t n_load_values,
+                       const double* pd, const double* qd, const int32_t* stage_cost,
+                       const int64_t* cost_off, int64_t n_cost_values, const double* ca, const double* cb,
+                       const double* cc, const double* weight, acopf_batch** out) {
+    return guard([&] {
+        std::unique_ptr<acopf_batch> B(new acopf_batch());
+        B->device = device;
+        for (int i = 0; i < n_topos; ++i) B->topos.push_back(&topos[i]->t);
+        // base tile tables
+        for (int i = 0; i < n_topos; ++i) {
+            const Topo& T = *B->topos[i];
+            std::vector<int> ids;
+            for (size_t t = 0; t + 1 < T.tile_b0.size(); ++t) {
+                B->tables.push_back(build_tile(T, (int)t, Live{}));
+                ids.push_back((int)B->tables.size() - 1);
+            }
+            B->base_table.push_back(ids);
+        }
+        B->pd.assign(pd, pd + n_load_values);
+        B->qd.assign(qd, qd + n_load_values);
+        B->ca.assign(ca, ca + n_cost_values);
+        B->cb.assign(cb, cb + n_cost_values);
+        B->cc.assign(cc, cc + n_cost_values);
+        B->stages.resize(n_stages);
+        for (int s = 0; s < n_stages; ++s) {
+            StageInfo& S = B->stages[s];
+            S.topo = stage_topo[s];
+            if (S.topo < 0 || S.topo >= n_topos) throw std::runtime_error("stage topology index out of range");
+            const Topo& T = *B->topos[S.topo];
+            S.removed.assign(removed_idx + removed_ptr[s], removed_idx + removed_ptr[s + 1]);
+            std::sort(S.removed.begin(), S.removed.end());
+            S.removed.erase(std::unique(S.removed.begin(), S.removed.end()), S.removed.end());
+            S.pd_off = load_off[stage_load[s]];
+            S.cost_off = cost_off[stage_cost[s]];
+            S.w = weight[s];
+            if (S.pd_off < 0 || S.pd_off + T.nb > n_load_values) throw std::runtime_error("load set out of range");
+            if (S.cost_off < 0 || S.cost_off + T.ng > n_cost_values) throw std::runtime_error("cost set out of range");
+            // tables: base unless the tile holds an endpoint of a removed branch
+            S.table = B->base_table[S.topo];
+            std::vector<int> touched;
+            for (int k : S.removed) {
+                if (k < 0 || k >= T.nbr) throw std::runtime_error("removed branch out of range");
+                if (T.ridx[k] >= 0) {
+                    S.removed_rated.push_back(T.ridx[k]);
+                    S.removed_rowsz.push_back(T.rowsz[T.ridx[k]]);
+                }
+                for (int bus : {T.fo[k], T.to[k]}) {
+                    int t = int(std::upper_bound(T.tile_b0.begin(), T.tile_b0.end(), bus) - T.tile_b0.begin()) - 1;
+                    touched.push_back(t);
+                }
+            }
+            {   // keep rated lists sorted together
+                std::vector<int> order(S.removed_rated.size());
+                std::iota(order.begin(), order.end(), 0);
+                std::sort(order.begin(), order.end(), [&](int a, int b) { return S.removed_rated[a] < S.removed_rated[b]; });
+                std::vector<int> rr, rz;
+                for (int o : order) { rr.push_back(S.removed_rated[o]); rz.push_back(S.removed_rowsz[o]); }
+                S.removed_rated = rr;
+                S.removed_rowsz = rz;
+            }
+            std::sort(touched.begin(), touched.end());
+            touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+            for (int t : touched) {
+                auto key = std::make_pair(S.topo, std::make_pair(S.removed, t));
+                auto it = B->patch_cache.find(key);
+                if (it == B->patch_cache.end()) {
+                    B->tables.push_back(build_tile(T, t, Live{&S.removed}));
+                    it = B->patch_cache.emplace(key, (int)B->tables.size() - 1).first;
+                }
+                S.table[t] = it->second;
+            }
+            // sizes and stage-local segment offsets
+            const int ntile = (int)S.table.size();
+            int64_t LP = 0, LQ = 0, LA = 0, LV = 0;
+            for (int t = 0; t < ntile; ++t) {
+                const TileTable& tt = B->tables[S.table[t]];
+                LP += tt.L[0]; LQ += tt.L[1]; LA += tt.L[2]; LV += tt.L[3];
+            }
+            S.tile_off.assign(4 * ntile, 0);
+            int64_t aP = 0, aQ = LP, aA = 0, aV = LA;
+            for (int t = 0; t < ntile; ++t) {
+                const TileTable& tt = B->tables[S.table[t]];
+                S.tile_off[4 * t + 0] = (int)aP; aP += tt.L[0];
+                S.tile_off[4 * t + 1] = (int)aQ; aQ += tt.L[1];
+                S.tile_off[4 * t + 2] = (int)aA; aA += tt.L[2];
+                S.tile_off[4 * t + 3] = (int)aV; aV += tt.L[3];
+            }
+            int64_t ineq = 0;
+            for (int r = 0; r < T.nr; ++r) ineq += T.rowsz[r];
+            for (int z : S.removed_rowsz) ineq -= z;
+            S.n = 2LL * T.nb + 2LL * T.ng;
+            S.m_eq = 2LL * T.nb;
+            S.m_ineq = 2LL * (T.nr - (int64_t)S.removed_rated.size());
+            S.nnz_jeq = LP + LQ;
+            S.nnz_jin = ineq;
+            S.hpg_local = LA + LV;
+            S.nnz_h = LA + LV + T.ng;
+            if (S.nnz_jeq + S.nnz_jin >= (1LL << 31) || S.nnz_h >= (1LL << 31))
+                throw std::runtime_error("stage too large for 32-bit offsets");
+        }
+        *out = B.release();
+    });
+}
+
+int acopf_batch_destroy(acopf_batch* b) {
+    if (b) {
+        cudaSetDevice(b->device);
+        delete b;
+    }
+    return 0;
+}
+
+int acopf_batch_stage_sizes(const acopf_batch* b, int64_t* out6) {
+    return guard([&] {
+        for (size_t s = 0; s < b->stages.size(); ++s) {
+            const StageInfo& S = b->stages[s];
+            int64_t* o = out6 + 6 * s;
+            o[0] = S.n; o[1] = S.m_eq; o[2] = S.m_ineq; o[3] = S.nnz_jeq; o[4] = S.nnz_jin; o[5] = S.nnz_h;
+        }
+    });
+}
+
+
+int acopf_batch_set_layout(acopf_batch* b, const int64_t* offsets6, int32_t obj_mode, const int32_t* obj_slot,
+                           int64_t n_coupling, const int64_t* cp_row, const int64_t* cp_jpos, const int64_t* cp_a,
+                           const int64_t* cp_b, const int8_t* cp_base_first) {
+    return guard([&] {
+        if (obj_mode < 0 || obj_mode > 2) throw std::runtime_error("bad objective mode");
+        const int S = (int)b->stages.size();
+        b->off6.assign(offsets6, offsets6 + 6 * (size_t)S);
+        b->obj_slot.assign(obj_slot, obj_slot + S);
+        b->cp_row.assign(cp_row, cp_row + n_coupling);
+        b->cp_jpos.assign(cp_jpos, cp_jpos + n_coupling);
+        b->cp_a.assign(cp_a, cp_a + n_coupling);
+        b->cp_b.assign(cp_b, cp_b + n_coupling);
+        b->cp_first.assign(cp_base_first, cp_base_first + n_coupling);
+        b->obj_mode = obj_mode;
+        b->laid_out = true;
+        b->uploaded = false;
+    });
+}
+
+int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const double* mult, uint32_t what,
+                     double* obj, double* grad, double* cons, double* jval, double* hval, void* stream) {
+    return guard([&] {
+        if (!b->laid_out) throw std::runtime_error("acopf_batch_set_layout was not called");
+        if (!b->uploaded) upload(b);
+        if ((what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD)) && !x) throw std::runtime_error("x is NULL");
+        if ((what & ACOPF_OBJ) && (!obj || !x)) throw std::runtime_error("obj/x is NULL");
+        if ((what & ACOPF_GRAD) && !grad) throw std::runtime_error("grad is NULL");
+        if ((what & ACOPF_CONS) && !cons) throw std::runtime_error("cons is NULL");
+        if ((what & ACOPF_JAC) && !jval) throw std::runtime_error("jval is NULL");
+        if ((what & ACOPF_HESS) && (!hval || !mult)) throw std::runtime_error("hval/mult is NULL");
+        cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
+        EvalParams P = b->params;
+        P.x = x; P.mult = mult; P.obj_factor = obj_factor; P.what = what;
+        P.obj = obj; P.grad = grad; P.cons = cons; P.jval = jval; P.hval = hval;
+        const int grid = P.n_bus_work + P.n_gen_work + P.n_cp_work;
+        if (grid == 0) return;
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
+        acopf_eval_kernel<<<grid, BLOCK, b->smem, st>>>(P);
+        cuda_check(cudaGetLastError(), "acopf_eval_kernel launch");
+        b->launches++;
+    });
+}
+
+int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double obj_factor, const double* mult,
+                          int64_t nm, uint32_t what, double* obj, int64_t nobj, double* grad, int64_t ngrad,
+                          double* cons, int64_t ncons, double* jval, int64_t nj, double* hval, int64_t nh) {
+    return guard([&] {
+        if (!b->laid_out) throw std::runtime_error("acopf_batch_set_layout was not called");
+        cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
+        auto ensure = [&](DevBuf& d, int64_t n) -> double* {
+            size_t bytes = sizeof(double) * (size_t)std::max<int64_t>(n, 1);
+            if (d.n < bytes) {
+                if (d.p) cudaFree(d.p);
+                d.p = nullptr;
+                d.alloc(bytes);
+            }
+            return static_cast<double*>(d.p);
+        };
+        double* dx = ensure(b->h_x, nx);
+        double* dm = ensure(b->h_m, nm);
+        double* dobj = ensure(b->h_obj, nobj);
+        double* dg = ensure(b->h_g, ngrad);
+        double* dc = ensure(b->h_c, ncons);
+        double* dj = ensure(b->h_j, nj);
+        double* dh = ensure(b->h_h, nh);
+        cudaStream_t st = b->stream;
+        if (x && nx) cuda_check(cudaMemcpyAsync(dx, x, 8 * nx, cudaMemcpyHostToDevice, st), "H2D x");
+        if (mult && nm) cuda_check(cudaMemcpyAsync(dm, mult, 8 * nm, cudaMemcpyHostToDevice, st), "H2D mult");
+        if (acopf_batch_eval(b, dx, obj_factor, mult ? dm : nullptr, what, dobj, dg, dc, dj, dh, st) != 0)
+            throw std::runtime_error(g_err);
+        if ((what & ACOPF_OBJ) && obj) cuda_check(cudaMemcpyAsync(obj, dobj, 8 * nobj, cudaMemcpyDeviceToHost, st), "D2H obj");
+        if ((what & ACOPF_GRAD) && grad) cuda_check(cudaMemcpyAsync(grad, dg, 8 * ngrad, cudaMemcpyDeviceToHost, st), "D2H grad");
+        if ((what & ACOPF_CONS) && cons) cuda_check(cudaMemcpyAsync(cons, dc, 8 * ncons, cudaMemcpyDeviceToHost, st), "D2H cons");
+        if ((what & ACOPF_JAC) && jval) cuda_check(cudaMemcpyAsync(jval, dj, 8 * nj, cudaMemcpyDeviceToHost, st), "D2H jac");
+        if ((what & ACOPF_HESS) && hval) cuda_check(cudaMemcpyAsync(hval, dh, 8 * nh, cudaMemcpyDeviceToHost, st), "D2H hess");
+        cuda_check(cudaStreamSynchronize(st), "stream sync");
+    });
+}
+
+// Stage-local pattern rows, in stage row order.
+static void stage_rows(const acopf_batch* b, int s, int which,
+                       std::vector<int64_t>& rowlen, std::vector<int32_t>& cols) {
+    const StageInfo& st = b->stages[s];
+    const Topo& T = *b->topos[st.topo];
+    rowlen.clear();
+    cols.clear();
+    const int ntile = (int)st.table.size();
+    int seg0 = which == 0 ? 0 : 2;
+    for (int seg = seg0; seg < seg0 + 2; ++seg) {
+        for (int t = 0; t < ntile; ++t) {
+            const TileTable& tt = b->tables[st.table[t]];
+            int64_t e0 = 0;
+            for (int q = 0; q < seg; ++q) e0 += tt.L[q];
+            for (int r = 0; r < tt.nB; ++r) {
+                int len = tt.rowlen[seg * tt.nB + r];
+                rowlen.push_back(len);
+                cols.insert(cols.end(), tt.cols.begin() + e0, tt.cols.begin() + e0 + len);
+                e0 += len;
+            }
+        }
+    }
+    if (which == 0) {
+        std::vector<int> c;
+        for (int r = 0; r < T.nr; ++r) {
+            if (std::binary_search(st.removed_rated.begin(), st.removed_rated.end(), r)) continue;
+            flow_row_cols(T, T.rated_branch[r], c);
+            for (int rep = 0; rep < 2; ++rep) {
+                rowlen.push_back((int64_t)c.size());
+                cols.insert(cols.end(), c.begin(), c.end());
+            }
+        }
+    } else {
+        for (int g = 0; g < T.ng; ++g) { rowlen.push_back(1); cols.push_back(2 * T.nb + g); }
+        for (int g = 0; g < T.ng; ++g) rowlen.push_back(0);
+    }
+}
+
+int acopf_batch_pattern(const acopf_batch* b, int32_t stage, int32_t which, int64_t n_rows, int64_t* indptr,
+                        int32_t* indices) {
+    return guard([&] {
+        if (which != 0 && which != 1) throw std::runtime_error("which must be 0 (J) or 1 (H)");
+        std::vector<int64_t> rowlen;
+        std::vector<int32_t> cols;
+        if (stage >= 0) {
+            if (stage >= (int)b->stages.size()) throw std::runtime_error("stage out of range");
+            stage_rows(b, stage, which, rowlen, cols);
+            if ((int64_t)rowlen.size() != n_rows) throw std::runtime_error("n_rows does not match the stage");
+            indptr[0] = 0;
+            for (int64_t r = 0; r < n_rows; ++r) indptr[r + 1] = indptr[r] + rowlen[r];
+            std::copy(cols.begin(), cols.end(), indices);
+            return;
+        }
+        if (!b->laid_out) throw std::runtime_error("acopf_batch_set_layout was not called");
+        // whole laid-out batch: place every row at its offset, then check the rows tile the data
+        std::vector<int64_t> start(n_rows, -1), len(n_rows, 0);
+        for (size_t s = 0; s < b->stages.size(); ++s) {
+            const StageInfo& st = b->stages[s];
+            const int64_t* o = &b->off6[6 * s];
+            stage_rows(b, (int)s, which, rowlen, cols);
+            int64_t pos = 0;
+            for (size_t r = 0; r < rowlen.size(); ++r) {
+                int64_t grow, gstart;
+                if (which == 0) {
+                    bool eq = (int64_t)r < st.m_eq;
+                    grow = eq ? o[1] + (int64_t)r : o[2] + ((int64_t)r - st.m_eq);
+                    gstart = eq ? o[3] + pos : o[4] + (pos - st.nnz_jeq);
+                } else {
+                    grow = o[0] + (int64_t)r;
+                    gstart = o[5] + pos;
+                }
+                if (grow < 0 || grow >= n_rows) throw std::runtime_error("row outside n_rows");
+                start[grow] = gstart;
+                len[grow] = rowlen[r];
+                for (int64_t e = 0; e < rowlen[r]; ++e) indices[gstart + e] = (int32_t)(o[0] + cols[pos + e]);
+                pos += rowlen[r];
+            }
+        }
+        if (which == 0) {
+            for (size_t c = 0; c < b->cp_row.size(); ++c) {
+                int64_t r = b->cp_row[c], p = b->cp_jpos[c];
+                start[r] = p;
+                len[r] = 2;
+                int64_t lo = std::min(b->cp_a[c], b->cp_b[c]), hi = std::max(b->cp_a[c], b->cp_b[c]);
+                indices[p] = (int32_t)lo;
+                indices[p + 1] = (int32_t)hi;
+            }
+        }
+        indptr[0] = 0;
+        for (int64_t r = 0; r < n_rows; ++r) {
+            if (len[r] > 0 && start[r] != indptr[r]) throw std::runtime_error("layout rows are not contiguous in row order");
+            indptr[r + 1] = indptr[r] + len[r];
+        }
+    });
+}
+
+int64_t acopf_batch_launches(const acopf_batch* b) { return b ? b->launches : 0; }
+
+}  // extern "C"

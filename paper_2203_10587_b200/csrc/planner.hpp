@@ -1,0 +1,346 @@
+// Host-side planner: packed topologies, canonical CSR patterns, and the
+// per-tile scatter maps ("term tables") the evaluation kernel executes.
+//
+// What it reproduces (acopf.py:153-195, 308-311,
+// 370-373; composer.py:199-311):
+//
+//  * The reference builds COO triplets in a fixed block order and lets scipy
+//    canonicalise them: coo_tocsr (stable counting sort by row), then
+//    csr_sort_indices (per row std::sort on the column only -- insertion sort
+//    for <= 16 entries, introsort beyond, so NOT stable), then
+//    csr_sum_duplicates (left-to-right sums of equal columns).  The planner
+//    generates each row's COO terms in the reference's order, sorts
+//    (column, term) pairs with the same libstdc++ std::sort and column-only
+//    comparator, and records for every CSR entry the ordered list of terms.
+//    The kernel then sums those terms in exactly that order.
+//  * Row-centric tiles: a tile is a run of consecutive buses; it owns the
+//    J rows P_i, Q_i and the H rows VA_i, VM_i of its buses, which are four
+//    contiguous runs of the CSR value arrays (coalesced stores).
+//  * Contingency stages are "base topology minus removed branches": only the
+//    tiles holding an endpoint of a removed branch get a stage-specific
+//    (patched) table; every other tile reuses the base table at shifted
+//    output offsets.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace acopf {
+
+// per-end quantity slots in the tile's shared-memory array
+constexpr int EQ = 17;          // doubles per branch end
+constexpr int Q_JP = 0;         // 0..3  -dP/d(VA_f, VA_t, VM_f, VM_t) of this end's P row
+constexpr int Q_JQ = 4;         // 4..7  same for the Q row
+constexpr int Q_H = 8;          // 8..14 Hessian values of the 7 positions this end owns
+constexpr int Q_FP = 15;        // P flow at this end (pf or pt)
+constexpr int Q_FQ = 16;        // Q flow at this end (qf or qt)
+constexpr int BQ = 3;           // doubles per bus: shunt J(P,VM), shunt J(Q,VM), shunt H(VM,VM)
+
+// POSITIONS (acopf.py:48-49): (row-axis, col-axis) over (VA_f, VA_t, VM_f, VM_t)
+constexpr int POS_A[10] = {0, 0, 0, 0, 1, 1, 1, 2, 2, 3};
+constexpr int POS_B[10] = {0, 1, 2, 3, 1, 2, 3, 2, 3, 3};
+// which of the 7 Hessian slots of the from (F) / to (T) end holds position p (-1: none)
+constexpr int HSLOT_F[10] = {0, 1, 2, 3, -1, 4, -1, 5, 6, -1};
+constexpr int HSLOT_T[10] = {-1, 0, -1, 1, 2, 3, 4, -1, 5, 6};
+constexpr int POS_OF_SLOT_F[7] = {0, 1, 2, 3, 5, 7, 8};
+constexpr int POS_OF_SLOT_T[7] = {1, 3, 4, 5, 6, 8, 9};
+
+constexpr int TILE_MAX_ENDS = 256;   // soft cap; a single high-degree bus may exceed it
+constexpr int TILE_MAX_BUSES = 128;
+constexpr int SMEM_LIMIT_DOUBLES = (200 * 1024) / 8;
+
+// symbolic term: what a COO entry's value is made of
+struct Sym {
+    int kind;   // 0 = branch end quantity, 1 = bus quantity, 2 = constant 1.0
+    int a;      // end: k*2+side ; bus: bus slot
+    int q;      // quantity slot
+};
+
+struct Row {
+    std::vector<int> cols;      // canonical (sorted, deduplicated) columns
+    std::vector<int> tptr;      // cols.size()+1 offsets into terms
+    std::vector<Sym> terms;     // summation order per entry
+};
+
+// Replays scipy's canonicalisation of one row given its COO terms in order.
+inline void canonicalise(const std::vector<std::pair<int, Sym>>& coo, Row& out) {
+    std::vector<std::pair<int, int>> tmp(coo.size());
+    for (size_t i = 0; i < coo.size(); ++i) tmp[i] = {coo[i].first, (int)i};
+    // same algorithm and comparator as scipy's csr_sort_indices (kv_pair_less)
+    std::sort(tmp.begin(), tmp.end(),
+              [](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+                  return x.first < y.first;
+              });
+    out.cols.clear();
+    out.tptr.assign(1, 0);
+    out.terms.clear();
+    size_t i = 0;
+    while (i < tmp.size()) {
+        int c = tmp[i].first;
+        out.cols.push_back(c);
+        while (i < tmp.size() && tmp[i].first == c) {
+            out.terms.push_back(coo[tmp[i].second].second);
+            ++i;
+        }
+        out.tptr.push_back((int)out.terms.size());
+    }
+}
+
+struct Topo {
+    int nb = 0, nbr = 0, ng = 0, nr = 0;
+    std::vector<int> fo, to;          // bus slots per live branch
+    std::vector<double> adm;          // AoS: gff,bff,gft,bft,gtf,btf,gtt,btt per branch
+    std::vector<int> ridx;            // rated index or -1
+    std::vector<int> rated_branch;    // rated index -> branch
+    std::vector<int> gbus;            // bus slot per live generator
+    std::vector<double> gs, bs;       // per unit shunts
+    // derived
+    std::vector<int> from_ptr, from_list, to_ptr, to_list;
+    std::vector<int> gen_ptr, gen_list;
+    std::vector<int> rowsz;           // Sf+St entries of each rated branch (8, or 4 for a self-loop)
+    std::vector<int64_t> foff;        // base offset of each rated branch's Sf row in the ineq J block
+    std::vector<int> tile_b0;         // tile bus ranges: [tile_b0[t], tile_b0[t+1])
+    std::vector<int> leaf_start, leaf_len;   // numpy pairwise-sum leaves over ng
+
+    void finalize();
+};
+
+inline void pairwise_leaves(int start, int n, std::vector<int>& ls, std::vector<int>& ll) {
+    // numpy pairwise_sum: n <= 128 is one unrolled block, else split at n/2 rounded down to 8
+    if (n <= 128) { ls.push_back(start); ll.push_back(n); return; }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    pairwise_leaves(start, n2, ls, ll);
+    pairwise_leaves(start + n2, n - n2, ls, ll);
+}
+
+inline void Topo::finalize() {
+    from_ptr.assign(nb + 1, 0);
+    to_ptr.assign(nb + 1, 0);
+    for (int k = 0; k < nbr; ++k) { from_ptr[fo[k] + 1]++; to_ptr[to[k] + 1]++; }
+    for (int i = 0; i < nb; ++i) { from_ptr[i + 1] += from_ptr[i]; to_ptr[i + 1] += to_ptr[i]; }
+    from_list.assign(nbr, 0);
+    to_list.assign(nbr, 0);
+    {
+        std::vector<int> pf(from_ptr.begin(), from_ptr.end() - 1), pt(to_ptr.begin(), to_ptr.end() - 1);
+        for (int k = 0; k < nbr; ++k) { from_list[pf[fo[k]]++] = k; to_list[pt[to[k]]++] = k; }
+    }
+    gen_ptr.assign(nb + 1, 0);
+    for (int g = 0; g < ng; ++g) gen_ptr[gbus[g] + 1]++;
+    for (int i = 0; i < nb; ++i) gen_ptr[i + 1] += gen_ptr[i];
+    gen_list.assign(ng, 0);
+    {
+        std::vector<int> p(gen_ptr.begin(), gen_ptr.end() - 1);
+        for (int g = 0; g < ng; ++g) gen_list[p[gbus[g]]++] = g;
+    }
+    rated_branch.clear();
+    for (int k = 0; k < nbr; ++k) if (ridx[k] >= 0) rated_branch.push_back(k);
+    nr = (int)rated_branch.size();
+    rowsz.assign(nr, 8);
+    foff.assign(nr, 0);
+    int64_t acc = 0;
+    for (int r = 0; r < nr; ++r) {
+        int k = rated_branch[r];
+        rowsz[r] = (fo[k] == to[k]) ? 4 : 8;
+        foff[r] = acc;
+        acc += rowsz[r];
+    }
+    // tiles: greedy runs of consecutive buses
+    tile_b0.clear();
+    int i = 0;
+    while (i < nb) {
+        tile_b0.push_back(i);
+        int ends = 0, nbus = 0;
+        while (i < nb) {
+            int d = (from_ptr[i + 1] - from_ptr[i]) + (to_ptr[i + 1] - to_ptr[i]);
+            if (nbus > 0 && (ends + d > TILE_MAX_ENDS || nbus >= TILE_MAX_BUSES)) break;
+            ends += d;
+            nbus++;
+            i++;
+        }
+    }
+    tile_b0.push_back(nb);
+    leaf_start.clear();
+    leaf_len.clear();
+    pairwise_leaves(0, ng, leaf_start, leaf_len);
+}
+
+// Live-branch predicate: base topology minus a sorted list of removed branches.
+struct Live {
+    const std::vector<int>* removed = nullptr;
+    bool operator()(int k) const {
+        return !removed || !std::binary_search(removed->begin(), removed->end(), k);
+    }
+};
+
+// Build the four rows (J P_i, J Q_i, H VA_i, H VM_i) of bus i.
+inline void build_bus_rows(const Topo& T, int i, const Live& live, Row rows[4]) {
+    const int nb = T.nb, ng = T.ng;
+    std::vector<int> F, Tt;
+    for (int p = T.from_ptr[i]; p < T.from_ptr[i + 1]; ++p) if (live(T.from_list[p])) F.push_back(T.from_list[p]);
+    for (int p = T.to_ptr[i]; p < T.to_ptr[i + 1]; ++p) if (live(T.to_list[p])) Tt.push_back(T.to_list[p]);
+    auto axis = [&](int k, int a) {
+        switch (a) {
+            case 0: return T.fo[k];
+            case 1: return T.to[k];
+            case 2: return nb + T.fo[k];
+            default: return nb + T.to[k];
+        }
+    };
+    std::vector<std::pair<int, Sym>> coo;
+    // J row P_i: gpf block, gpt block, shunt P, generator P (acopf.py:164-170)
+    for (int jr = 0; jr < 2; ++jr) {
+        coo.clear();
+        const int qb = jr == 0 ? Q_JP : Q_JQ;
+        for (int k : F) for (int q = 0; q < 4; ++q) coo.push_back({axis(k, q), Sym{0, 2 * k, qb + q}});
+        for (int k : Tt) for (int q = 0; q < 4; ++q) coo.push_back({axis(k, q), Sym{0, 2 * k + 1, qb + q}});
+        coo.push_back({nb + i, Sym{1, i, jr}});
+        for (int p = T.gen_ptr[i]; p < T.gen_ptr[i + 1]; ++p) {
+            int g = T.gen_list[p];
+            coo.push_back({2 * nb + (jr == 0 ? 0 : ng) + g, Sym{2, 0, 0}});
+        }
+        canonicalise(coo, rows[jr]);
+    }
+    // H rows VA_i (axes 0/1) and VM_i (axes 2/3): POSITIONS blocks, mirrored
+    // off-diagonals, then the shunt diagonal on VM rows (acopf.py:182-195)
+    for (int hr = 0; hr < 2; ++hr) {
+        coo.clear();
+        const int axF = hr == 0 ? 0 : 2, axT = hr == 0 ? 1 : 3;
+        for (int p = 0; p < 10; ++p) {
+            const int a = POS_A[p], b = POS_B[p];
+            if (a == axF) for (int k : F) coo.push_back({axis(k, b), Sym{0, 2 * k, Q_H + HSLOT_F[p]}});
+            if (a == axT) for (int k : Tt) coo.push_back({axis(k, b), Sym{0, 2 * k + 1, Q_H + HSLOT_T[p]}});
+            if (a != b) {
+                if (b == axF) for (int k : F) coo.push_back({axis(k, a), Sym{0, 2 * k, Q_H + HSLOT_F[p]}});
+                if (b == axT) for (int k : Tt) coo.push_back({axis(k, a), Sym{0, 2 * k + 1, Q_H + HSLOT_T[p]}});
+            }
+        }
+        if (hr == 1) coo.push_back({nb + i, Sym{1, i, 2}});
+        canonicalise(coo, rows[2 + hr]);
+    }
+}
+
+// Flow rows (Sf, St) of rated branch k: columns (VA_f, VA_t, VM_f, VM_t) sorted.
+inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
+    int f = T.fo[k], t = T.to[k], nb = T.nb;
+    cols.clear();
+    if (f < t) cols = {f, t, nb + f, nb + t};
+    else if (f > t) cols = {t, f, nb + t, nb + f};
+    else cols = {f, nb + f};
+}
+
+// ---------------------------------------------------------------------------
+// Tile tables (serialised into one device blob)
+
+struct TileHdr {            // 64 bytes, all offsets in bytes from the header
+    int32_t b0, nB, nE, nQ;
+    int32_t LP, LQ, LHA, LHV;
+    int32_t nTerms, off_ends, off_busptr, off_eptr;
+    int32_t off_terms, pad0, pad1, pad2;
+};
+static_assert(sizeof(TileHdr) == 64, "TileHdr layout");
+
+struct TileTable {
+    int b0 = 0, nB = 0;
+    std::vector<int> ends;        // k*2+side, per bus: from-ends then to-ends
+    std::vector<int> busptr;      // nB+1
+    int L[4] = {0, 0, 0, 0};      // entries in P, Q, VA, VM segments
+    std::vector<int> cols;        // stage-local column per entry (pattern export)
+    std::vector<int> rowlen;      // entries per row, 4 segments x nB rows
+    std::vector<int> eptr;        // entries+1
+    std::vector<uint16_t> terms;  // shared-memory slot per term
+    int nQ() const { return EQ * (int)ends.size() + BQ * nB + 1; }
+    size_t bytes() const;
+    void serialise(std::vector<uint8_t>& blob) const;
+};
+
+inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+inline size_t TileTable::bytes() const {
+    size_t s = sizeof(TileHdr);
+    s = align16(s + 4 * ends.size());
+    s = align16(s + 4 * busptr.size());
+    s = align16(s + 4 * eptr.size());
+    s = align16(s + 2 * terms.size());
+    return s;
+}
+
+inline void TileTable::serialise(std::vector<uint8_t>& blob) const {
+    size_t base = blob.size();
+    blob.resize(base + bytes(), 0);
+    uint8_t* p = blob.data() + base;
+    TileHdr h{};
+    h.b0 = b0; h.nB = nB; h.nE = (int)ends.size(); h.nQ = nQ();
+    h.LP = L[0]; h.LQ = L[1]; h.LHA = L[2]; h.LHV = L[3];
+    h.nTerms = (int)terms.size();
+    size_t off = sizeof(TileHdr);
+    h.off_ends = (int)off;   off = align16(off + 4 * ends.size());
+    h.off_busptr = (int)off; off = align16(off + 4 * busptr.size());
+    h.off_eptr = (int)off;   off = align16(off + 4 * eptr.size());
+    h.off_terms = (int)off;
+    std::memcpy(p, &h, sizeof h);
+    if (!ends.empty()) std::memcpy(p + h.off_ends, ends.data(), 4 * ends.size());
+    std::memcpy(p + h.off_busptr, busptr.data(), 4 * busptr.size());
+    std::memcpy(p + h.off_eptr, eptr.data(), 4 * eptr.size());
+    if (!terms.empty()) std::memcpy(p + h.off_terms, terms.data(), 2 * terms.size());
+}
+
+inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
+    TileTable tt;
+    const int b0 = T.tile_b0[tile], b1 = T.tile_b0[tile + 1];
+    tt.b0 = b0;
+    tt.nB = b1 - b0;
+    std::vector<Row> rows(4 * tt.nB);
+    std::unordered_map<int, int> end_pos;
+    tt.busptr.push_back(0);
+    for (int i = b0; i < b1; ++i) {
+        for (int p = T.from_ptr[i]; p < T.from_ptr[i + 1]; ++p) {
+            int k = T.from_list[p];
+            if (!live(k)) continue;
+            end_pos[2 * k] = (int)tt.ends.size();
+            tt.ends.push_back(2 * k);
+        }
+        for (int p = T.to_ptr[i]; p < T.to_ptr[i + 1]; ++p) {
+            int k = T.to_list[p];
+            if (!live(k)) continue;
+            end_pos[2 * k + 1] = (int)tt.ends.size();
+            tt.ends.push_back(2 * k + 1);
+        }
+        tt.busptr.push_back((int)tt.ends.size());
+        Row r4[4];
+        build_bus_rows(T, i, live, r4);
+        for (int s = 0; s < 4; ++s) rows[s * tt.nB + (i - b0)] = std::move(r4[s]);
+    }
+    const int nE = (int)tt.ends.size();
+    if (tt.nQ() > SMEM_LIMIT_DOUBLES)
+        throw std::runtime_error("bus degree too high for one tile's shared memory");
+    tt.eptr.push_back(0);
+    for (int s = 0; s < 4; ++s) {
+        for (int r = 0; r < tt.nB; ++r) {
+            const Row& row = rows[s * tt.nB + r];
+            tt.rowlen.push_back((int)row.cols.size());
+            tt.L[s] += (int)row.cols.size();
+            for (size_t e = 0; e < row.cols.size(); ++e) {
+                tt.cols.push_back(row.cols[e]);
+                for (int t = row.tptr[e]; t < row.tptr[e + 1]; ++t) {
+                    const Sym& y = row.terms[t];
+                    int slot;
+                    if (y.kind == 0) slot = EQ * end_pos.at(y.a) + y.q;
+                    else if (y.kind == 1) slot = EQ * nE + BQ * (y.a - b0) + y.q;
+                    else slot = EQ * nE + BQ * tt.nB;
+                    tt.terms.push_back((uint16_t)slot);
+                }
+                tt.eptr.push_back((int)tt.terms.size());
+            }
+        }
+    }
+    return tt;
+}
+
+}  // namespace acopf

@@ -1,0 +1,115 @@
+// Accurate sin/cos for the branch-angle trig of the ACOPF kernels.
+//
+// The reference evaluates np.sin/np.cos (glibc libm, <= 0.52 ulp) on
+// theta = va_f - va_t (acopf.py:233-234).  CUDA's sin/cos are up to 2 ulp,
+// which the 1e-12/1e-14 parity gate does not tolerate on cancellation-heavy
+// Jacobian/Hessian entries (SURVEY.md §7 "Hard parts" #1).  This routine is
+// table-driven double-double: result error ~2^-68 relative before the final
+// rounding, i.e. the correctly rounded value except on ~1e-5 of arguments.
+//
+//   x = k*pi/2 + r        (3-part Cody-Waite, |x| < 2^20)
+//   r = j/64 + d          (|d| <= 1/128, table of sin/cos(j/64) as hi+lo)
+//   sin(j/64 + d) = S cos d + C sin d,  cos(...) = C cos d - S sin d
+//
+// Explicit fma() is used inside this routine (error-free products); the
+// rest of the kernels are built with -fmad=false to keep the reference's
+// rounding sequence.  Header is __host__ __device__ so the CPU tests can
+// exercise the exact same code.
+#pragma once
+#include <math.h>
+#include "sincos_table.h"
+
+#ifdef __CUDACC__
+#define SC_HD __host__ __device__ __forceinline__
+__device__ static const double sc_table_dev[SC_NJ * 4] = {SC_TABLE_VALUES};
+#else
+#define SC_HD static inline
+#endif
+static const double sc_table_host[SC_NJ * 4] = {SC_TABLE_VALUES};
+
+SC_HD void sc_two_sum(double a, double b, double& s, double& e) {
+    s = a + b;
+    double bb = s - a;
+    e = (a - (s - bb)) + (b - bb);
+}
+
+SC_HD void acc_sincos(double x, double* sp, double* cp) {
+    double ax = fabs(x);
+    if (!(ax < 1048576.0)) {          // huge, inf or nan: library path
+#ifdef __CUDA_ARCH__
+        sincos(x, sp, cp);
+#else
+        *sp = sin(x);
+        *cp = cos(x);
+#endif
+        return;
+    }
+    if (ax < 7.450580596923828e-09) {   // 2^-27: sin x -> x, cos x -> 1 (keeps -0.0)
+        *sp = x;
+        *cp = 1.0;
+        return;
+    }
+    double rh = x, rl = 0.0;
+    int q = 0;
+    if (ax > 0.78539816339744828) {
+        double k = rint(x * SC_TWO_OVER_PI);
+        q = ((int)k) & 3;
+        double t1 = x - k * SC_PIO2_1;             // exact
+        double p2 = k * SC_PIO2_2;                  // exact (32-bit constant)
+        double s, e;
+        sc_two_sum(t1, -p2, s, e);
+        double p3h = k * SC_PIO2_3;
+        double p3l = fma(k, SC_PIO2_3, -p3h);
+        double s2, e2;
+        sc_two_sum(s, -p3h, s2, e2);
+        rh = s2;
+        rl = (e + e2) - p3l;
+        double r2, r2e;
+        sc_two_sum(rh, rl, r2, r2e);
+        rh = r2;
+        rl = r2e;
+    }
+    double jf = rint(rh * 64.0);
+    int j = (int)jf;
+    int aj = j < 0 ? -j : j;
+    double dh = rh - jf * 0.015625;                // exact (Sterbenz / j == 0)
+    double dl = rl;
+#ifdef __CUDA_ARCH__
+    const double* tab = sc_table_dev + 4 * aj;
+#else
+    const double* tab = sc_table_host + 4 * aj;
+#endif
+    double S_hi = tab[0], S_lo = tab[1];
+    double C_hi = tab[2], C_lo = tab[3];
+    if (j < 0) { S_hi = -S_hi; S_lo = -S_lo; }
+    double z = dh * dh;
+    // sin d - d  and  cos d - 1, Taylor to d^11 / d^10
+    double ps = fma(z, fma(z, fma(z, fma(z, -2.5052108385441720e-08, 2.7557319223985893e-06),
+                               -1.9841269841269841e-04), 8.3333333333333332e-03),
+                    -1.6666666666666666e-01);
+    double sd_t = fma(dh * z, ps, dl);             // (sin d) - dh
+    double pc = fma(z, fma(z, fma(z, fma(z, -2.7557319223985888e-07, 2.4801587301587302e-05),
+                               -1.3888888888888889e-03), 4.1666666666666664e-02),
+                    -0.5);
+    double cm = fma(z, pc, -(dl * dh));            // (cos d) - 1
+    // sin: S + C*dh + [C*sd_t + S*cm + S_lo + C_lo*dh]
+    double ah = C_hi * dh;
+    double al = fma(C_hi, dh, -ah);
+    double s0, e0;
+    sc_two_sum(S_hi, ah, s0, e0);
+    double ts = e0 + al + S_lo + C_lo * dh + C_hi * sd_t + S_hi * cm;
+    double sn = s0 + ts;
+    // cos: C - S*dh + [-S*sd_t + C*cm + C_lo - S_lo*dh]
+    double bh = S_hi * dh;
+    double bl = fma(S_hi, dh, -bh);
+    double c0, f0;
+    sc_two_sum(C_hi, -bh, c0, f0);
+    double tc = f0 - bl + C_lo - S_lo * dh - S_hi * sd_t + C_hi * cm;
+    double cs = c0 + tc;
+    switch (q) {
+        case 0: *sp = sn;  *cp = cs;  break;
+        case 1: *sp = cs;  *cp = -sn; break;
+        case 2: *sp = -sn; *cp = -cs; break;
+        default: *sp = -cs; *cp = sn; break;
+    }
+}
