@@ -96,12 +96,13 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
                      uint32_t what, double* obj, double* grad, double* cons, double* jval,
                      double* hval, void* stream);
 
-/* Same, host pointers; sizes of the flat buffers in doubles.  Copies in,
- * evaluates and copies out on the handle's stream, then synchronises. */
+/* Same, host pointers (pinned memory gives asynchronous copies); sizes of the
+ * flat buffers in doubles.  Copies in, evaluates and copies out on `stream`
+ * (NULL = the handle's stream), then synchronises that stream. */
 int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double obj_factor,
                           const double* mult, int64_t nm, uint32_t what, double* obj, int64_t nobj,
                           double* grad, int64_t ngrad, double* cons, int64_t ncons, double* jval,
-                          int64_t nj, double* hval, int64_t nh);
+                          int64_t nj, double* hval, int64_t nh, void* stream);
 
 /* CSR pattern of one stage (stage >= 0; rows: that stage's constraints or
  * variables; columns stage-local) or of the whole laid-out batch (stage = -1,
@@ -109,6 +110,13 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
  * indptr has rows+1 entries (int64), indices nnz entries (int32). */
 int acopf_batch_pattern(const acopf_batch* b, int32_t stage, int32_t which, int64_t n_rows,
                         int64_t* indptr, int32_t* indices);
+
+/* Host utility: the order in which one CSR row's COO terms (given by their
+ * columns, in COO order) are visited after scipy's canonicalisation
+ * (csr_sort_indices = std::sort on the column only).  perm[t] = COO index of
+ * the t-th term; equal columns are adjacent and summed left to right.  Used by
+ * the tests to pin the replay against scipy itself. */
+int acopf_canonical_order(int64_t n, const int32_t* cols, int32_t* perm);
 
 /* Kernel launches issued by this handle since creation (evidence counter). */
 int64_t acopf_batch_launches(const acopf_batch* b);

@@ -440,7 +440,8 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
 
 int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double obj_factor, const double* mult,
                           int64_t nm, uint32_t what, double* obj, int64_t nobj, double* grad, int64_t ngrad,
-                          double* cons, int64_t ncons, double* jval, int64_t nj, double* hval, int64_t nh) {
+                          double* cons, int64_t ncons, double* jval, int64_t nj, double* hval, int64_t nh,
+                          void* stream) {
     return guard([&] {
         if (!b->laid_out) throw std::runtime_error("acopf_batch_set_layout was not called");
         cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
@@ -460,7 +461,8 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
         double* dc = ensure(b->h_c, ncons);
         double* dj = ensure(b->h_j, nj);
         double* dh = ensure(b->h_h, nh);
-        cudaStream_t st = b->stream;
+        if (!b->uploaded) upload(b);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
         if (x && nx) cuda_check(cudaMemcpyAsync(dx, x, 8 * nx, cudaMemcpyHostToDevice, st), "H2D x");
         if (mult && nm) cuda_check(cudaMemcpyAsync(dm, mult, 8 * nm, cudaMemcpyHostToDevice, st), "H2D mult");
         if (acopf_batch_eval(b, dx, obj_factor, mult ? dm : nullptr, what, dobj, dg, dc, dj, dh, st) != 0)
@@ -571,5 +573,15 @@ int acopf_batch_pattern(const acopf_batch* b, int32_t stage, int32_t which, int6
 }
 
 int64_t acopf_batch_launches(const acopf_batch* b) { return b ? b->launches : 0; }
+
+int acopf_canonical_order(int64_t n, const int32_t* cols, int32_t* perm) {
+    return guard([&] {
+        std::vector<std::pair<int, Sym>> coo(n);
+        for (int64_t i = 0; i < n; ++i) coo[i] = {cols[i], Sym{0, (int)i, 0}};
+        Row row;
+        canonicalise(coo, row);
+        for (size_t t = 0; t < row.terms.size(); ++t) perm[t] = row.terms[t].a;
+    });
+}
 
 }  // extern "C"

@@ -257,10 +257,11 @@ class BatchEvaluator:
         sz = lambda a: 0 if a is None else len(a)
         L.check(L.lib().acopf_batch_eval_host(
             self._h, vp(x), len(x), float(obj_factor), vp(mult), sz(mult), int(what), vp(o), sz(o),
-            vp(g), sz(g), vp(c), sz(c), vp(j), sz(j), vp(h), sz(h)))
+            vp(g), sz(g), vp(c), sz(c), vp(j), sz(j), vp(h), sz(h), None))
         return out
 
-    def eval_host_ptrs(self, x_ptr: int, mult_ptr: int, obj_factor: float, what: int, outs: dict) -> None:
+    def eval_host_ptrs(self, x_ptr: int, mult_ptr: int, obj_factor: float, what: int, outs: dict,
+                       stream=None) -> None:
         """Host-buffer evaluation on raw pointers (pinned torch tensors in bench.py)."""
         v = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
         n = lambda t: 0 if t is None else t.numel()
@@ -268,7 +269,8 @@ class BatchEvaluator:
             self._h, ctypes.c_void_p(x_ptr), self.n, float(obj_factor), ctypes.c_void_p(mult_ptr),
             self.m if mult_ptr else 0, int(what), v(outs.get("obj")), n(outs.get("obj")),
             v(outs.get("grad")), n(outs.get("grad")), v(outs.get("cons")), n(outs.get("cons")),
-            v(outs.get("jac")), n(outs.get("jac")), v(outs.get("hess")), n(outs.get("hess"))))
+            v(outs.get("jac")), n(outs.get("jac")), v(outs.get("hess")), n(outs.get("hess")),
+            ctypes.c_void_p(stream) if stream else None))
 
     def launches(self) -> int:
         return int(L.lib().acopf_batch_launches(self._h))

@@ -1,0 +1,167 @@
+"""Generate the golden fixtures in this directory from the REAL reference.
+
+Run in the build container (the reference is mounted read-only at
+/root/reference; it does not exist on GPU boxes):
+
+    python tests/golden/make_golden.py
+
+Every fixture is one seeded synthetic input (rebuilt in tests from the
+``spec`` JSON through ``paper_2203_10587_b200.synthetic``) evaluated by the
+reference's own ``build_acopf`` / ``compose_*`` callbacks: objective,
+gradient, constraints, Jacobian and Lagrangian-Hessian CSR, bounds and
+(for composites) offsets and coupling rows.  ``case_digest`` pins the
+generator: a test fails if the synthetic inputs drift.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+from paper_2203_10587_b200 import synthetic as syn  # noqa: E402
+from paper_2203_10587_b200.types import CouplingMode  # noqa: E402
+
+STAGE_SPECS = {
+    "stage_ring9": dict(nb=9, nc=0, ng=3, seed=9, ring=True, features=False, points=3),
+    "stage_feat30": dict(nb=30, nc=10, ng=6, seed=30, ring=False, features=True, points=3),
+    "stage_feat200": dict(nb=200, nc=60, ng=40, seed=200, ring=False, features=True, points=2),
+    "stage_synth2000": dict(nb=2000, nc=600, ng=500, seed=2000, ring=False, features=False, points=1),
+}
+
+COMPOSITE_SPECS = {
+    "scopf_corrective": dict(kind="scopf", nb=60, nc=20, ng=12, n_ctg=6, features=True,
+                             mode=dict(kind="corrective")),
+    "scopf_preventive": dict(kind="scopf", nb=60, nc=20, ng=12, n_ctg=6, features=True,
+                             mode=dict(kind="preventive", pin_voltages=True)),
+    "multiperiod": dict(kind="multiperiod", nb=50, nc=15, ng=10, n_periods=5, dt=15.0),
+    "general": dict(kind="general", nb=80, nc=25, ng=20, n_scen=3, n_ctg=2, n_periods=2, dt=15.0,
+                    mode=dict(kind="preventive")),
+    "sopf_flat": dict(kind="flat", nb=80, nc=25, ng=20, n_scen=3, n_ctg=2,
+                      mode=dict(kind="corrective", contingency_scale=0.5, scenario_scale=2.0)),
+}
+
+
+def case_digest(case) -> str:
+    """Stable hash of every field of a case (pins the synthetic generator)."""
+    h = hashlib.sha256()
+    for b in case.buses:
+        h.update(repr((b.id, b.btype, b.pd, b.qd, b.gs, b.bs, b.vm, b.va, b.vmin, b.vmax)).encode())
+    for g in case.gens:
+        h.update(repr((g.bus, g.status, g.pmin, g.pmax, g.qmin, g.qmax, g.ramp_30, g.cost.c2,
+                       g.cost.c1, g.cost.c0, g.is_wind)).encode())
+    for br in case.branches:
+        h.update(repr((br.fbus, br.tbus, br.r, br.x, br.b, br.rate_a, br.ratio, br.angle,
+                       br.status)).encode())
+    return h.hexdigest()
+
+
+def stage_case(spec):
+    return syn.make_case(spec["nb"], spec["nc"], spec["ng"], seed=spec["seed"], ring=spec["ring"],
+                         features=spec["features"])
+
+
+def composite_inputs(spec):
+    """(kind, args for compose_*, list of base cases) rebuilt from a spec."""
+    kind = spec["kind"]
+    mode = CouplingMode(**spec.get("mode", {}))
+    size = dict(nb=spec["nb"], n_chords=spec["nc"], ng=spec["ng"])
+    if kind == "scopf":
+        base, ctgs = syn.config2_inputs(n_ctg=spec["n_ctg"], features=spec.get("features", False), **size)
+        return dict(base=base, ctgs=ctgs, mode=mode), [base]
+    if kind == "multiperiod":
+        periods = syn.config3_periods(spec["n_periods"], **size)
+        return dict(periods=periods, dt=spec["dt"]), periods
+    base, scens, ctgs = syn.config4_inputs(n_scen=spec["n_scen"], n_ctg=spec["n_ctg"], **size)
+    if kind == "general":
+        return dict(scens=scens, ctgs=ctgs, periods=[base] * spec["n_periods"], mode=mode,
+                    dt=spec["dt"]), [base]
+    return dict(base=base, scens=scens, ctgs=ctgs, mode=mode), [base]
+
+
+def compose(api, kind, a, conv=None):
+    """Call the right compose_* of ``api`` (reference module or this package)."""
+    c = conv or (lambda kind_, v: v)
+    if kind == "scopf":
+        return api.compose_scopf(c("case", a["base"]), c("ctgs", a["ctgs"]), c("mode", a["mode"]))
+    if kind == "multiperiod":
+        return api.compose_multiperiod([c("case", p) for p in a["periods"]], a["dt"])
+    if kind == "general":
+        return api.compose_general(c("scens", a["scens"]), c("ctgs", a["ctgs"]),
+                                   [c("case", p) for p in a["periods"]], c("mode", a["mode"]), a["dt"])
+    return api.compose_sopf_flat(c("case", a["base"]), c("scens", a["scens"]), c("ctgs", a["ctgs"]),
+                                 c("mode", a["mode"]))
+
+
+def variable_kinds_from_layouts(layouts):
+    return syn.variable_kinds([(len(l.va), len(l.pg)) for l in layouts])
+
+
+def dump(path, p, points, extra):
+    out = dict(extra)
+    out["n"], out["m_eq"], out["m_ineq"] = p.n, p.m_eq, p.m_ineq
+    for a in ("xl", "xu", "x0", "gl", "gu"):
+        out[a] = getattr(p, a)
+    for i, (x, mult, of) in enumerate(points):
+        out[f"px{i}"], out[f"pmult{i}"], out[f"pof{i}"] = x, mult, of
+        out[f"obj{i}"] = np.array([p.objective(x)])
+        out[f"grad{i}"] = p.gradient(x)
+        out[f"cons{i}"] = p.constraints(x)
+        J = p.jacobian(x)
+        H = p.lagrangian_hessian(x, of, mult)
+        out[f"jdata{i}"], out[f"hdata{i}"] = J.data, H.data
+        if i == 0:
+            out["jindptr"], out["jindices"] = J.indptr, J.indices
+            out["hindptr"], out["hindices"] = H.indptr, H.indices
+    out["npoints"] = len(points)
+    np.savez_compressed(path, **out)
+
+
+def main():
+    import refbridge as rb
+    ok = rb.opfkit()
+    if ok is None:
+        raise SystemExit("reference not mounted at /root/reference")
+    for name, spec in STAGE_SPECS.items():
+        case = stage_case(spec)
+        p, lay = ok.build_acopf(rb.to_ref_case(case))
+        kinds = syn.variable_kinds([(len(lay.va), len(lay.pg))])
+        pts = []
+        for s in range(spec["points"]):
+            x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 1000 + s)
+            pts.append((x, mult, 1.0 + 0.25 * s))
+        dump(os.path.join(HERE, name + ".npz"), p, pts,
+             dict(spec=json.dumps(spec), case_digest=case_digest(case)))
+        print(name, p.n, p.m_eq + p.m_ineq)
+    conv_map = dict(case=rb.to_ref_case, ctgs=rb.to_ref_ctgs, scens=rb.to_ref_scens, mode=rb.to_ref_mode)
+    for name, spec in COMPOSITE_SPECS.items():
+        a, bases = composite_inputs(spec)
+        p, imap = compose(ok, spec["kind"], a, conv=lambda k, v: conv_map[k](v))
+        kinds = variable_kinds_from_layouts(imap.layouts)
+        pts = []
+        for s in range(2):
+            x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 2000 + s)
+            pts.append((x, mult, 0.5 + s))
+        rows = np.array([[r.stage_a, r.stage_b, -1 if r.gen is None else r.gen,
+                          -1 if r.bus is None else r.bus, r.row, int(r.is_equality)]
+                         for r in imap.coupling_rows], dtype=np.int64).reshape(-1, 6)
+        kinds_s = np.array([r.kind for r in imap.coupling_rows])
+        bounds = np.array([r.bound for r in imap.coupling_rows], dtype=np.float64)
+        dump(os.path.join(HERE, name + ".npz"), p, pts,
+             dict(spec=json.dumps(spec), case_digest=case_digest(bases[0]),
+                  var_offset=np.array(imap.var_offset), eq_offset=np.array(imap.eq_offset),
+                  ineq_offset=np.array(imap.ineq_offset), weights=np.array(imap.weights),
+                  cp_rows=rows, cp_kinds=kinds_s, cp_bounds=bounds))
+        print(name, p.n, p.m_eq + p.m_ineq, len(imap.coupling_rows))
+
+
+if __name__ == "__main__":
+    main()

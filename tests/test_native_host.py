@@ -1,0 +1,130 @@
+"""Native library host side (no GPU): symbols, scipy-order replay, sincos, planner."""
+
+import ctypes
+import os
+import re
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+from scipy.sparse import _sparsetools
+
+import common as C
+from golden.make_golden import STAGE_SPECS, COMPOSITE_SPECS, composite_inputs, compose, stage_case
+import paper_2203_10587_b200 as pkg
+from paper_2203_10587_b200 import _lib as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "acopf_b200.h")
+CSRC = os.path.join(ROOT, "paper_2203_10587_b200", "csrc")
+
+
+def test_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(L.LIB_PATH)
+    names = set(re.findall(r"\b(acopf_\w+)\s*\(", open(HEADER).read()))
+    assert len(names) >= 12
+    for n in sorted(names):
+        assert hasattr(lib, n), n
+    assert L.lib().acopf_version() == 1
+
+
+def _scipy_order(cols):
+    """Term order scipy's csr_sort_indices gives one row (payload replay)."""
+    n = len(cols)
+    indptr = np.array([0, n], dtype=np.int32)
+    idx = np.asarray(cols, dtype=np.int32).copy()
+    payload = np.arange(n, dtype=np.float64)
+    _sparsetools.csr_sort_indices(1, indptr, idx, payload)
+    return payload.astype(np.int32)
+
+
+def _ours(cols):
+    cols = np.ascontiguousarray(cols, dtype=np.int32)
+    perm = np.zeros(len(cols), dtype=np.int32)
+    L.check(L.lib().acopf_canonical_order(len(cols), L.ptr(cols, ctypes.c_int32), L.ptr(perm, ctypes.c_int32)))
+    return perm
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_canonical_order_replays_scipy(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 80))
+    cols = rng.integers(0, max(2, n // 3), size=n)
+    assert np.array_equal(_ours(cols), _scipy_order(cols))
+
+
+def test_canonical_order_real_rows_longer_than_16():
+    """Rows above the insertion-sort threshold (introsort: not stable)."""
+    rng = np.random.default_rng(1)
+    for n in (17, 24, 33, 64, 200, 1000):
+        cols = np.repeat(rng.integers(0, 6, size=n // 3 + 1), 3)[:n]
+        assert np.array_equal(_ours(cols), _scipy_order(cols))
+
+
+@pytest.fixture(scope="module")
+def sincos_bin():
+    d = tempfile.mkdtemp()
+    src = os.path.join(d, "t.cpp")
+    with open(src, "w") as fh:
+        fh.write('#include <cstdio>\n#include <cstdlib>\n#include "sincos.cuh"\n'
+                 'int main(){size_t n; if(fread(&n,8,1,stdin)!=1) return 1; double* x=(double*)malloc(8*n);'
+                 'if(fread(x,8,n,stdin)!=n) return 1; double* o=(double*)malloc(16*n);'
+                 'for(size_t i=0;i<n;i++) acc_sincos(x[i],&o[2*i],&o[2*i+1]); fwrite(o,16,n,stdout); return 0;}\n')
+    exe = os.path.join(d, "t")
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-I", CSRC, src, "-o", exe], check=True)
+    return exe
+
+
+def test_accurate_sincos_vs_libm(sincos_bin):
+    """Device sincos (same source, host build) is within 1 ulp of libm and equal on >99.5%."""
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([rng.uniform(-0.6, 0.6, 200000), rng.uniform(-4, 4, 50000),
+                         rng.uniform(-1e4, 1e4, 5000), [0.0, -0.0, 1e-300, -3e-9, np.pi / 4]])
+    inp = np.array([len(xs)], dtype=np.uint64).tobytes() + xs.tobytes()
+    out = np.frombuffer(subprocess.run([sincos_bin], input=inp, capture_output=True, check=True).stdout)
+    s, c = out[0::2], out[1::2]
+    ns, nc = np.sin(xs), np.cos(xs)
+    ulp = lambda a, b: np.abs(a.view(np.int64) - b.view(np.int64))
+    assert ulp(s, ns).max() <= 1 and ulp(c, nc).max() <= 1
+    assert np.count_nonzero(s != ns) < 0.005 * len(xs)
+    assert np.count_nonzero(c != nc) < 0.005 * len(xs)
+    assert np.signbit(s[len(xs) - 4])      # sin(-0.0) = -0.0
+
+
+@pytest.mark.parametrize("name", C.STAGE_FIXTURES)
+def test_stage_structure_matches_golden(name):
+    """Patterns, bounds and sizes of build_acopf (planner only, no GPU)."""
+    g = C.load(name)
+    p, lay = pkg.build_acopf(stage_case(STAGE_SPECS[name]))
+    assert (p.n, p.m_eq, p.m_ineq) == (int(g["n"]), int(g["m_eq"]), int(g["m_ineq"]))
+    for a in ("xl", "xu", "x0", "gl", "gu"):
+        assert C.bit_diffs(getattr(p, a), g[a]) == 0, a
+    ip, ix = p.evaluator.pattern("J")
+    assert np.array_equal(ip, g["jindptr"]) and np.array_equal(ix, g["jindices"])
+    ip, ix = p.evaluator.pattern("H")
+    assert np.array_equal(ip, g["hindptr"]) and np.array_equal(ix, g["hindices"])
+
+
+@pytest.mark.parametrize("name", C.COMPOSITE_FIXTURES)
+def test_composite_structure_matches_golden(name):
+    g = C.load(name)
+    spec = COMPOSITE_SPECS[name]
+    a, _ = composite_inputs(spec)
+    p, imap = compose(pkg, spec["kind"], a)
+    assert (p.n, p.m_eq, p.m_ineq) == (int(g["n"]), int(g["m_eq"]), int(g["m_ineq"]))
+    for k in ("xl", "xu", "x0", "gl", "gu"):
+        assert C.bit_diffs(getattr(p, k), g[k]) == 0, k
+    assert list(imap.var_offset) == list(g["var_offset"])
+    assert list(imap.eq_offset) == list(g["eq_offset"])
+    assert list(imap.ineq_offset) == list(g["ineq_offset"])
+    assert np.array_equal(np.array(imap.weights), g["weights"])
+    rows = np.array([[r.stage_a, r.stage_b, -1 if r.gen is None else r.gen, -1 if r.bus is None else r.bus,
+                      r.row, int(r.is_equality)] for r in imap.coupling_rows], dtype=np.int64).reshape(-1, 6)
+    assert np.array_equal(rows, g["cp_rows"])
+    assert [r.kind for r in imap.coupling_rows] == list(g["cp_kinds"])
+    assert C.bit_diffs([r.bound for r in imap.coupling_rows], g["cp_bounds"]) == 0
+    ip, ix = p.evaluator.pattern("J")
+    assert np.array_equal(ip, g["jindptr"]) and np.array_equal(ix, g["jindices"])
+    ip, ix = p.evaluator.pattern("H")
+    assert np.array_equal(ip, g["hindptr"]) and np.array_equal(ix, g["hindices"])
