@@ -268,7 +268,9 @@ def main():
     x = torch.from_numpy(x_h).to(dev)
     mult = torch.from_numpy(m_h).to(dev)
     out = ev.alloc()
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream: the kernels, the events and the copies all live on it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     from paper_2203_10587_b200 import _lib as L

@@ -99,11 +99,11 @@ struct acopf_batch {
     int obj_mode = 0, n_obj = 0;
     // device
     cudaStream_t stream = nullptr;
-    DevBuf d_topo, d_stage, d_work, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
+    DevBuf d_topo, d_stage, d_items, d_recs, d_aux, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
     DevBuf d_cprow, d_cpj, d_cpa, d_cpb, d_cpf, d_objterms, d_counter;
     std::vector<std::unique_ptr<DevBuf>> topo_bufs;
     EvalParams params{};
-    size_t smem = 0;
+    size_t smem = 0, aux_smem = 0;
     int64_t launches = 0;
     // host staging for eval_host
     DevBuf h_x, h_m, h_obj, h_g, h_c, h_j, h_h;
@@ -113,125 +113,142 @@ struct acopf_batch {
     }
 };
 
+// Upload everything the kernels read and build the work lists.
 static void upload(acopf_batch* b) {
-        cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
-        const int S = (int)b->stages.size();
-        const int64_t n_coupling = (int64_t)b->cp_row.size();
-        const int obj_mode = b->obj_mode;
-        if (!b->stream) cuda_check(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
+    const int S = (int)b->stages.size();
+    const int64_t n_coupling = (int64_t)b->cp_row.size();
+    if (!b->stream) cuda_check(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "stream");
 
-        // topologies
-        std::vector<DTopo> dt;
-        b->topo_bufs.clear();
-        for (const Topo* T : b->topos) {
-            DTopo d{};
-            d.nb = T->nb; d.nbr = T->nbr; d.ng = T->ng; d.nr = T->nr;
-            auto up = [&](const auto& v) {
-                b->topo_bufs.emplace_back(new DevBuf());
-                return b->topo_bufs.back()->upload(v);
-            };
-            d.fo = up(T->fo); d.to = up(T->to); d.adm = up(T->adm); d.ridx = up(T->ridx);
-            d.gs = up(T->gs); d.bs = up(T->bs); d.gen_ptr = up(T->gen_ptr); d.gen_list = up(T->gen_list);
-            std::vector<long long> foff(T->foff.begin(), T->foff.end());
-            d.foff = up(foff);
-            d.rowsz = up(T->rowsz);
-            std::vector<int> leaf;
-            for (size_t l = 0; l < T->leaf_start.size(); ++l) { leaf.push_back(T->leaf_start[l]); leaf.push_back(T->leaf_len[l]); }
-            d.leaf = up(leaf);
-            d.nleaf = (int)T->leaf_start.size();
-            dt.push_back(d);
-        }
-        // blob of tile tables
-        std::vector<uint8_t> blob;
-        std::vector<int64_t> table_off(b->tables.size());
-        size_t max_q = 64;
-        for (size_t i = 0; i < b->tables.size(); ++i) {
-            table_off[i] = (int64_t)blob.size();
-            b->tables[i].serialise(blob);
-            max_q = std::max(max_q, (size_t)b->tables[i].nQ());
-        }
-        // stages, removed lists, work items (bus tiles first, stage-major)
-        std::vector<DStage> ds(S);
-        std::vector<int> rem, remsz;
-        std::vector<DWork> work;
-        int n_obj = 0;
-        for (int s = 0; s < S; ++s) {
-            const StageInfo& st = b->stages[s];
-            const Topo& T = *b->topos[st.topo];
-            DStage& d = ds[s];
-            const int64_t* o = &b->off6[6 * s];
-            d.var_off = o[0]; d.eq_row = o[1]; d.ineq_row = o[2];
-            d.jeq_base = o[3]; d.jineq_base = o[4]; d.h_base = o[5];
-            d.hpg_local = st.hpg_local;
-            d.pd_off = st.pd_off;
-            d.cost_off = st.cost_off;
-            d.rem_off = (long long)rem.size();
-            d.nrem = (int)st.removed_rated.size();
-            rem.insert(rem.end(), st.removed_rated.begin(), st.removed_rated.end());
-            remsz.insert(remsz.end(), st.removed_rowsz.begin(), st.removed_rowsz.end());
-            d.topo = st.topo;
-            d.obj_slot = b->obj_slot[s];
-            d.w = st.w;
-            max_q = std::max(max_q, T.leaf_start.size());
-            for (size_t t = 0; t < st.table.size(); ++t) {
-                DWork w{};
-                w.stage = s;
-                w.blob_off = table_off[st.table[t]];
-                w.jP = st.tile_off[4 * t + 0]; w.jQ = st.tile_off[4 * t + 1];
-                w.hA = st.tile_off[4 * t + 2]; w.hV = st.tile_off[4 * t + 3];
-                work.push_back(w);
+    // topologies (only what the aux kernel needs; the bus kernel reads tile tables)
+    std::vector<DTopo> dt;
+    b->topo_bufs.clear();
+    size_t max_leaf = 1;
+    for (const Topo* T : b->topos) {
+        DTopo d{};
+        d.nb = T->nb; d.nbr = T->nbr; d.ng = T->ng; d.nr = T->nr;
+        std::vector<int> leaf;
+        for (size_t l = 0; l < T->leaf_start.size(); ++l) { leaf.push_back(T->leaf_start[l]); leaf.push_back(T->leaf_len[l]); }
+        b->topo_bufs.emplace_back(new DevBuf());
+        d.leaf = b->topo_bufs.back()->upload(leaf);
+        d.nleaf = (int)T->leaf_start.size();
+        max_leaf = std::max(max_leaf, T->leaf_start.size());
+        dt.push_back(d);
+    }
+    // blob of tile tables (each 16-byte aligned, sized for one bulk copy)
+    std::vector<uint8_t> blob;
+    std::vector<int64_t> table_off(b->tables.size());
+    std::vector<int> table_bytes(b->tables.size());
+    size_t max_smem = 0;
+    for (size_t i = 0; i < b->tables.size(); ++i) {
+        table_off[i] = (int64_t)blob.size();
+        b->tables[i].serialise(*b->topos[b->tables[i].topo], blob);
+        table_bytes[i] = (int)(blob.size() - table_off[i]);
+        max_smem = std::max(max_smem, (size_t)table_bytes[i] + 8 * (size_t)b->tables[i].nQ());
+    }
+    if (max_smem > (size_t)SMEM_LIMIT_BYTES) throw std::runtime_error("tile table exceeds shared memory");
+    // stages and removed lists
+    std::vector<DStage> ds(S);
+    std::vector<int> rem, remsz;
+    for (int s = 0; s < S; ++s) {
+        const StageInfo& st = b->stages[s];
+        DStage& d = ds[s];
+        const int64_t* o = &b->off6[6 * s];
+        d.var_off = o[0]; d.eq_row = o[1]; d.ineq_row = o[2];
+        d.jeq_base = o[3]; d.jineq_base = o[4]; d.h_base = o[5];
+        d.hpg_local = st.hpg_local;
+        d.pd_off = st.pd_off;
+        d.cost_off = st.cost_off;
+        d.rem_off = (long long)rem.size();
+        d.nrem = (int)st.removed_rated.size();
+        rem.insert(rem.end(), st.removed_rated.begin(), st.removed_rated.end());
+        remsz.insert(remsz.end(), st.removed_rowsz.begin(), st.removed_rowsz.end());
+        d.topo = st.topo;
+        d.obj_slot = b->obj_slot[s];
+        d.w = st.w;
+    }
+    // bus work: for every tile, the stages sharing one table, in chunks of G
+    int64_t total_recs = 0;
+    for (const StageInfo& st : b->stages) total_recs += (int64_t)st.table.size();
+    const int64_t target_items = 148 * 2 * 6;
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(32, total_recs / target_items));
+    std::vector<DBusItem> items;
+    std::vector<DBusRec> recs;
+    std::map<int, std::vector<int>> by_table;     // table id -> stages (in order)
+    std::vector<std::pair<int, int>> tiles;       // (topo, tile)
+    for (size_t ti = 0; ti < b->topos.size(); ++ti)
+        for (size_t t = 0; t < b->base_table[ti].size(); ++t) tiles.push_back({(int)ti, (int)t});
+    for (auto [topo, t] : tiles) {
+        by_table.clear();
+        for (int s = 0; s < S; ++s)
+            if (b->stages[s].topo == topo) by_table[b->stages[s].table[t]].push_back(s);
+        for (auto& kv : by_table) {
+            const std::vector<int>& ss = kv.second;
+            for (size_t c = 0; c < ss.size(); c += G) {
+                DBusItem it{};
+                it.blob_off = table_off[kv.first];
+                it.bytes = table_bytes[kv.first];
+                it.first = (int)recs.size();
+                it.count = (int)std::min<size_t>(G, ss.size() - c);
+                for (size_t j = c; j < c + it.count; ++j) {
+                    const StageInfo& st = b->stages[ss[j]];
+                    DBusRec r{};
+                    r.stage = ss[j];
+                    r.jP = st.tile_off[4 * t + 0]; r.jQ = st.tile_off[4 * t + 1];
+                    r.hA = st.tile_off[4 * t + 2]; r.hV = st.tile_off[4 * t + 3];
+                    recs.push_back(r);
+                }
+                items.push_back(it);
             }
         }
-        const int n_bus = (int)work.size();
-        for (int s = 0; s < S; ++s) {
-            const Topo& T = *b->topos[b->stages[s].topo];
-            int nch = std::max(1, (T.ng + GEN_CHUNK - 1) / GEN_CHUNK);
-            for (int c = 0; c < nch; ++c) {
-                DWork w{};
-                w.stage = s;
-                w.jP = c;
-                work.push_back(w);
-            }
-            n_obj++;
-        }
-        const int n_gen = (int)work.size() - n_bus;
-        const int n_cp = (int)((n_coupling + CP_CHUNK - 1) / CP_CHUNK);
-        b->n_obj = n_obj;
+    }
+    // aux work: generator chunks per stage, then coupling chunks
+    std::vector<DAuxItem> aux;
+    for (int s = 0; s < S; ++s) {
+        const Topo& T = *b->topos[b->stages[s].topo];
+        int nch = std::max(1, (T.ng + GEN_CHUNK - 1) / GEN_CHUNK);
+        for (int c = 0; c < nch; ++c) aux.push_back(DAuxItem{0, s, c, 0});
+    }
+    const int n_cp = (int)((n_coupling + CP_CHUNK - 1) / CP_CHUNK);
+    for (int c = 0; c < n_cp; ++c) aux.push_back(DAuxItem{1, 0, c, 0});
+    b->n_obj = S;
 
-        EvalParams& P = b->params;
-        P = EvalParams{};
-        P.topos = b->d_topo.upload(dt);
-        P.stages = b->d_stage.upload(ds);
-        P.work = b->d_work.upload(work);
-        P.blob = b->d_blob.upload(blob);
-        P.pd = b->d_pd.upload(b->pd);
-        P.qd = b->d_qd.upload(b->qd);
-        P.ca = b->d_ca.upload(b->ca);
-        P.cb = b->d_cb.upload(b->cb);
-        P.cc = b->d_cc.upload(b->cc);
-        P.rem_ridx = b->d_rem.upload(rem);
-        P.rem_rowsz = b->d_remsz.upload(remsz);
-        P.cp_row = reinterpret_cast<const long long*>(b->d_cprow.upload(b->cp_row));
-        P.cp_jpos = reinterpret_cast<const long long*>(b->d_cpj.upload(b->cp_jpos));
-        P.cp_a = reinterpret_cast<const long long*>(b->d_cpa.upload(b->cp_a));
-        P.cp_b = reinterpret_cast<const long long*>(b->d_cpb.upload(b->cp_b));
-        P.cp_base_first = reinterpret_cast<const signed char*>(b->d_cpf.upload(b->cp_first));
-        P.ncp = n_coupling;
-        P.n_bus_work = n_bus;
-        P.n_gen_work = n_gen;
-        P.n_cp_work = n_cp;
-        P.n_obj = n_obj;
-        P.obj_mode = obj_mode;
-        P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
-        P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
-        b->smem = sizeof(double) * max_q;
-        if (b->smem > 48 * 1024)
-            cuda_check(cudaFuncSetAttribute(acopf_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)b->smem), "cudaFuncSetAttribute");
-        b->uploaded = true;
+    EvalParams& P = b->params;
+    P = EvalParams{};
+    P.topos = b->d_topo.upload(dt);
+    P.stages = b->d_stage.upload(ds);
+    P.bus_items = b->d_items.upload(items);
+    P.bus_recs = b->d_recs.upload(recs);
+    P.aux_items = b->d_aux.upload(aux);
+    P.blob = b->d_blob.upload(blob);
+    P.pd = b->d_pd.upload(b->pd);
+    P.qd = b->d_qd.upload(b->qd);
+    P.ca = b->d_ca.upload(b->ca);
+    P.cb = b->d_cb.upload(b->cb);
+    P.cc = b->d_cc.upload(b->cc);
+    P.rem_ridx = b->d_rem.upload(rem);
+    P.rem_rowsz = b->d_remsz.upload(remsz);
+    P.cp_row = reinterpret_cast<const long long*>(b->d_cprow.upload(b->cp_row));
+    P.cp_jpos = reinterpret_cast<const long long*>(b->d_cpj.upload(b->cp_jpos));
+    P.cp_a = reinterpret_cast<const long long*>(b->d_cpa.upload(b->cp_a));
+    P.cp_b = reinterpret_cast<const long long*>(b->d_cpb.upload(b->cp_b));
+    P.cp_base_first = reinterpret_cast<const signed char*>(b->d_cpf.upload(b->cp_first));
+    P.ncp = n_coupling;
+    P.n_bus_items = (int)items.size();
+    P.n_aux_items = (int)aux.size();
+    P.n_obj = S;
+    P.obj_mode = b->obj_mode;
+    P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
+    P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
+    b->smem = (max_smem + 127) & ~size_t(127);
+    b->aux_smem = sizeof(double) * max_leaf;
+    cuda_check(cudaFuncSetAttribute(acopf_bus_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(bus)");
+    if (b->aux_smem > 48 * 1024)
+        cuda_check(cudaFuncSetAttribute(acopf_aux_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)b->aux_smem), "cudaFuncSetAttribute(aux)");
+    b->uploaded = true;
 }
-
-
 
 extern "C" {
 
@@ -286,6 +303,7 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
             std::vector<int> ids;
             for (size_t t = 0; t + 1 < T.tile_b0.size(); ++t) {
                 B->tables.push_back(build_tile(T, (int)t, Live{}));
+                B->tables.back().topo = i;
                 ids.push_back((int)B->tables.size() - 1);
             }
             B->base_table.push_back(ids);
@@ -339,6 +357,7 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
                 auto it = B->patch_cache.find(key);
                 if (it == B->patch_cache.end()) {
                     B->tables.push_back(build_tile(T, t, Live{&S.removed}));
+                    B->tables.back().topo = S.topo;
                     it = B->patch_cache.emplace(key, (int)B->tables.size() - 1).first;
                 }
                 S.table[t] = it->second;
@@ -429,12 +448,19 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         EvalParams P = b->params;
         P.x = x; P.mult = mult; P.obj_factor = obj_factor; P.what = what;
         P.obj = obj; P.grad = grad; P.cons = cons; P.jval = jval; P.hval = hval;
-        const int grid = P.n_bus_work + P.n_gen_work + P.n_cp_work;
-        if (grid == 0) return;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
-        acopf_eval_kernel<<<grid, BLOCK, b->smem, st>>>(P);
-        cuda_check(cudaGetLastError(), "acopf_eval_kernel launch");
-        b->launches++;
+        const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD)) && P.n_bus_items > 0;
+        const bool aux = (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
+        if (aux) {
+            acopf_aux_kernel<<<P.n_aux_items, BLOCK, b->aux_smem, st>>>(P);
+            cuda_check(cudaGetLastError(), "acopf_aux_kernel launch");
+            b->launches++;
+        }
+        if (bus) {
+            acopf_bus_kernel<<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
+            cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
+            b->launches++;
+        }
     });
 }
 

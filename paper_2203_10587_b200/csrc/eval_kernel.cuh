@@ -1,27 +1,31 @@
-// Fused ACOPF callback evaluation kernel for sm_100a (fp64, no atomics on
-// values, built with -fmad=false so every expression rounds exactly like
-// the reference's numpy evaluation).
+// Fused ACOPF callback evaluation kernels for sm_100a (fp64, no floating
+// atomics, built with -fmad=false so every expression rounds exactly like the
+// reference's numpy evaluation).
 //
-// One CTA = one work item:
-//   * bus tile (stage s, buses [b0,b1)): phase A computes, per incident
-//     branch end, the flows, their 16 partials and the 7 Hessian positions
-//     the end owns (acopf.py:230-250, 313-369) into shared memory; rated
-//     ends also emit their |S|^2 row value and its 4 Jacobian entries.
-//     Phase A2 fills bus-level shunt terms and, in the order np.add.at
-//     uses, the P/Q balance rows (acopf.py:252-288).  Phase B walks the
-//     tile's scatter map: every CSR value of the tile's J rows P_i/Q_i and
-//     H rows VA_i/VM_i is the ordered sum of its terms (scipy's duplicate
-//     order, planner.hpp), stored contiguously.
-//   * generator chunk (stage s, 256 generators): gradient, PG Hessian
-//     diagonal, and (chunk 0) the stage objective by numpy's pairwise sum;
-//     the last objective CTA sums the weighted stage objectives in stage
-//     order (composer.py:256-258).
-//   * coupling chunk: child - base values and the +-1 Jacobian entries
-//     (composer.py:229-242, 274-276).
+// acopf_bus_kernel -- one CTA = (tile of consecutive buses, group of stages
+// that share the tile's table):
+//   0. one thread issues a cp.async.bulk (TMA bulk copy) of the tile's whole
+//      table -- per-end bus slots / rated index / flow-row offset, SoA branch
+//      admittances, per-bus shunts and generator lists, the scatter map --
+//      into shared memory, completing on an mbarrier;
+//   then for every stage of the group:
+//   A. per branch end: flows, their 16 partials and the 7 Hessian positions
+//      this end owns (acopf.py:230-250, 313-369) into shared memory; rated
+//      ends also store their |S|^2 row value and its Jacobian entries;
+//   A2. per bus: shunt terms (acopf.py:262-263, 296-297, 366);
+//   B. per bus: P/Q balance rows in np.add.at order (acopf.py:252-288); per
+//      CSR entry of the tile's J rows P_i/Q_i and H rows VA_i/VM_i: the
+//      ordered sum of its terms (scipy's duplicate order, planner.hpp),
+//      stored to four contiguous runs (coalesced).
+//
+// acopf_aux_kernel -- generator chunks (gradient, PG Hessian diagonal, the
+// stage objective by numpy's pairwise sum, the weighted composite sum in
+// stage order, composer.py:256-258) and coupling-row chunks (child - base
+// values and +-1 Jacobian entries, composer.py:229-242, 274-276).
 #pragma once
 #include <cstdint>
-#include "sincos.cuh"
 #include "planner.hpp"
+#include "sincos.cuh"
 
 namespace acopf {
 
@@ -29,17 +33,7 @@ enum : unsigned { W_OBJ = 1u, W_GRAD = 2u, W_CONS = 4u, W_JAC = 8u, W_HESS = 16u
 
 struct DTopo {
     int nb, nbr, ng, nr;
-    const int* fo;
-    const int* to;
-    const double* adm;        // 8 per branch (AoS)
-    const int* ridx;
-    const double* gs;
-    const double* bs;
-    const int* gen_ptr;
-    const int* gen_list;
-    const long long* foff;
-    const int* rowsz;
-    const int* leaf;          // (start, len) pairs
+    const int* leaf;          // (start, len) pairs of the pairwise sum over ng
     int nleaf;
     int pad;
 };
@@ -51,20 +45,26 @@ struct DStage {
     double w;
 };
 
-struct DWork {
-    int stage, pad;
+struct DBusItem {             // one CTA of the bus kernel
     long long blob_off;
-    int jP, jQ, hA, hV;
+    int bytes, first, count, pad;
 };
 
-struct TileHdrD {
-    int b0, nB, nE, nQ, LP, LQ, LHA, LHV, nTerms, off_ends, off_busptr, off_eptr, off_terms, p0, p1, p2;
+struct DBusRec {              // (stage, tile) output offsets, stage-local
+    int stage, jP, jQ, hA, hV, pad;
+};
+
+struct DAuxItem {
+    int kind;                 // 0 generator chunk, 1 coupling chunk
+    int stage, chunk, pad;
 };
 
 struct EvalParams {
     const DTopo* topos;
     const DStage* stages;
-    const DWork* work;
+    const DBusItem* bus_items;
+    const DBusRec* bus_recs;
+    const DAuxItem* aux_items;
     const unsigned char* blob;
     const double* pd;
     const double* qd;
@@ -79,9 +79,9 @@ struct EvalParams {
     const long long* cp_b;
     const signed char* cp_base_first;
     long long ncp;
-    int n_bus_work, n_gen_work, n_cp_work;
+    int n_bus_items, n_aux_items;
     int n_obj;                // objective stages (chunk-0 generator items)
-    int obj_mode;             // 0: per-stage f_s into obj[slot]; 1: weighted sum into obj[0]; 2: weighted terms only
+    int obj_mode;             // 0: f_s into obj[slot]; 1: weighted sum into obj[0]; 2: weighted terms only
     const double* x;
     const double* mult;
     double obj_factor;
@@ -96,26 +96,41 @@ struct EvalParams {
 };
 
 constexpr int BLOCK = 256;
+constexpr int GEN_CHUNK = 256;
+constexpr int CP_CHUNK = 1024;
 
 // POSITIONS (acopf.py:48-49) and the end-slot -> position maps of planner.hpp,
 // as constexpr functions so unrolled device loops fold them to constants.
 __host__ __device__ constexpr int pos_a(int p) { return p < 4 ? 0 : (p < 7 ? 1 : (p < 9 ? 2 : 3)); }
 __host__ __device__ constexpr int pos_b(int p) { return p < 4 ? p : (p < 7 ? p - 3 : (p < 9 ? p - 5 : 3)); }
 __host__ __device__ constexpr int slot_pos_f(int s) { return s < 4 ? s : (s == 4 ? 5 : (s == 5 ? 7 : 8)); }
-__host__ __device__ constexpr int slot_pos_t(int s) { return s == 0 ? 1 : (s == 1 ? 3 : (s <= 4 ? s + 2 : (s == 5 ? 8 : 9))); }
-constexpr int GEN_CHUNK = 256;
-constexpr int CP_CHUNK = 1024;
-
-// Stage-local rated index and Sf-row offset after removing rated branches.
-__device__ __forceinline__ void stage_rated(const EvalParams& P, const DStage& S, const DTopo& T,
-                                            int r, int& rs, long long& off) {
-    rs = r;
-    off = T.foff[r];
-    for (int i = 0; i < S.nrem; ++i) {
-        int q = P.rem_ridx[S.rem_off + i];
-        if (q < r) { rs--; off -= P.rem_rowsz[S.rem_off + i]; }
-    }
+__host__ __device__ constexpr int slot_pos_t(int s) {
+    return s == 0 ? 1 : (s == 1 ? 3 : (s <= 4 ? s + 2 : (s == 5 ? 8 : 9)));
 }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// ---------------------------------------------------------------------------
+// bus kernel
+
+struct TileView {
+    TileHdr h;
+    const int* code;
+    const int* f;
+    const int* t;
+    const int* ridx;
+    const int* foff;
+    const int* busptr;
+    const int* gptr;
+    const int* glist;
+    const double* gs;
+    const double* bs;
+    const double* adm;
+    const int* eptr;
+    const unsigned short* terms;
+};
 
 __device__ __forceinline__ double hpos(int p, double cpf, double cqf, double cpt, double cqt,
                                        double s2f, double s2t, const double* gpf, const double* gqf,
@@ -130,177 +145,222 @@ __device__ __forceinline__ double hpos(int p, double cpf, double cqf, double cpt
     return v;
 }
 
-__device__ void bus_tile(const EvalParams& P, const DWork& W, double* Q) {
-    const DStage S = P.stages[W.stage];
-    const DTopo T = P.topos[S.topo];
-    const unsigned char* base = P.blob + W.blob_off;
-    const TileHdrD H = *reinterpret_cast<const TileHdrD*>(base);
-    const int* ends = reinterpret_cast<const int*>(base + H.off_ends);
-    const int* busptr = reinterpret_cast<const int*>(base + H.off_busptr);
-    const int* eptr = reinterpret_cast<const int*>(base + H.off_eptr);
-    const unsigned short* terms = reinterpret_cast<const unsigned short*>(base + H.off_terms);
-    const int nb = T.nb;
+// Phase A for one branch end of one stage.
+__device__ __forceinline__ void branch_end(const EvalParams& P, const DStage& S, int nb, const TileView& V,
+                                           int e, double* Q, bool need_j, bool need_h, bool need_c) {
     const double* va = P.x + S.var_off;
     const double* vm = va + nb;
-    const double* mu = P.mult + S.eq_row;
-    const double* mi = P.mult + S.ineq_row;
-    const unsigned what = P.what;
-    const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
-
-    // ---- phase A: branch ends -------------------------------------------
-    if (need_j || need_h || need_c) {
-        for (int e = threadIdx.x; e < H.nE; e += blockDim.x) {
-            const int code = ends[e];
-            const int k = code >> 1, side = code & 1;
-            const int f = T.fo[k], t = T.to[k];
-            const double2* ap = reinterpret_cast<const double2*>(T.adm + 8 * (long long)k);
-            const double2 a01 = ap[0], a23 = ap[1], a45 = ap[2], a67 = ap[3];
-            const double gff = a01.x, bff = a01.y, gft = a23.x, bft = a23.y;
-            const double gtf = a45.x, btf = a45.y, gtt = a67.x, btt = a67.y;
-            const double vf = vm[f], vt = vm[t];
-            const double th = va[f] - va[t];
-            double sn, cs;
-            acc_sincos(th, &sn, &cs);
-            const double u = gft * cs + bft * sn;
-            const double w = gft * sn - bft * cs;
-            const double u2 = gtf * cs - btf * sn;
-            const double w2 = -(gtf * sn + btf * cs);
-            const double vv = vf * vt;
-            const double pf = (gff * vf) * vf + vv * u;
-            const double qf = ((-bff) * vf) * vf + vv * w;
-            const double pt = (gtt * vt) * vt + vv * u2;
-            const double qt = ((-btt) * vt) * vt + vv * w2;
-            double* q = Q + EQ * e;
-            q[15] = side ? pt : pf;
-            q[16] = side ? qt : qf;
-            const int r = T.ridx[k];
-            int rs = 0;
-            long long foff = 0;
-            if (r >= 0) stage_rated(P, S, T, r, rs, foff);
-            if (r >= 0 && need_c) {
-                P.cons[S.ineq_row + 2 * rs + side] = side ? pt * pt + qt * qt : pf * pf + qf * qf;
-            }
-            if (!(need_j || need_h)) continue;
-            double gpf[4], gqf[4], gpt[4], gqt[4];
-            gpf[0] = (-vv) * w;  gpf[1] = vv * w;   gpf[2] = (2.0 * gff) * vf + vt * u;   gpf[3] = vf * u;
-            gqf[0] = vv * u;     gqf[1] = (-vv) * u; gqf[2] = (-2.0 * bff) * vf + vt * w; gqf[3] = vf * w;
-            gpt[0] = vv * w2;    gpt[1] = (-vv) * w2; gpt[2] = vt * u2; gpt[3] = (2.0 * gtt) * vt + vf * u2;
-            gqt[0] = (-vv) * u2; gqt[1] = vv * u2;  gqt[2] = vt * w2; gqt[3] = (-2.0 * btt) * vt + vf * w2;
-            if (need_j) {
-                double gp[4], gq[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    gp[i] = side ? gpt[i] : gpf[i];
-                    gq[i] = side ? gqt[i] : gqf[i];
-                    q[i] = -gp[i];
-                    q[4 + i] = -gq[i];
-                }
-                if (r >= 0) {
-                    const double fp = side ? pt : pf, fq = side ? qt : qf;
-                    double d[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) d[i] = (0.0 + (2.0 * fp) * gp[i]) + (2.0 * fq) * gq[i];
-                    const int half = T.rowsz[r] >> 1;
-                    double* out = P.jval + S.jineq_base + foff + side * half;
-                    if (f < t) { out[0] = d[0]; out[1] = d[1]; out[2] = d[2]; out[3] = d[3]; }
-                    else if (f > t) { out[0] = d[1]; out[1] = d[0]; out[2] = d[3]; out[3] = d[2]; }
-                    else { out[0] = d[0] + d[1]; out[1] = d[2] + d[3]; }
-                }
-            }
-            if (need_h) {
-                double sf = 0.0, st = 0.0;
-                if (r >= 0) { sf = mi[2 * rs]; st = mi[2 * rs + 1]; }
-                const double lpf = -mu[f], lqf = -mu[nb + f], lpt = -mu[t], lqt = -mu[nb + t];
-                const double s2f = 2.0 * sf, s2t = 2.0 * st;
-                const double cpf = lpf + s2f * pf, cqf = lqf + s2f * qf;
-                const double cpt = lpt + s2t * pt, cqt = lqt + s2t * qt;
-                const double vvu = vv * u, vvw = vv * w, vvu2 = vv * u2, vvw2 = vv * w2;
-                const double vtw = vt * w, vfw = vf * w, vtu = vt * u, vfu = vf * u;
-                const double vtw2 = vt * w2, vfw2 = vf * w2, vtu2 = vt * u2, vfu2 = vf * u2;
-                const double z = 0.0;
-                // second derivatives of Pf, Qf, Pt, Qt per position (acopf.py:321-328)
-                const double hpf[10] = {-vvu, vvu, -vtw, -vfw, -vvu, vtw, vfw, 2.0 * gff, u, z};
-                const double hqf[10] = {-vvw, vvw, vtu, vfu, -vvw, -vtu, -vfu, -(2.0 * bff), w, z};
-                const double hpt[10] = {-vvu2, vvu2, vtw2, vfw2, -vvu2, -vtw2, -vfw2, z, u2, 2.0 * gtt};
-                const double hqt[10] = {-vvw2, vvw2, -vtu2, -vfu2, -vvw2, vtu2, vfu2, z, w2, -(2.0 * btt)};
-                if (side == 0) {
-#pragma unroll
-                    for (int s = 0; s < 7; ++s)
-                        q[8 + s] = hpos(slot_pos_f(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt,
-                                        hpf, hqf, hpt, hqt);
-                } else {
-#pragma unroll
-                    for (int s = 0; s < 7; ++s)
-                        q[8 + s] = hpos(slot_pos_t(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt,
-                                        hpf, hqf, hpt, hqt);
-                }
-            }
+    const int side = V.code[e] & 1;
+    const int f = V.f[e], t = V.t[e];
+    const int ne = V.h.nE;
+    const double gff = V.adm[e], bff = V.adm[ne + e], gft = V.adm[2 * ne + e], bft = V.adm[3 * ne + e];
+    const double gtf = V.adm[4 * ne + e], btf = V.adm[5 * ne + e], gtt = V.adm[6 * ne + e], btt = V.adm[7 * ne + e];
+    const double vf = vm[f], vt = vm[t];
+    const double th = va[f] - va[t];
+    double sn, cs;
+    acc_sincos(th, &sn, &cs);
+    const double u = gft * cs + bft * sn;
+    const double w = gft * sn - bft * cs;
+    const double u2 = gtf * cs - btf * sn;
+    const double w2 = -(gtf * sn + btf * cs);
+    const double vv = vf * vt;
+    const double pf = (gff * vf) * vf + vv * u;
+    const double qf = ((-bff) * vf) * vf + vv * w;
+    const double pt = (gtt * vt) * vt + vv * u2;
+    const double qt = ((-btt) * vt) * vt + vv * w2;
+    double* q = Q + EQ * e;
+    q[Q_FP] = side ? pt : pf;
+    q[Q_FQ] = side ? qt : qf;
+    const int r = V.ridx[e];
+    int rs = r;
+    long long foff = V.foff[e];
+    if (r >= 0) {
+        for (int i = 0; i < S.nrem; ++i) {
+            if (P.rem_ridx[S.rem_off + i] < r) { rs--; foff -= P.rem_rowsz[S.rem_off + i]; }
         }
+        if (need_c) P.cons[S.ineq_row + 2 * rs + side] = side ? pt * pt + qt * qt : pf * pf + qf * qf;
     }
-
-    // ---- phase A2: bus-level terms ----------------------------------------
-    const int qbus = EQ * H.nE;
-    for (int bl = threadIdx.x; bl < H.nB; bl += blockDim.x) {
-        const int i = H.b0 + bl;
-        const double vmi = vm[i], gsi = T.gs[i], bsi = T.bs[i];
-        double* qb = Q + qbus + BQ * bl;
-        qb[0] = (-2.0 * gsi) * vmi;
-        qb[1] = (2.0 * bsi) * vmi;
-        if (need_h) {
-            const double lp = -mu[i], lq = -mu[nb + i];
-            qb[2] = 2.0 * ((lp * gsi) - (lq * bsi));
-        }
-        if (what & W_GRAD) {
-            P.grad[S.var_off + i] = S.w * 0.0;
-            P.grad[S.var_off + nb + i] = S.w * 0.0;
-        }
-    }
-    if (threadIdx.x == 0) Q[qbus + BQ * H.nB] = 1.0;
-    __syncthreads();
-
-    if (need_c) {
-        const double* pgv = va + 2 * nb;
-        const double* qgv = pgv + T.ng;
-        for (int bl = threadIdx.x; bl < H.nB; bl += blockDim.x) {
-            const int i = H.b0 + bl;
-            const double vmi = vm[i];
-            double p = 0.0, r = 0.0;
-            for (int e = busptr[bl]; e < busptr[bl + 1]; ++e) {
-                p = p + Q[EQ * e + 15];
-                r = r + Q[EQ * e + 16];
-            }
-            p = p + (T.gs[i] * vmi) * vmi;
-            r = r - (T.bs[i] * vmi) * vmi;
-            double cp = -(P.pd[S.pd_off + i] + p);
-            double cq = -(P.qd[S.pd_off + i] + r);
-            for (int gi = T.gen_ptr[i]; gi < T.gen_ptr[i + 1]; ++gi) {
-                const int g = T.gen_list[gi];
-                cp = cp + pgv[g];
-                cq = cq + qgv[g];
-            }
-            P.cons[S.eq_row + i] = cp;
-            P.cons[S.eq_row + nb + i] = cq;
-        }
-    }
-
-    // ---- phase B: scatter-map sums, contiguous stores ------------------------
     if (!(need_j || need_h)) return;
-    const int LJ = H.LP + H.LQ;
-    const int E = LJ + H.LHA + H.LHV;
-    const int e0 = need_j ? 0 : LJ;
-    const int e1 = need_h ? E : LJ;
-    double* oP = P.jval + S.jeq_base + W.jP;
-    double* oQ = P.jval + S.jeq_base + W.jQ - H.LP;
-    double* oA = P.hval + S.h_base + W.hA - LJ;
-    double* oV = P.hval + S.h_base + W.hV - LJ - H.LHA;
-    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-        const int t0 = eptr[e], t1 = eptr[e + 1];
-        double v = Q[terms[t0]];
-        for (int t = t0 + 1; t < t1; ++t) v = v + Q[terms[t]];
-        double* o = e < H.LP ? oP : (e < LJ ? oQ : (e < LJ + H.LHA ? oA : oV));
-        o[e] = v;
+    double gpf[4], gqf[4], gpt[4], gqt[4];
+    gpf[0] = (-vv) * w;  gpf[1] = vv * w;    gpf[2] = (2.0 * gff) * vf + vt * u;   gpf[3] = vf * u;
+    gqf[0] = vv * u;     gqf[1] = (-vv) * u; gqf[2] = (-2.0 * bff) * vf + vt * w; gqf[3] = vf * w;
+    gpt[0] = vv * w2;    gpt[1] = (-vv) * w2; gpt[2] = vt * u2; gpt[3] = (2.0 * gtt) * vt + vf * u2;
+    gqt[0] = (-vv) * u2; gqt[1] = vv * u2;   gqt[2] = vt * w2; gqt[3] = (-2.0 * btt) * vt + vf * w2;
+    if (need_j) {
+        double gp[4], gq[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            gp[i] = side ? gpt[i] : gpf[i];
+            gq[i] = side ? gqt[i] : gqf[i];
+            q[Q_JP + i] = -gp[i];
+            q[Q_JQ + i] = -gq[i];
+        }
+        if (r >= 0) {
+            const double fp = side ? pt : pf, fq = side ? qt : qf;
+            double d[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d[i] = (0.0 + (2.0 * fp) * gp[i]) + (2.0 * fq) * gq[i];
+            double* out = P.jval + S.jineq_base + foff + (f == t ? 2 : 4) * side;
+            if (f < t) { out[0] = d[0]; out[1] = d[1]; out[2] = d[2]; out[3] = d[3]; }
+            else if (f > t) { out[0] = d[1]; out[1] = d[0]; out[2] = d[3]; out[3] = d[2]; }
+            else { out[0] = d[0] + d[1]; out[1] = d[2] + d[3]; }
+        }
+    }
+    if (need_h) {
+        const double* mu = P.mult + S.eq_row;
+        const double* mi = P.mult + S.ineq_row;
+        double sf = 0.0, st = 0.0;
+        if (r >= 0) { sf = mi[2 * rs]; st = mi[2 * rs + 1]; }
+        const double lpf = -mu[f], lqf = -mu[nb + f], lpt = -mu[t], lqt = -mu[nb + t];
+        const double s2f = 2.0 * sf, s2t = 2.0 * st;
+        const double cpf = lpf + s2f * pf, cqf = lqf + s2f * qf;
+        const double cpt = lpt + s2t * pt, cqt = lqt + s2t * qt;
+        const double vvu = vv * u, vvw = vv * w, vvu2 = vv * u2, vvw2 = vv * w2;
+        const double vtw = vt * w, vfw = vf * w, vtu = vt * u, vfu = vf * u;
+        const double vtw2 = vt * w2, vfw2 = vf * w2, vtu2 = vt * u2, vfu2 = vf * u2;
+        const double z = 0.0;
+        // second derivatives of Pf, Qf, Pt, Qt per position (acopf.py:321-328)
+        const double hpf[10] = {-vvu, vvu, -vtw, -vfw, -vvu, vtw, vfw, 2.0 * gff, u, z};
+        const double hqf[10] = {-vvw, vvw, vtu, vfu, -vvw, -vtu, -vfu, -(2.0 * bff), w, z};
+        const double hpt[10] = {-vvu2, vvu2, vtw2, vfw2, -vvu2, -vtw2, -vfw2, z, u2, 2.0 * gtt};
+        const double hqt[10] = {-vvw2, vvw2, -vtu2, -vfu2, -vvw2, vtu2, vfu2, z, w2, -(2.0 * btt)};
+        if (side == 0) {
+#pragma unroll
+            for (int s = 0; s < 7; ++s)
+                q[Q_H + s] = hpos(slot_pos_f(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
+        } else {
+#pragma unroll
+            for (int s = 0; s < 7; ++s)
+                q[Q_H + s] = hpos(slot_pos_t(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
+        }
     }
 }
+
+__global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) unsigned long long bar;
+    const DBusItem it = P.bus_items[blockIdx.x];
+    const unsigned char* src = P.blob + it.blob_off;
+    // ---- 0. bulk copy of the tile table into shared memory ----------------
+    if (threadIdx.x == 0) {
+        const unsigned b = smem_u32(&bar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(it.bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(smem)),
+            "l"(src), "r"(it.bytes), "r"(b)
+            : "memory");
+    }
+    __syncthreads();
+    {
+        const unsigned b = smem_u32(&bar);
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(b)
+                : "memory");
+        }
+    }
+    TileView V;
+    V.h = *reinterpret_cast<const TileHdr*>(smem);
+    V.code = reinterpret_cast<const int*>(smem + V.h.o_code);
+    V.f = reinterpret_cast<const int*>(smem + V.h.o_f);
+    V.t = reinterpret_cast<const int*>(smem + V.h.o_t);
+    V.ridx = reinterpret_cast<const int*>(smem + V.h.o_ridx);
+    V.foff = reinterpret_cast<const int*>(smem + V.h.o_foff);
+    V.busptr = reinterpret_cast<const int*>(smem + V.h.o_busptr);
+    V.gptr = reinterpret_cast<const int*>(smem + V.h.o_gptr);
+    V.glist = reinterpret_cast<const int*>(smem + V.h.o_glist);
+    V.gs = reinterpret_cast<const double*>(smem + V.h.o_gs);
+    V.bs = reinterpret_cast<const double*>(smem + V.h.o_bs);
+    V.adm = reinterpret_cast<const double*>(smem + V.h.o_adm);
+    V.eptr = reinterpret_cast<const int*>(smem + V.h.o_eptr);
+    V.terms = reinterpret_cast<const unsigned short*>(smem + V.h.o_terms);
+    double* Q = reinterpret_cast<double*>(smem + V.h.bytes);
+    const unsigned what = P.what;
+    const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
+    const int qbus = EQ * V.h.nE;
+    if (threadIdx.x == 0) Q[qbus + BQ * V.h.nB] = 1.0;
+
+    for (int ri = 0; ri < it.count; ++ri) {
+        const DBusRec R = P.bus_recs[it.first + ri];
+        const DStage S = P.stages[R.stage];
+        const int nb = P.topos[S.topo].nb;
+        const int ng = P.topos[S.topo].ng;
+        const double* vm = P.x + S.var_off + nb;
+        // ---- A: branch ends ------------------------------------------------
+        if (need_j || need_h || need_c)
+            for (int e = threadIdx.x; e < V.h.nE; e += blockDim.x)
+                branch_end(P, S, nb, V, e, Q, need_j, need_h, need_c);
+        // ---- A2: bus-level terms -----------------------------------------------
+        for (int bl = threadIdx.x; bl < V.h.nB; bl += blockDim.x) {
+            const int i = V.h.b0 + bl;
+            const double vmi = vm[i], gsi = V.gs[bl], bsi = V.bs[bl];
+            double* qb = Q + qbus + BQ * bl;
+            qb[0] = (-2.0 * gsi) * vmi;
+            qb[1] = (2.0 * bsi) * vmi;
+            if (need_h) {
+                const double* mu = P.mult + S.eq_row;
+                qb[2] = 2.0 * ((-mu[i] * gsi) - (-mu[nb + i] * bsi));
+            }
+            if (what & W_GRAD) {
+                P.grad[S.var_off + i] = S.w * 0.0;
+                P.grad[S.var_off + nb + i] = S.w * 0.0;
+            }
+        }
+        __syncthreads();
+        // ---- B: balance rows, then the scatter-map sums -------------------------
+        if (need_c) {
+            const double* pgv = P.x + S.var_off + 2 * nb;
+            const double* qgv = pgv + ng;
+            for (int bl = threadIdx.x; bl < V.h.nB; bl += blockDim.x) {
+                const int i = V.h.b0 + bl;
+                const double vmi = vm[i];
+                double p = 0.0, r = 0.0;
+                for (int e = V.busptr[bl]; e < V.busptr[bl + 1]; ++e) {
+                    p = p + Q[EQ * e + Q_FP];
+                    r = r + Q[EQ * e + Q_FQ];
+                }
+                p = p + (V.gs[bl] * vmi) * vmi;
+                r = r - (V.bs[bl] * vmi) * vmi;
+                double cp = -(P.pd[S.pd_off + i] + p);
+                double cq = -(P.qd[S.pd_off + i] + r);
+                for (int gi = V.gptr[bl]; gi < V.gptr[bl + 1]; ++gi) {
+                    const int g = V.glist[gi];
+                    cp = cp + pgv[g];
+                    cq = cq + qgv[g];
+                }
+                P.cons[S.eq_row + i] = cp;
+                P.cons[S.eq_row + nb + i] = cq;
+            }
+        }
+        if (need_j || need_h) {
+            const int LP = V.h.LP, LJ = V.h.LP + V.h.LQ, LA = LJ + V.h.LHA;
+            const int E = LA + V.h.LHV;
+            const int e0 = need_j ? 0 : LJ;
+            const int e1 = need_h ? E : LJ;
+            double* oP = P.jval + S.jeq_base + R.jP;
+            double* oQ = P.jval + S.jeq_base + R.jQ - LP;
+            double* oA = P.hval + S.h_base + R.hA - LJ;
+            double* oV = P.hval + S.h_base + R.hV - LA;
+            for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+                const int t0 = V.eptr[e], t1 = V.eptr[e + 1];
+                double v = Q[V.terms[t0]];
+                for (int t = t0 + 1; t < t1; ++t) v = v + Q[V.terms[t]];
+                double* o = e < LP ? oP : (e < LJ ? oQ : (e < LA ? oA : oV));
+                o[e] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// generator / coupling kernel
 
 __device__ double pairwise_tree(int n, const double* leaves, int& idx) {
     if (n <= 128) return leaves[idx++];
@@ -316,10 +376,7 @@ __device__ __forceinline__ double cost_term(const EvalParams& P, const DStage& S
     return ((P.ca[S.cost_off + g] * p + P.cb[S.cost_off + g]) * p) + P.cc[S.cost_off + g];
 }
 
-__device__ void gen_chunk(const EvalParams& P, int item, double* Q) {
-    // items are laid out stage-major: stage s owns chunks [first, first + nchunk)
-    const int s = P.work[item].stage;
-    const int chunk = P.work[item].jP;
+__device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
     const DStage S = P.stages[s];
     const DTopo T = P.topos[S.topo];
     const int nb = T.nb, ng = T.ng;
@@ -337,7 +394,7 @@ __device__ void gen_chunk(const EvalParams& P, int item, double* Q) {
         }
     }
     if (chunk != 0 || !(P.what & W_OBJ)) return;
-    // stage objective: numpy pairwise sum over the ng cost terms
+    // stage objective: numpy's pairwise sum over the ng cost terms (acopf.py:266-269)
     for (int l = threadIdx.x; l < T.nleaf; l += blockDim.x) {
         const int st = T.leaf[2 * l], n = T.leaf[2 * l + 1];
         double res;
@@ -368,25 +425,28 @@ __device__ void gen_chunk(const EvalParams& P, int item, double* Q) {
             last = false;
         } else {
             P.obj_terms[S.obj_slot] = S.w * fs;
+            if (P.obj_mode == 2) P.obj[S.obj_slot] = S.w * fs;
             __threadfence();
             const unsigned done = atomicAdd(P.counter, 1u);
             last = (done == (unsigned)P.n_obj - 1);
         }
     }
     __syncthreads();
-    if (!last || P.obj_mode != 1) return;
+    if (!last) return;
     if (threadIdx.x == 0) {
         __threadfence();
-        const volatile double* terms = P.obj_terms;
-        double acc = 0.0;
-        for (int i = 0; i < P.n_obj; ++i) acc = acc + terms[i];
-        P.obj[0] = acc;
+        if (P.obj_mode == 1) {
+            const volatile double* terms = P.obj_terms;
+            double acc = 0.0;
+            for (int i = 0; i < P.n_obj; ++i) acc = acc + terms[i];
+            P.obj[0] = acc;
+        }
         *P.counter = 0u;
     }
 }
 
-__device__ void coupling_chunk(const EvalParams& P, int item) {
-    const long long c = (long long)item * CP_CHUNK;
+__device__ void coupling_chunk(const EvalParams& P, int chunk) {
+    const long long c = (long long)chunk * CP_CHUNK;
     for (long long i = c + threadIdx.x; i < c + CP_CHUNK && i < P.ncp; i += blockDim.x) {
         if (P.what & W_CONS) P.cons[P.cp_row[i]] = P.x[P.cp_a[i]] - P.x[P.cp_b[i]];
         if (P.what & W_JAC) {
@@ -397,16 +457,11 @@ __device__ void coupling_chunk(const EvalParams& P, int item) {
     }
 }
 
-__global__ void __launch_bounds__(BLOCK) acopf_eval_kernel(const EvalParams P) {
-    extern __shared__ double Q[];
-    const int item = blockIdx.x;
-    if (item < P.n_bus_work) {
-        bus_tile(P, P.work[item], Q);
-    } else if (item < P.n_bus_work + P.n_gen_work) {
-        gen_chunk(P, item, Q);
-    } else {
-        coupling_chunk(P, item - P.n_bus_work - P.n_gen_work);
-    }
+__global__ void __launch_bounds__(BLOCK) acopf_aux_kernel(const EvalParams P) {
+    extern __shared__ __align__(16) double leaves[];
+    const DAuxItem it = P.aux_items[blockIdx.x];
+    if (it.kind == 0) gen_chunk(P, it.stage, it.chunk, leaves);
+    else coupling_chunk(P, it.chunk);
 }
 
 }  // namespace acopf

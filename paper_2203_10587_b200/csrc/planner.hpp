@@ -53,7 +53,7 @@ constexpr int POS_OF_SLOT_T[7] = {1, 3, 4, 5, 6, 8, 9};
 
 constexpr int TILE_MAX_ENDS = 256;   // soft cap; a single high-degree bus may exceed it
 constexpr int TILE_MAX_BUSES = 128;
-constexpr int SMEM_LIMIT_DOUBLES = (200 * 1024) / 8;
+constexpr int SMEM_LIMIT_BYTES = 220 * 1024;
 
 // symbolic term: what a COO entry's value is made of
 struct Sym {
@@ -238,15 +238,23 @@ inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
 // ---------------------------------------------------------------------------
 // Tile tables (serialised into one device blob)
 
-struct TileHdr {            // 64 bytes, all offsets in bytes from the header
-    int32_t b0, nB, nE, nQ;
-    int32_t LP, LQ, LHA, LHV;
-    int32_t nTerms, off_ends, off_busptr, off_eptr;
-    int32_t off_terms, pad0, pad1, pad2;
+struct TileHdr {            // 128 bytes; offsets in bytes from the header start
+    int32_t b0, nB, nE, nQ;           // first bus, buses, ends, shared doubles for quantities
+    int32_t LP, LQ, LHA, LHV;         // entries of the four row segments
+    int32_t nTerms, ngl, bytes, pad0; // terms, generator ids, serialised size (multiple of 16)
+    int32_t o_code, o_f, o_t, o_ridx;
+    int32_t o_foff, o_busptr, o_gptr, o_glist;
+    int32_t o_gs, o_bs, o_adm, o_eptr;
+    int32_t o_terms, pad1, pad2, pad3;
+    int32_t pad4, pad5, pad6, pad7;
 };
-static_assert(sizeof(TileHdr) == 64, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 128, "TileHdr layout");
 
+// A tile's complete working set, copied to shared memory in one bulk copy:
+// per-end topology (bus slots, rated index, flow-row offset, SoA admittances),
+// per-bus shunts and generator lists, and the scatter map (entry -> terms).
 struct TileTable {
+    int topo = 0;
     int b0 = 0, nB = 0;
     std::vector<int> ends;        // k*2+side, per bus: from-ends then to-ends
     std::vector<int> busptr;      // nB+1
@@ -256,39 +264,69 @@ struct TileTable {
     std::vector<int> eptr;        // entries+1
     std::vector<uint16_t> terms;  // shared-memory slot per term
     int nQ() const { return EQ * (int)ends.size() + BQ * nB + 1; }
-    size_t bytes() const;
-    void serialise(std::vector<uint8_t>& blob) const;
+    void serialise(const Topo& T, std::vector<uint8_t>& blob) const;
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-inline size_t TileTable::bytes() const {
-    size_t s = sizeof(TileHdr);
-    s = align16(s + 4 * ends.size());
-    s = align16(s + 4 * busptr.size());
-    s = align16(s + 4 * eptr.size());
-    s = align16(s + 2 * terms.size());
-    return s;
-}
-
-inline void TileTable::serialise(std::vector<uint8_t>& blob) const {
-    size_t base = blob.size();
-    blob.resize(base + bytes(), 0);
-    uint8_t* p = blob.data() + base;
+inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) const {
+    const int nE = (int)ends.size();
+    std::vector<int> f(nE), t(nE), ridx(nE), foff(nE), gptr(1, 0), glist;
+    std::vector<double> adm(8 * (size_t)nE), gs(nB), bs(nB);
+    for (int e = 0; e < nE; ++e) {
+        int k = ends[e] >> 1;
+        f[e] = T.fo[k];
+        t[e] = T.to[k];
+        ridx[e] = T.ridx[k];
+        foff[e] = T.ridx[k] >= 0 ? (int)T.foff[T.ridx[k]] : 0;
+        for (int q = 0; q < 8; ++q) adm[(size_t)q * nE + e] = T.adm[8 * (size_t)k + q];
+    }
+    for (int bl = 0; bl < nB; ++bl) {
+        int i = b0 + bl;
+        gs[bl] = T.gs[i];
+        bs[bl] = T.bs[i];
+        for (int p = T.gen_ptr[i]; p < T.gen_ptr[i + 1]; ++p) glist.push_back(T.gen_list[p]);
+        gptr.push_back((int)glist.size());
+    }
     TileHdr h{};
-    h.b0 = b0; h.nB = nB; h.nE = (int)ends.size(); h.nQ = nQ();
+    h.b0 = b0; h.nB = nB; h.nE = nE; h.nQ = nQ();
     h.LP = L[0]; h.LQ = L[1]; h.LHA = L[2]; h.LHV = L[3];
     h.nTerms = (int)terms.size();
+    h.ngl = (int)glist.size();
     size_t off = sizeof(TileHdr);
-    h.off_ends = (int)off;   off = align16(off + 4 * ends.size());
-    h.off_busptr = (int)off; off = align16(off + 4 * busptr.size());
-    h.off_eptr = (int)off;   off = align16(off + 4 * eptr.size());
-    h.off_terms = (int)off;
+    auto take = [&](size_t n) { int o = (int)off; off = align16(off + n); return o; };
+    h.o_code = take(4 * (size_t)nE);
+    h.o_f = take(4 * (size_t)nE);
+    h.o_t = take(4 * (size_t)nE);
+    h.o_ridx = take(4 * (size_t)nE);
+    h.o_foff = take(4 * (size_t)nE);
+    h.o_busptr = take(4 * busptr.size());
+    h.o_gptr = take(4 * gptr.size());
+    h.o_glist = take(4 * glist.size());
+    h.o_gs = take(8 * (size_t)nB);
+    h.o_bs = take(8 * (size_t)nB);
+    h.o_adm = take(8 * adm.size());
+    h.o_eptr = take(4 * eptr.size());
+    h.o_terms = take(2 * terms.size());
+    h.bytes = (int)off;
+    size_t base = blob.size();
+    blob.resize(base + off, 0);
+    uint8_t* p = blob.data() + base;
     std::memcpy(p, &h, sizeof h);
-    if (!ends.empty()) std::memcpy(p + h.off_ends, ends.data(), 4 * ends.size());
-    std::memcpy(p + h.off_busptr, busptr.data(), 4 * busptr.size());
-    std::memcpy(p + h.off_eptr, eptr.data(), 4 * eptr.size());
-    if (!terms.empty()) std::memcpy(p + h.off_terms, terms.data(), 2 * terms.size());
+    auto put = [&](int o, const void* src, size_t n) { if (n) std::memcpy(p + o, src, n); };
+    put(h.o_code, ends.data(), 4 * (size_t)nE);
+    put(h.o_f, f.data(), 4 * (size_t)nE);
+    put(h.o_t, t.data(), 4 * (size_t)nE);
+    put(h.o_ridx, ridx.data(), 4 * (size_t)nE);
+    put(h.o_foff, foff.data(), 4 * (size_t)nE);
+    put(h.o_busptr, busptr.data(), 4 * busptr.size());
+    put(h.o_gptr, gptr.data(), 4 * gptr.size());
+    put(h.o_glist, glist.data(), 4 * glist.size());
+    put(h.o_gs, gs.data(), 8 * (size_t)nB);
+    put(h.o_bs, bs.data(), 8 * (size_t)nB);
+    put(h.o_adm, adm.data(), 8 * adm.size());
+    put(h.o_eptr, eptr.data(), 4 * eptr.size());
+    put(h.o_terms, terms.data(), 2 * terms.size());
 }
 
 inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
@@ -318,8 +356,6 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         for (int s = 0; s < 4; ++s) rows[s * tt.nB + (i - b0)] = std::move(r4[s]);
     }
     const int nE = (int)tt.ends.size();
-    if (tt.nQ() > SMEM_LIMIT_DOUBLES)
-        throw std::runtime_error("bus degree too high for one tile's shared memory");
     tt.eptr.push_back(0);
     for (int s = 0; s < 4; ++s) {
         for (int r = 0; r < tt.nB; ++r) {
@@ -340,6 +376,11 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             }
         }
     }
+    // shared memory = serialised table + quantity array (checked again at upload)
+    size_t approx = 128 + 20 * (size_t)nE + 8 * (size_t)tt.nB + 64 * (size_t)nE + 4 * tt.eptr.size() +
+                    2 * tt.terms.size() + 8 * (size_t)tt.nQ() + 256;
+    if (approx > (size_t)SMEM_LIMIT_BYTES)
+        throw std::runtime_error("bus degree too high for one tile's shared memory");
     return tt;
 }
 
