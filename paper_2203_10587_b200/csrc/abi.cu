@@ -178,22 +178,23 @@ static void upload(acopf_batch* b) {
     std::vector<std::pair<int, int>> tiles;       // (topo, tile)
     for (size_t ti = 0; ti < b->topos.size(); ++ti)
         for (size_t t = 0; t < b->base_table[ti].size(); ++t) tiles.push_back({(int)ti, (int)t});
-    for (auto [topo, t] : tiles) {
-        by_table.clear();
-        for (int s = 0; s < S; ++s)
-            if (b->stages[s].topo == topo) by_table[b->stages[s].table[t]].push_back(s);
-        for (auto& kv : by_table) {
-            const std::vector<int>& ss = kv.second;
-            for (size_t c = 0; c < ss.size(); c += G) {
+    // stage-group-major order: CTAs running together share one group's x/mult in L2
+    for (int g0 = 0; g0 < S; g0 += G) {
+        const int g1 = std::min(S, g0 + G);
+        for (auto [topo, t] : tiles) {
+            by_table.clear();
+            for (int s = g0; s < g1; ++s)
+                if (b->stages[s].topo == topo) by_table[b->stages[s].table[t]].push_back(s);
+            for (auto& kv : by_table) {
                 DBusItem it{};
                 it.blob_off = table_off[kv.first];
                 it.bytes = table_bytes[kv.first];
                 it.first = (int)recs.size();
-                it.count = (int)std::min<size_t>(G, ss.size() - c);
-                for (size_t j = c; j < c + it.count; ++j) {
-                    const StageInfo& st = b->stages[ss[j]];
+                it.count = (int)kv.second.size();
+                for (int s : kv.second) {
+                    const StageInfo& st = b->stages[s];
                     DBusRec r{};
-                    r.stage = ss[j];
+                    r.stage = s;
                     r.jP = st.tile_off[4 * t + 0]; r.jQ = st.tile_off[4 * t + 1];
                     r.hA = st.tile_off[4 * t + 2]; r.hV = st.tile_off[4 * t + 3];
                     recs.push_back(r);

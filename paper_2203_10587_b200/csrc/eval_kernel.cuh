@@ -116,7 +116,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 // bus kernel
 
 struct TileView {
-    TileHdr h;
+    const TileHdr* h;
     const int* code;
     const int* f;
     const int* t;
@@ -152,11 +152,34 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const DStage& S,
     const double* vm = va + nb;
     const int side = V.code[e] & 1;
     const int f = V.f[e], t = V.t[e];
-    const int ne = V.h.nE;
+    const int r = V.ridx[e];
+    int rs = r;
+    long long foff = V.foff[e];
+    if (r >= 0) {
+        for (int i = 0; i < S.nrem; ++i) {
+            if (__ldg(P.rem_ridx + S.rem_off + i) < r) { rs--; foff -= __ldg(P.rem_rowsz + S.rem_off + i); }
+        }
+    }
+    // all gathers first (read-only path), so they are in flight together
+    const double vaf = __ldg(va + f), vat = __ldg(va + t);
+    const double vf = __ldg(vm + f), vt = __ldg(vm + t);
+    double mpf = 0.0, mqf = 0.0, mpt = 0.0, mqt = 0.0, sf = 0.0, st = 0.0;
+    if (need_h) {
+        const double* mu = P.mult + S.eq_row;
+        mpf = __ldg(mu + f);
+        mqf = __ldg(mu + nb + f);
+        mpt = __ldg(mu + t);
+        mqt = __ldg(mu + nb + t);
+        if (r >= 0) {
+            const double* mi = P.mult + S.ineq_row + 2 * rs;
+            sf = __ldg(mi);
+            st = __ldg(mi + 1);
+        }
+    }
+    const int ne = V.h->nE;
     const double gff = V.adm[e], bff = V.adm[ne + e], gft = V.adm[2 * ne + e], bft = V.adm[3 * ne + e];
     const double gtf = V.adm[4 * ne + e], btf = V.adm[5 * ne + e], gtt = V.adm[6 * ne + e], btt = V.adm[7 * ne + e];
-    const double vf = vm[f], vt = vm[t];
-    const double th = va[f] - va[t];
+    const double th = vaf - vat;
     double sn, cs;
     acc_sincos(th, &sn, &cs);
     const double u = gft * cs + bft * sn;
@@ -171,15 +194,7 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const DStage& S,
     double* q = Q + EQ * e;
     q[Q_FP] = side ? pt : pf;
     q[Q_FQ] = side ? qt : qf;
-    const int r = V.ridx[e];
-    int rs = r;
-    long long foff = V.foff[e];
-    if (r >= 0) {
-        for (int i = 0; i < S.nrem; ++i) {
-            if (P.rem_ridx[S.rem_off + i] < r) { rs--; foff -= P.rem_rowsz[S.rem_off + i]; }
-        }
-        if (need_c) P.cons[S.ineq_row + 2 * rs + side] = side ? pt * pt + qt * qt : pf * pf + qf * qf;
-    }
+    if (r >= 0 && need_c) P.cons[S.ineq_row + 2 * rs + side] = side ? pt * pt + qt * qt : pf * pf + qf * qf;
     if (!(need_j || need_h)) return;
     double gpf[4], gqf[4], gpt[4], gqt[4];
     gpf[0] = (-vv) * w;  gpf[1] = vv * w;    gpf[2] = (2.0 * gff) * vf + vt * u;   gpf[3] = vf * u;
@@ -207,11 +222,7 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const DStage& S,
         }
     }
     if (need_h) {
-        const double* mu = P.mult + S.eq_row;
-        const double* mi = P.mult + S.ineq_row;
-        double sf = 0.0, st = 0.0;
-        if (r >= 0) { sf = mi[2 * rs]; st = mi[2 * rs + 1]; }
-        const double lpf = -mu[f], lqf = -mu[nb + f], lpt = -mu[t], lqt = -mu[nb + t];
+        const double lpf = -mpf, lqf = -mqf, lpt = -mpt, lqt = -mqt;
         const double s2f = 2.0 * sf, s2t = 2.0 * st;
         const double cpf = lpf + s2f * pf, cqf = lqf + s2f * qf;
         const double cpt = lpt + s2t * pt, cqt = lqt + s2t * qt;
@@ -266,25 +277,26 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
         }
     }
     TileView V;
-    V.h = *reinterpret_cast<const TileHdr*>(smem);
-    V.code = reinterpret_cast<const int*>(smem + V.h.o_code);
-    V.f = reinterpret_cast<const int*>(smem + V.h.o_f);
-    V.t = reinterpret_cast<const int*>(smem + V.h.o_t);
-    V.ridx = reinterpret_cast<const int*>(smem + V.h.o_ridx);
-    V.foff = reinterpret_cast<const int*>(smem + V.h.o_foff);
-    V.busptr = reinterpret_cast<const int*>(smem + V.h.o_busptr);
-    V.gptr = reinterpret_cast<const int*>(smem + V.h.o_gptr);
-    V.glist = reinterpret_cast<const int*>(smem + V.h.o_glist);
-    V.gs = reinterpret_cast<const double*>(smem + V.h.o_gs);
-    V.bs = reinterpret_cast<const double*>(smem + V.h.o_bs);
-    V.adm = reinterpret_cast<const double*>(smem + V.h.o_adm);
-    V.eptr = reinterpret_cast<const int*>(smem + V.h.o_eptr);
-    V.terms = reinterpret_cast<const unsigned short*>(smem + V.h.o_terms);
-    double* Q = reinterpret_cast<double*>(smem + V.h.bytes);
+    const TileHdr* H = reinterpret_cast<const TileHdr*>(smem);
+    V.h = H;
+    V.code = reinterpret_cast<const int*>(smem + H->o_code);
+    V.f = reinterpret_cast<const int*>(smem + H->o_f);
+    V.t = reinterpret_cast<const int*>(smem + H->o_t);
+    V.ridx = reinterpret_cast<const int*>(smem + H->o_ridx);
+    V.foff = reinterpret_cast<const int*>(smem + H->o_foff);
+    V.busptr = reinterpret_cast<const int*>(smem + H->o_busptr);
+    V.gptr = reinterpret_cast<const int*>(smem + H->o_gptr);
+    V.glist = reinterpret_cast<const int*>(smem + H->o_glist);
+    V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
+    V.bs = reinterpret_cast<const double*>(smem + H->o_bs);
+    V.adm = reinterpret_cast<const double*>(smem + H->o_adm);
+    V.eptr = reinterpret_cast<const int*>(smem + H->o_eptr);
+    V.terms = reinterpret_cast<const unsigned short*>(smem + H->o_terms);
+    double* Q = reinterpret_cast<double*>(smem + H->bytes);
     const unsigned what = P.what;
     const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
-    const int qbus = EQ * V.h.nE;
-    if (threadIdx.x == 0) Q[qbus + BQ * V.h.nB] = 1.0;
+    const int qbus = EQ * H->nE;
+    if (threadIdx.x == 0) Q[qbus + BQ * H->nB] = 1.0;
 
     for (int ri = 0; ri < it.count; ++ri) {
         const DBusRec R = P.bus_recs[it.first + ri];
@@ -294,11 +306,11 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
         const double* vm = P.x + S.var_off + nb;
         // ---- A: branch ends ------------------------------------------------
         if (need_j || need_h || need_c)
-            for (int e = threadIdx.x; e < V.h.nE; e += blockDim.x)
+            for (int e = threadIdx.x; e < H->nE; e += blockDim.x)
                 branch_end(P, S, nb, V, e, Q, need_j, need_h, need_c);
         // ---- A2: bus-level terms -----------------------------------------------
-        for (int bl = threadIdx.x; bl < V.h.nB; bl += blockDim.x) {
-            const int i = V.h.b0 + bl;
+        for (int bl = threadIdx.x; bl < H->nB; bl += blockDim.x) {
+            const int i = H->b0 + bl;
             const double vmi = vm[i], gsi = V.gs[bl], bsi = V.bs[bl];
             double* qb = Q + qbus + BQ * bl;
             qb[0] = (-2.0 * gsi) * vmi;
@@ -317,8 +329,8 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
         if (need_c) {
             const double* pgv = P.x + S.var_off + 2 * nb;
             const double* qgv = pgv + ng;
-            for (int bl = threadIdx.x; bl < V.h.nB; bl += blockDim.x) {
-                const int i = V.h.b0 + bl;
+            for (int bl = threadIdx.x; bl < H->nB; bl += blockDim.x) {
+                const int i = H->b0 + bl;
                 const double vmi = vm[i];
                 double p = 0.0, r = 0.0;
                 for (int e = V.busptr[bl]; e < V.busptr[bl + 1]; ++e) {
@@ -339,8 +351,8 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
             }
         }
         if (need_j || need_h) {
-            const int LP = V.h.LP, LJ = V.h.LP + V.h.LQ, LA = LJ + V.h.LHA;
-            const int E = LA + V.h.LHV;
+            const int LP = H->LP, LJ = H->LP + H->LQ, LA = LJ + H->LHA;
+            const int E = LA + H->LHV;
             const int e0 = need_j ? 0 : LJ;
             const int e1 = need_h ? E : LJ;
             double* oP = P.jval + S.jeq_base + R.jP;
