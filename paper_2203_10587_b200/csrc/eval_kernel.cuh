@@ -128,8 +128,6 @@ struct TileView {
     const double* gs;
     const double* bs;
     const double* adm;
-    const int* eptr;
-    const unsigned short* terms;
 };
 
 __device__ __forceinline__ double hpos(int p, double cpf, double cqf, double cpt, double cqt,
@@ -290,8 +288,6 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
     V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
     V.bs = reinterpret_cast<const double*>(smem + H->o_bs);
     V.adm = reinterpret_cast<const double*>(smem + H->o_adm);
-    V.eptr = reinterpret_cast<const int*>(smem + H->o_eptr);
-    V.terms = reinterpret_cast<const unsigned short*>(smem + H->o_terms);
     double* Q = reinterpret_cast<double*>(smem + H->bytes);
     const unsigned what = P.what;
     const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
@@ -350,21 +346,31 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
                 P.cons[S.eq_row + nb + i] = cq;
             }
         }
-        if (need_j || need_h) {
-            const int LP = H->LP, LJ = H->LP + H->LQ, LA = LJ + H->LHA;
-            const int E = LA + H->LHV;
-            const int e0 = need_j ? 0 : LJ;
-            const int e1 = need_h ? E : LJ;
-            double* oP = P.jval + S.jeq_base + R.jP;
-            double* oQ = P.jval + S.jeq_base + R.jQ - LP;
-            double* oA = P.hval + S.h_base + R.hA - LJ;
-            double* oV = P.hval + S.h_base + R.hV - LA;
-            for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-                const int t0 = V.eptr[e], t1 = V.eptr[e + 1];
-                double v = Q[V.terms[t0]];
-                for (int t = t0 + 1; t < t1; ++t) v = v + Q[V.terms[t]];
-                double* o = e < LP ? oP : (e < LJ ? oQ : (e < LA ? oA : oV));
-                o[e] = v;
+        const unsigned short* mterms = reinterpret_cast<const unsigned short*>(smem + H->o_mterms);
+        for (int cls = 0; cls < 2; ++cls) {
+            if (cls == 0 ? !need_j : !need_h) continue;
+            double* o0 = cls == 0 ? P.jval + S.jeq_base + R.jP : P.hval + S.h_base + R.hA;
+            double* o1 = cls == 0 ? P.jval + S.jeq_base + R.jQ : P.hval + S.h_base + R.hV;
+            const int ns = cls == 0 ? H->nSJ : H->nSH;
+            const unsigned* sdst = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_sj_dst : H->o_sh_dst));
+            const unsigned short* sterm =
+                reinterpret_cast<const unsigned short*>(smem + (cls == 0 ? H->o_sj_term : H->o_sh_term));
+            for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+                const unsigned d = sdst[i];
+                double* o = (d & 0x80000000u) ? o1 : o0;
+                o[d & 0x7fffffffu] = Q[sterm[i]];
+            }
+            const int nm = cls == 0 ? H->nMJ : H->nMH;
+            const unsigned* mdst = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_mj_dst : H->o_mh_dst));
+            const unsigned* minfo = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_mj_info : H->o_mh_info));
+            for (int i = threadIdx.x; i < nm; i += blockDim.x) {
+                const unsigned d = mdst[i], info = minfo[i];
+                const unsigned short* tp = mterms + (info >> 10);
+                const int c = (int)(info & 1023u);
+                double v = Q[tp[0]];
+                for (int k = 1; k < c; ++k) v = v + Q[tp[k]];
+                double* o = (d & 0x80000000u) ? o1 : o0;
+                o[d & 0x7fffffffu] = v;
             }
         }
         __syncthreads();

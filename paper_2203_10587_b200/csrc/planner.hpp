@@ -238,21 +238,27 @@ inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
 // ---------------------------------------------------------------------------
 // Tile tables (serialised into one device blob)
 
-struct TileHdr {            // 128 bytes; offsets in bytes from the header start
+struct TileHdr {            // 192 bytes; offsets in bytes from the header start
     int32_t b0, nB, nE, nQ;           // first bus, buses, ends, shared doubles for quantities
     int32_t LP, LQ, LHA, LHV;         // entries of the four row segments
-    int32_t nTerms, ngl, bytes, pad0; // terms, generator ids, serialised size (multiple of 16)
+    int32_t ngl, bytes, nSJ, nSH;     // generator ids, serialised size, single-term J / H entries
+    int32_t nMJ, nMH, nMT, pad0;      // multi-term J / H entries, their term count
     int32_t o_code, o_f, o_t, o_ridx;
     int32_t o_foff, o_busptr, o_gptr, o_glist;
-    int32_t o_gs, o_bs, o_adm, o_eptr;
-    int32_t o_terms, pad1, pad2, pad3;
-    int32_t pad4, pad5, pad6, pad7;
+    int32_t o_gs, o_bs, o_adm, o_sj_dst;
+    int32_t o_sj_term, o_sh_dst, o_sh_term, o_mj_dst;
+    int32_t o_mj_info, o_mh_dst, o_mh_info, o_mterms;
+    int32_t pad[12];
 };
-static_assert(sizeof(TileHdr) == 128, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
 
 // A tile's complete working set, copied to shared memory in one bulk copy:
 // per-end topology (bus slots, rated index, flow-row offset, SoA admittances),
-// per-bus shunts and generator lists, and the scatter map (entry -> terms).
+// per-bus shunts and generator lists, and the scatter map split into classes:
+//   single-term entries  dst (bit 31: Q row / VM row segment, else P / VA)
+//                        + the one quantity slot;
+//   multi-term entries   dst + (first term << 10 | term count), sorted by count
+//                        so a warp runs uniform trip counts.
 struct TileTable {
     int topo = 0;
     int b0 = 0, nB = 0;
@@ -261,8 +267,11 @@ struct TileTable {
     int L[4] = {0, 0, 0, 0};      // entries in P, Q, VA, VM segments
     std::vector<int> cols;        // stage-local column per entry (pattern export)
     std::vector<int> rowlen;      // entries per row, 4 segments x nB rows
-    std::vector<int> eptr;        // entries+1
-    std::vector<uint16_t> terms;  // shared-memory slot per term
+    std::vector<uint32_t> sdst[2];      // [0] J, [1] H
+    std::vector<uint16_t> sterm[2];
+    std::vector<uint32_t> mdst[2];
+    std::vector<uint32_t> minfo[2];
+    std::vector<uint16_t> mterms;
     int nQ() const { return EQ * (int)ends.size() + BQ * nB + 1; }
     void serialise(const Topo& T, std::vector<uint8_t>& blob) const;
 };
@@ -291,8 +300,10 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     TileHdr h{};
     h.b0 = b0; h.nB = nB; h.nE = nE; h.nQ = nQ();
     h.LP = L[0]; h.LQ = L[1]; h.LHA = L[2]; h.LHV = L[3];
-    h.nTerms = (int)terms.size();
     h.ngl = (int)glist.size();
+    h.nSJ = (int)sdst[0].size(); h.nSH = (int)sdst[1].size();
+    h.nMJ = (int)mdst[0].size(); h.nMH = (int)mdst[1].size();
+    h.nMT = (int)mterms.size();
     size_t off = sizeof(TileHdr);
     auto take = [&](size_t n) { int o = (int)off; off = align16(off + n); return o; };
     h.o_code = take(4 * (size_t)nE);
@@ -306,8 +317,15 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     h.o_gs = take(8 * (size_t)nB);
     h.o_bs = take(8 * (size_t)nB);
     h.o_adm = take(8 * adm.size());
-    h.o_eptr = take(4 * eptr.size());
-    h.o_terms = take(2 * terms.size());
+    h.o_sj_dst = take(4 * sdst[0].size());
+    h.o_sj_term = take(2 * sterm[0].size());
+    h.o_sh_dst = take(4 * sdst[1].size());
+    h.o_sh_term = take(2 * sterm[1].size());
+    h.o_mj_dst = take(4 * mdst[0].size());
+    h.o_mj_info = take(4 * minfo[0].size());
+    h.o_mh_dst = take(4 * mdst[1].size());
+    h.o_mh_info = take(4 * minfo[1].size());
+    h.o_mterms = take(2 * mterms.size());
     h.bytes = (int)off;
     size_t base = blob.size();
     blob.resize(base + off, 0);
@@ -325,8 +343,15 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     put(h.o_gs, gs.data(), 8 * (size_t)nB);
     put(h.o_bs, bs.data(), 8 * (size_t)nB);
     put(h.o_adm, adm.data(), 8 * adm.size());
-    put(h.o_eptr, eptr.data(), 4 * eptr.size());
-    put(h.o_terms, terms.data(), 2 * terms.size());
+    put(h.o_sj_dst, sdst[0].data(), 4 * sdst[0].size());
+    put(h.o_sj_term, sterm[0].data(), 2 * sterm[0].size());
+    put(h.o_sh_dst, sdst[1].data(), 4 * sdst[1].size());
+    put(h.o_sh_term, sterm[1].data(), 2 * sterm[1].size());
+    put(h.o_mj_dst, mdst[0].data(), 4 * mdst[0].size());
+    put(h.o_mj_info, minfo[0].data(), 4 * minfo[0].size());
+    put(h.o_mh_dst, mdst[1].data(), 4 * mdst[1].size());
+    put(h.o_mh_info, minfo[1].data(), 4 * minfo[1].size());
+    put(h.o_mterms, mterms.data(), 2 * mterms.size());
 }
 
 inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
@@ -356,29 +381,50 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         for (int s = 0; s < 4; ++s) rows[s * tt.nB + (i - b0)] = std::move(r4[s]);
     }
     const int nE = (int)tt.ends.size();
-    tt.eptr.push_back(0);
+    // classify entries: single-term gather-stores and multi-term sums
+    struct Multi { uint32_t dst; std::vector<uint16_t> t; };
+    std::vector<Multi> multi[2];
     for (int s = 0; s < 4; ++s) {
+        const int cls = s / 2;                    // 0: J (P, Q rows), 1: H (VA, VM rows)
+        const uint32_t segbit = (s & 1) ? 0x80000000u : 0u;
+        uint32_t local = 0;
         for (int r = 0; r < tt.nB; ++r) {
             const Row& row = rows[s * tt.nB + r];
             tt.rowlen.push_back((int)row.cols.size());
             tt.L[s] += (int)row.cols.size();
-            for (size_t e = 0; e < row.cols.size(); ++e) {
+            for (size_t e = 0; e < row.cols.size(); ++e, ++local) {
                 tt.cols.push_back(row.cols[e]);
+                std::vector<uint16_t> slots;
                 for (int t = row.tptr[e]; t < row.tptr[e + 1]; ++t) {
                     const Sym& y = row.terms[t];
                     int slot;
                     if (y.kind == 0) slot = EQ * end_pos.at(y.a) + y.q;
                     else if (y.kind == 1) slot = EQ * nE + BQ * (y.a - b0) + y.q;
                     else slot = EQ * nE + BQ * tt.nB;
-                    tt.terms.push_back((uint16_t)slot);
+                    slots.push_back((uint16_t)slot);
                 }
-                tt.eptr.push_back((int)tt.terms.size());
+                if (slots.size() == 1) {
+                    tt.sdst[cls].push_back(segbit | local);
+                    tt.sterm[cls].push_back(slots[0]);
+                } else {
+                    multi[cls].push_back(Multi{segbit | local, slots});
+                }
             }
         }
     }
+    for (int cls = 0; cls < 2; ++cls) {
+        std::stable_sort(multi[cls].begin(), multi[cls].end(),
+                         [](const Multi& x, const Multi& y) { return x.t.size() < y.t.size(); });
+        for (const Multi& m : multi[cls]) {
+            if (m.t.size() >= 1024) throw std::runtime_error("entry with >= 1024 duplicate terms");
+            tt.mdst[cls].push_back(m.dst);
+            tt.minfo[cls].push_back(((uint32_t)tt.mterms.size() << 10) | (uint32_t)m.t.size());
+            tt.mterms.insert(tt.mterms.end(), m.t.begin(), m.t.end());
+        }
+    }
     // shared memory = serialised table + quantity array (checked again at upload)
-    size_t approx = 128 + 20 * (size_t)nE + 8 * (size_t)tt.nB + 64 * (size_t)nE + 4 * tt.eptr.size() +
-                    2 * tt.terms.size() + 8 * (size_t)tt.nQ() + 256;
+    size_t approx = 192 + 84 * (size_t)nE + 24 * (size_t)tt.nB + 6 * tt.cols.size() + 2 * tt.mterms.size() +
+                    8 * (size_t)tt.nQ() + 512;
     if (approx > (size_t)SMEM_LIMIT_BYTES)
         throw std::runtime_error("bus degree too high for one tile's shared memory");
     return tt;
