@@ -139,14 +139,11 @@ static void upload(acopf_batch* b) {
     std::vector<uint8_t> blob;
     std::vector<int64_t> table_off(b->tables.size());
     std::vector<int> table_bytes(b->tables.size());
-    size_t max_smem = 0;
     for (size_t i = 0; i < b->tables.size(); ++i) {
         table_off[i] = (int64_t)blob.size();
         b->tables[i].serialise(*b->topos[b->tables[i].topo], blob);
         table_bytes[i] = (int)(blob.size() - table_off[i]);
-        max_smem = std::max(max_smem, (size_t)table_bytes[i] + 8 * (size_t)b->tables[i].nQ());
     }
-    if (max_smem > (size_t)SMEM_LIMIT_BYTES) throw std::runtime_error("tile table exceeds shared memory");
     // stages and removed lists
     std::vector<DStage> ds(S);
     std::vector<int> rem, remsz;
@@ -174,6 +171,7 @@ static void upload(acopf_batch* b) {
     const int G = (int)std::max<int64_t>(1, std::min<int64_t>(32, total_recs / target_items));
     std::vector<DBusItem> items;
     std::vector<DBusRec> recs;
+    size_t max_smem = 0;
     std::map<int, std::vector<int>> by_table;     // table id -> stages (in order)
     std::vector<std::pair<int, int>> tiles;       // (topo, tile)
     for (size_t ti = 0; ti < b->topos.size(); ++ti)
@@ -200,9 +198,14 @@ static void upload(acopf_batch* b) {
                     recs.push_back(r);
                 }
                 items.push_back(it);
+                size_t q, gv, gb, rs, fo, rc;
+                const TileTable& tt = b->tables[kv.first];
+                max_smem = std::max(max_smem, bus_smem_layout(table_bytes[kv.first], tt.nQ(), (int)tt.ends.size(),
+                                                              tt.nB, it.count, &q, &gv, &gb, &rs, &fo, &rc));
             }
         }
     }
+    if (max_smem > (size_t)SMEM_LIMIT_BYTES) throw std::runtime_error("tile working set exceeds shared memory");
     // aux work: generator chunks per stage, then coupling chunks
     std::vector<DAuxItem> aux;
     for (int s = 0; s < S; ++s) {

@@ -143,38 +143,78 @@ __device__ __forceinline__ double hpos(int p, double cpf, double cqf, double cpt
     return v;
 }
 
-// Phase A for one branch end of one stage.
-__device__ __forceinline__ void branch_end(const EvalParams& P, const DStage& S, int nb, const TileView& V,
-                                           int e, double* Q, bool need_j, bool need_h, bool need_c) {
-    const double* va = P.x + S.var_off;
-    const double* vm = va + nb;
+// Per (stage, tile) record, staged in shared memory once per CTA.
+struct SRec {
+    long long var_off, eq_row, ineq_row, pd_off, rem_off;
+    long long oP, oQ, oA, oV, jineq;   // absolute output offsets of the tile's segments
+    double w;
+    int nrem, nb, ng, pad;
+};
+
+constexpr int GV = 10;   // gathered doubles per end: va_f va_t vm_f vm_t mu(Pf Qf Pt Qt) s_f s_t
+constexpr int GB = 5;    // gathered doubles per bus: vm mu_P mu_Q pd qd
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Issue the asynchronous gathers (LDGSTS) of one stage's inputs into shared memory.
+__device__ __forceinline__ void issue_gathers(const EvalParams& P, const SRec& R, const TileView& V, double* Gv,
+                                              double* Gb, int* RS, int* FO, bool need_h, bool need_c) {
+    const TileHdr* H = V.h;
+    const int ne = H->nE, nbt = H->nB, nb = R.nb;
+    const double* x = P.x + R.var_off;
+    const double* mu = P.mult + R.eq_row;
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+        const int f = V.f[e], t = V.t[e], r = V.ridx[e];
+        int rs = r, fo = V.foff[e];
+        if (r >= 0) {
+            for (int i = 0; i < R.nrem; ++i) {
+                if (__ldg(P.rem_ridx + R.rem_off + i) < r) { rs--; fo -= __ldg(P.rem_rowsz + R.rem_off + i); }
+            }
+        }
+        RS[e] = rs;
+        FO[e] = fo;
+        cp_async8(Gv + 0 * ne + e, x + f);
+        cp_async8(Gv + 1 * ne + e, x + t);
+        cp_async8(Gv + 2 * ne + e, x + nb + f);
+        cp_async8(Gv + 3 * ne + e, x + nb + t);
+        if (need_h) {
+            cp_async8(Gv + 4 * ne + e, mu + f);
+            cp_async8(Gv + 5 * ne + e, mu + nb + f);
+            cp_async8(Gv + 6 * ne + e, mu + t);
+            cp_async8(Gv + 7 * ne + e, mu + nb + t);
+            if (r >= 0) {
+                const double* mi = P.mult + R.ineq_row + 2 * rs;
+                cp_async8(Gv + 8 * ne + e, mi);
+                cp_async8(Gv + 9 * ne + e, mi + 1);
+            }
+        }
+    }
+    for (int bl = threadIdx.x; bl < nbt; bl += blockDim.x) {
+        const int i = H->b0 + bl;
+        cp_async8(Gb + 0 * nbt + bl, x + nb + i);
+        if (need_h) {
+            cp_async8(Gb + 1 * nbt + bl, mu + i);
+            cp_async8(Gb + 2 * nbt + bl, mu + nb + i);
+        }
+        if (need_c) {
+            cp_async8(Gb + 3 * nbt + bl, P.pd + R.pd_off + i);
+            cp_async8(Gb + 4 * nbt + bl, P.qd + R.pd_off + i);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Phase A for one branch end of one stage (inputs already gathered in shared memory).
+__device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, const TileView& V, const double* Gv,
+                                           int rs, long long foff, int e, double* Q, bool need_j, bool need_h,
+                                           bool need_c) {
+    const int ne = V.h->nE;
     const int side = V.code[e] & 1;
     const int f = V.f[e], t = V.t[e];
     const int r = V.ridx[e];
-    int rs = r;
-    long long foff = V.foff[e];
-    if (r >= 0) {
-        for (int i = 0; i < S.nrem; ++i) {
-            if (__ldg(P.rem_ridx + S.rem_off + i) < r) { rs--; foff -= __ldg(P.rem_rowsz + S.rem_off + i); }
-        }
-    }
-    // all gathers first (read-only path), so they are in flight together
-    const double vaf = __ldg(va + f), vat = __ldg(va + t);
-    const double vf = __ldg(vm + f), vt = __ldg(vm + t);
-    double mpf = 0.0, mqf = 0.0, mpt = 0.0, mqt = 0.0, sf = 0.0, st = 0.0;
-    if (need_h) {
-        const double* mu = P.mult + S.eq_row;
-        mpf = __ldg(mu + f);
-        mqf = __ldg(mu + nb + f);
-        mpt = __ldg(mu + t);
-        mqt = __ldg(mu + nb + t);
-        if (r >= 0) {
-            const double* mi = P.mult + S.ineq_row + 2 * rs;
-            sf = __ldg(mi);
-            st = __ldg(mi + 1);
-        }
-    }
-    const int ne = V.h->nE;
+    const double vaf = Gv[e], vat = Gv[ne + e], vf = Gv[2 * ne + e], vt = Gv[3 * ne + e];
     const double gff = V.adm[e], bff = V.adm[ne + e], gft = V.adm[2 * ne + e], bft = V.adm[3 * ne + e];
     const double gtf = V.adm[4 * ne + e], btf = V.adm[5 * ne + e], gtt = V.adm[6 * ne + e], btt = V.adm[7 * ne + e];
     const double th = vaf - vat;
@@ -192,7 +232,7 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const DStage& S,
     double* q = Q + EQ * e;
     q[Q_FP] = side ? pt : pf;
     q[Q_FQ] = side ? qt : qf;
-    if (r >= 0 && need_c) P.cons[S.ineq_row + 2 * rs + side] = side ? pt * pt + qt * qt : pf * pf + qf * qf;
+    if (r >= 0 && need_c) P.cons[R.ineq_row + 2 * rs + side] = side ? pt * pt + qt * qt : pf * pf + qf * qf;
     if (!(need_j || need_h)) return;
     double gpf[4], gqf[4], gpt[4], gqt[4];
     gpf[0] = (-vv) * w;  gpf[1] = vv * w;    gpf[2] = (2.0 * gff) * vf + vt * u;   gpf[3] = vf * u;
@@ -213,14 +253,16 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const DStage& S,
             double d[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) d[i] = (0.0 + (2.0 * fp) * gp[i]) + (2.0 * fq) * gq[i];
-            double* out = P.jval + S.jineq_base + foff + (f == t ? 2 : 4) * side;
+            double* out = P.jval + R.jineq + foff + (f == t ? 2 : 4) * side;
             if (f < t) { out[0] = d[0]; out[1] = d[1]; out[2] = d[2]; out[3] = d[3]; }
             else if (f > t) { out[0] = d[1]; out[1] = d[0]; out[2] = d[3]; out[3] = d[2]; }
             else { out[0] = d[0] + d[1]; out[1] = d[2] + d[3]; }
         }
     }
     if (need_h) {
-        const double lpf = -mpf, lqf = -mqf, lpt = -mpt, lqt = -mqt;
+        double sf = 0.0, st = 0.0;
+        if (r >= 0) { sf = Gv[8 * ne + e]; st = Gv[9 * ne + e]; }
+        const double lpf = -Gv[4 * ne + e], lqf = -Gv[5 * ne + e], lpt = -Gv[6 * ne + e], lqt = -Gv[7 * ne + e];
         const double s2f = 2.0 * sf, s2t = 2.0 * st;
         const double cpf = lpf + s2f * pf, cqf = lqf + s2f * qf;
         const double cpt = lpt + s2t * pt, cqt = lqt + s2t * qt;
@@ -245,6 +287,21 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const DStage& S,
     }
 }
 
+// Dynamic shared memory of one bus CTA (must match the host's bus_smem_bytes).
+__host__ __device__ __forceinline__ size_t bus_smem_layout(int table_bytes, int nQ, int nE, int nB, int count,
+                                                           size_t* o_q, size_t* o_gv, size_t* o_gb, size_t* o_rs,
+                                                           size_t* o_fo, size_t* o_rec) {
+    size_t off = (size_t)table_bytes;
+    *o_q = off;   off += 8 * (size_t)nQ;
+    *o_gv = off;  off += 8 * (size_t)GV * nE;
+    *o_gb = off;  off += 8 * (size_t)GB * nB;
+    *o_rs = off;  off += 4 * (size_t)nE;
+    *o_fo = off;  off += 4 * (size_t)nE;
+    off = (off + 15) & ~size_t(15);
+    *o_rec = off; off += sizeof(SRec) * (size_t)count;
+    return off;
+}
+
 __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
@@ -262,6 +319,8 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
             "l"(src), "r"(it.bytes), "r"(b)
             : "memory");
     }
+    // stage records: thread i loads record i while the table is in flight
+    const TileHdr* H = reinterpret_cast<const TileHdr*>(smem);
     __syncthreads();
     {
         const unsigned b = smem_u32(&bar);
@@ -274,8 +333,29 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
                 : "memory");
         }
     }
+    size_t o_q, o_gv, o_gb, o_rs, o_fo, o_rec;
+    bus_smem_layout(H->bytes, H->nQ, H->nE, H->nB, it.count, &o_q, &o_gv, &o_gb, &o_rs, &o_fo, &o_rec);
+    double* Q = reinterpret_cast<double*>(smem + o_q);
+    double* Gv = reinterpret_cast<double*>(smem + o_gv);
+    double* Gb = reinterpret_cast<double*>(smem + o_gb);
+    int* RS = reinterpret_cast<int*>(smem + o_rs);
+    int* FO = reinterpret_cast<int*>(smem + o_fo);
+    SRec* recs = reinterpret_cast<SRec*>(smem + o_rec);
+    for (int i = threadIdx.x; i < it.count; i += blockDim.x) {
+        const DBusRec R = P.bus_recs[it.first + i];
+        const DStage S = P.stages[R.stage];
+        SRec o;
+        o.var_off = S.var_off; o.eq_row = S.eq_row; o.ineq_row = S.ineq_row; o.pd_off = S.pd_off;
+        o.rem_off = S.rem_off; o.nrem = S.nrem; o.w = S.w;
+        o.oP = S.jeq_base + R.jP; o.oQ = S.jeq_base + R.jQ;
+        o.oA = S.h_base + R.hA; o.oV = S.h_base + R.hV;
+        o.jineq = S.jineq_base;
+        o.nb = P.topos[S.topo].nb;
+        o.ng = P.topos[S.topo].ng;
+        o.pad = 0;
+        recs[i] = o;
+    }
     TileView V;
-    const TileHdr* H = reinterpret_cast<const TileHdr*>(smem);
     V.h = H;
     V.code = reinterpret_cast<const int*>(smem + H->o_code);
     V.f = reinterpret_cast<const int*>(smem + H->o_f);
@@ -288,46 +368,52 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
     V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
     V.bs = reinterpret_cast<const double*>(smem + H->o_bs);
     V.adm = reinterpret_cast<const double*>(smem + H->o_adm);
-    double* Q = reinterpret_cast<double*>(smem + H->bytes);
     const unsigned what = P.what;
     const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
     const int qbus = EQ * H->nE;
-    if (threadIdx.x == 0) Q[qbus + BQ * H->nB] = 1.0;
+    const int nbt = H->nB;
+    if (threadIdx.x == 0) Q[qbus + BQ * nbt] = 1.0;
+    __syncthreads();
+    issue_gathers(P, recs[0], V, Gv, Gb, RS, FO, need_h, need_c);
 
     for (int ri = 0; ri < it.count; ++ri) {
-        const DBusRec R = P.bus_recs[it.first + ri];
-        const DStage S = P.stages[R.stage];
-        const int nb = P.topos[S.topo].nb;
-        const int ng = P.topos[S.topo].ng;
-        const double* vm = P.x + S.var_off + nb;
+        const SRec& R = recs[ri];
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
         // ---- A: branch ends ------------------------------------------------
         if (need_j || need_h || need_c)
             for (int e = threadIdx.x; e < H->nE; e += blockDim.x)
-                branch_end(P, S, nb, V, e, Q, need_j, need_h, need_c);
+                branch_end(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c);
         // ---- A2: bus-level terms -----------------------------------------------
-        for (int bl = threadIdx.x; bl < H->nB; bl += blockDim.x) {
+        for (int bl = threadIdx.x; bl < nbt; bl += blockDim.x) {
             const int i = H->b0 + bl;
-            const double vmi = vm[i], gsi = V.gs[bl], bsi = V.bs[bl];
+            const double vmi = Gb[bl], gsi = V.gs[bl], bsi = V.bs[bl];
             double* qb = Q + qbus + BQ * bl;
             qb[0] = (-2.0 * gsi) * vmi;
             qb[1] = (2.0 * bsi) * vmi;
-            if (need_h) {
-                const double* mu = P.mult + S.eq_row;
-                qb[2] = 2.0 * ((-mu[i] * gsi) - (-mu[nb + i] * bsi));
-            }
+            if (need_h) qb[2] = 2.0 * ((-Gb[nbt + bl] * gsi) - (-Gb[2 * nbt + bl] * bsi));
             if (what & W_GRAD) {
-                P.grad[S.var_off + i] = S.w * 0.0;
-                P.grad[S.var_off + nb + i] = S.w * 0.0;
+                P.grad[R.var_off + i] = R.w * 0.0;
+                P.grad[R.var_off + R.nb + i] = R.w * 0.0;
             }
         }
         __syncthreads();
+        // the staging buffers are free again: gather the next stage's inputs
+        // while this stage's balance rows and scatter sums are stored
+        double vm_c = 0.0, pd_c = 0.0, qd_c = 0.0;
+        const int blc = threadIdx.x;
+        if (need_c && blc < nbt) { vm_c = Gb[blc]; pd_c = Gb[3 * nbt + blc]; qd_c = Gb[4 * nbt + blc]; }
+        if (ri + 1 < it.count) {
+            __syncthreads();
+            issue_gathers(P, recs[ri + 1], V, Gv, Gb, RS, FO, need_h, need_c);
+        }
         // ---- B: balance rows, then the scatter-map sums -------------------------
         if (need_c) {
-            const double* pgv = P.x + S.var_off + 2 * nb;
-            const double* qgv = pgv + ng;
-            for (int bl = threadIdx.x; bl < H->nB; bl += blockDim.x) {
+            const double* pgv = P.x + R.var_off + 2 * R.nb;
+            const double* qgv = pgv + R.ng;
+            for (int bl = threadIdx.x; bl < nbt; bl += blockDim.x) {
                 const int i = H->b0 + bl;
-                const double vmi = vm[i];
+                const double vmi = bl == blc ? vm_c : 0.0;
                 double p = 0.0, r = 0.0;
                 for (int e = V.busptr[bl]; e < V.busptr[bl + 1]; ++e) {
                     p = p + Q[EQ * e + Q_FP];
@@ -335,22 +421,22 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
                 }
                 p = p + (V.gs[bl] * vmi) * vmi;
                 r = r - (V.bs[bl] * vmi) * vmi;
-                double cp = -(P.pd[S.pd_off + i] + p);
-                double cq = -(P.qd[S.pd_off + i] + r);
+                double cp = -(pd_c + p);
+                double cq = -(qd_c + r);
                 for (int gi = V.gptr[bl]; gi < V.gptr[bl + 1]; ++gi) {
                     const int g = V.glist[gi];
-                    cp = cp + pgv[g];
-                    cq = cq + qgv[g];
+                    cp = cp + __ldg(pgv + g);
+                    cq = cq + __ldg(qgv + g);
                 }
-                P.cons[S.eq_row + i] = cp;
-                P.cons[S.eq_row + nb + i] = cq;
+                P.cons[R.eq_row + i] = cp;
+                P.cons[R.eq_row + R.nb + i] = cq;
             }
         }
         const unsigned short* mterms = reinterpret_cast<const unsigned short*>(smem + H->o_mterms);
         for (int cls = 0; cls < 2; ++cls) {
             if (cls == 0 ? !need_j : !need_h) continue;
-            double* o0 = cls == 0 ? P.jval + S.jeq_base + R.jP : P.hval + S.h_base + R.hA;
-            double* o1 = cls == 0 ? P.jval + S.jeq_base + R.jQ : P.hval + S.h_base + R.hV;
+            double* o0 = cls == 0 ? P.jval + R.oP : P.hval + R.oA;
+            double* o1 = cls == 0 ? P.jval + R.oQ : P.hval + R.oV;
             const int ns = cls == 0 ? H->nSJ : H->nSH;
             const unsigned* sdst = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_sj_dst : H->o_sh_dst));
             const unsigned short* sterm =
@@ -373,7 +459,6 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
                 o[d & 0x7fffffffu] = v;
             }
         }
-        __syncthreads();
     }
 }
 

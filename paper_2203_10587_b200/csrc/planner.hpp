@@ -51,8 +51,8 @@ constexpr int HSLOT_T[10] = {-1, 0, -1, 1, 2, 3, 4, -1, 5, 6};
 constexpr int POS_OF_SLOT_F[7] = {0, 1, 2, 3, 5, 7, 8};
 constexpr int POS_OF_SLOT_T[7] = {1, 3, 4, 5, 6, 8, 9};
 
-constexpr int TILE_MAX_ENDS = 256;   // soft cap; a single high-degree bus may exceed it
-constexpr int TILE_MAX_BUSES = 128;
+constexpr int TILE_MAX_ENDS = 192;   // soft cap; a single high-degree bus may exceed it
+constexpr int TILE_MAX_BUSES = 96;    // <= kernel block size (one bus per thread)
 constexpr int SMEM_LIMIT_BYTES = 220 * 1024;
 
 // symbolic term: what a COO entry's value is made of
