@@ -246,8 +246,9 @@ static void upload(acopf_batch* b) {
     P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
     b->smem = (max_smem + 127) & ~size_t(127);
     b->aux_smem = sizeof(double) * max_leaf;
-    cuda_check(cudaFuncSetAttribute(acopf_bus_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(bus)");
+    for (auto fn : {acopf_bus_kernel<0u>, acopf_bus_kernel<ACOPF_ALL>})
+        cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(bus)");
     if (b->aux_smem > 48 * 1024)
         cuda_check(cudaFuncSetAttribute(acopf_aux_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)b->aux_smem), "cudaFuncSetAttribute(aux)");
@@ -461,7 +462,8 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
             b->launches++;
         }
         if (bus) {
-            acopf_bus_kernel<<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
+            if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
+            else acopf_bus_kernel<0u><<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
             cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
             b->launches++;
         }

@@ -302,6 +302,7 @@ __host__ __device__ __forceinline__ size_t bus_smem_layout(int table_bytes, int 
     return off;
 }
 
+template <unsigned WHAT>
 __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
@@ -368,7 +369,8 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
     V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
     V.bs = reinterpret_cast<const double*>(smem + H->o_bs);
     V.adm = reinterpret_cast<const double*>(smem + H->o_adm);
-    const unsigned what = P.what;
+    // WHAT != 0: the mask is a compile-time constant (the all-callbacks path)
+    const unsigned what = WHAT ? WHAT : P.what;
     const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
     const int qbus = EQ * H->nE;
     const int nbt = H->nB;

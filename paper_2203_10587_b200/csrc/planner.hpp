@@ -257,8 +257,9 @@ static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
 // per-bus shunts and generator lists, and the scatter map split into classes:
 //   single-term entries  dst (bit 31: Q row / VM row segment, else P / VA)
 //                        + the one quantity slot;
-//   multi-term entries   dst + (first term << 10 | term count), sorted by count
-//                        so a warp runs uniform trip counts.
+//   multi-term entries   dst + (first term << 10 | term count), sorted by
+//                        decreasing count: warps run uniform trip counts and
+//                        the longest sums start first.
 struct TileTable {
     int topo = 0;
     int b0 = 0, nB = 0;
@@ -414,7 +415,7 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     }
     for (int cls = 0; cls < 2; ++cls) {
         std::stable_sort(multi[cls].begin(), multi[cls].end(),
-                         [](const Multi& x, const Multi& y) { return x.t.size() < y.t.size(); });
+                         [](const Multi& x, const Multi& y) { return x.t.size() > y.t.size(); });
         for (const Multi& m : multi[cls]) {
             if (m.t.size() >= 1024) throw std::runtime_error("entry with >= 1024 duplicate terms");
             tt.mdst[cls].push_back(m.dst);
