@@ -99,11 +99,14 @@ struct acopf_batch {
     int obj_mode = 0, n_obj = 0;
     // device
     cudaStream_t stream = nullptr;
-    DevBuf d_topo, d_stage, d_items, d_recs, d_aux, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
+    DevBuf d_topo, d_stage, d_items, d_titems, d_recs, d_aux, d_blob, d_scratch, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
     DevBuf d_cprow, d_cpj, d_cpa, d_cpb, d_cpf, d_objterms, d_counter;
     std::vector<std::unique_ptr<DevBuf>> topo_bufs;
     EvalParams params{};
     size_t smem = 0, aux_smem = 0;
+    int64_t scratch_budget = 24ll << 20;     // bytes of branch scratch per chunk (L2-resident)
+    struct Chunk { int b_first, b_count, t_first, t_count; };
+    std::vector<Chunk> chunks;
     int64_t launches = 0;
     // host staging for eval_host
     DevBuf h_x, h_m, h_obj, h_g, h_c, h_j, h_h;
@@ -120,22 +123,28 @@ static void upload(acopf_batch* b) {
     const int64_t n_coupling = (int64_t)b->cp_row.size();
     if (!b->stream) cuda_check(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "stream");
 
-    // topologies (only what the aux kernel needs; the bus kernel reads tile tables)
+    // topologies
     std::vector<DTopo> dt;
     b->topo_bufs.clear();
     size_t max_leaf = 1;
     for (const Topo* T : b->topos) {
         DTopo d{};
         d.nb = T->nb; d.nbr = T->nbr; d.ng = T->ng; d.nr = T->nr;
+        auto up = [&](const auto& v) {
+            b->topo_bufs.emplace_back(new DevBuf());
+            return b->topo_bufs.back()->upload(v);
+        };
+        d.fo = up(T->fo); d.to = up(T->to); d.adm = up(T->adm); d.ridx = up(T->ridx);
+        std::vector<long long> foff(T->foff.begin(), T->foff.end());
+        d.foff = up(foff);
         std::vector<int> leaf;
         for (size_t l = 0; l < T->leaf_start.size(); ++l) { leaf.push_back(T->leaf_start[l]); leaf.push_back(T->leaf_len[l]); }
-        b->topo_bufs.emplace_back(new DevBuf());
-        d.leaf = b->topo_bufs.back()->upload(leaf);
+        d.leaf = up(leaf);
         d.nleaf = (int)T->leaf_start.size();
         max_leaf = std::max(max_leaf, T->leaf_start.size());
         dt.push_back(d);
     }
-    // blob of tile tables (each 16-byte aligned, sized for one bulk copy)
+    // blob of tile tables (each 16-byte aligned, one bulk copy each)
     std::vector<uint8_t> blob;
     std::vector<int64_t> table_off(b->tables.size());
     std::vector<int> table_bytes(b->tables.size());
@@ -144,6 +153,19 @@ static void upload(acopf_batch* b) {
         b->tables[i].serialise(*b->topos[b->tables[i].topo], blob);
         table_bytes[i] = (int)(blob.size() - table_off[i]);
     }
+    // chunks of consecutive stages whose branch scratch fits the L2 budget
+    const int64_t budget = b->scratch_budget / 8;       // doubles
+    std::vector<int> chunk_begin;
+    std::vector<int64_t> sbase(S, 0);
+    int64_t cur = 0, max_scratch = 1;
+    for (int s = 0; s < S; ++s) {
+        const int64_t need = (int64_t)SQ * b->topos[b->stages[s].topo]->nbr;
+        if (s == 0 || cur + need > budget) { chunk_begin.push_back(s); cur = 0; }
+        sbase[s] = cur;
+        cur += need;
+        max_scratch = std::max(max_scratch, cur);
+    }
+    chunk_begin.push_back(S);
     // stages and removed lists
     std::vector<DStage> ds(S);
     std::vector<int> rem, remsz;
@@ -158,52 +180,61 @@ static void upload(acopf_batch* b) {
         d.cost_off = st.cost_off;
         d.rem_off = (long long)rem.size();
         d.nrem = (int)st.removed_rated.size();
+        d.sbase = sbase[s];
         rem.insert(rem.end(), st.removed_rated.begin(), st.removed_rated.end());
         remsz.insert(remsz.end(), st.removed_rowsz.begin(), st.removed_rowsz.end());
         d.topo = st.topo;
         d.obj_slot = b->obj_slot[s];
         d.w = st.w;
     }
-    // bus work: for every tile, the stages sharing one table, in chunks of G
-    int64_t total_recs = 0;
-    for (const StageInfo& st : b->stages) total_recs += (int64_t)st.table.size();
-    const int64_t target_items = 148 * 2 * 6;
-    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(32, total_recs / target_items));
-    std::vector<DBusItem> items;
-    std::vector<DBusRec> recs;
-    size_t max_smem = 0;
-    std::map<int, std::vector<int>> by_table;     // table id -> stages (in order)
-    std::vector<std::pair<int, int>> tiles;       // (topo, tile)
+    // per chunk: branch items (256 branches of one stage), then tile items
+    std::vector<DBranchItem> bitems;
+    std::vector<DTileItem> titems;
+    std::vector<DTileRec> recs;
+    std::vector<std::pair<int, int>> tiles;        // (topo, tile)
     for (size_t ti = 0; ti < b->topos.size(); ++ti)
         for (size_t t = 0; t < b->base_table[ti].size(); ++t) tiles.push_back({(int)ti, (int)t});
-    // stage-group-major order: CTAs running together share one group's x/mult in L2
-    for (int g0 = 0; g0 < S; g0 += G) {
-        const int g1 = std::min(S, g0 + G);
+    size_t max_smem = 0;
+    b->chunks.clear();
+    std::map<int, std::vector<int>> by_table;
+    for (size_t c = 0; c + 1 < chunk_begin.size(); ++c) {
+        const int s0 = chunk_begin[c], s1 = chunk_begin[c + 1];
+        acopf_batch::Chunk ch{};
+        ch.b_first = (int)bitems.size();
+        for (int s = s0; s < s1; ++s) {
+            const int nbr = b->topos[b->stages[s].topo]->nbr;
+            for (int k = 0; k < nbr; k += BLOCK) bitems.push_back(DBranchItem{s, k});
+        }
+        ch.b_count = (int)bitems.size() - ch.b_first;
+        ch.t_first = (int)titems.size();
         for (auto [topo, t] : tiles) {
             by_table.clear();
-            for (int s = g0; s < g1; ++s)
+            for (int s = s0; s < s1; ++s)
                 if (b->stages[s].topo == topo) by_table[b->stages[s].table[t]].push_back(s);
             for (auto& kv : by_table) {
-                DBusItem it{};
-                it.blob_off = table_off[kv.first];
-                it.bytes = table_bytes[kv.first];
-                it.first = (int)recs.size();
-                it.count = (int)kv.second.size();
-                for (int s : kv.second) {
-                    const StageInfo& st = b->stages[s];
-                    DBusRec r{};
-                    r.stage = s;
-                    r.jP = st.tile_off[4 * t + 0]; r.jQ = st.tile_off[4 * t + 1];
-                    r.hA = st.tile_off[4 * t + 2]; r.hV = st.tile_off[4 * t + 3];
-                    recs.push_back(r);
-                }
-                items.push_back(it);
-                size_t q, gv, gb, rs, fo, rc;
                 const TileTable& tt = b->tables[kv.first];
-                max_smem = std::max(max_smem, bus_smem_layout(table_bytes[kv.first], tt.nQ(), (int)tt.ends.size(),
-                                                              tt.nB, it.count, &q, &gv, &gb, &rs, &fo, &rc));
+                const std::vector<int>& ss = kv.second;
+                for (size_t g = 0; g < ss.size(); g += 32) {
+                    DTileItem it{};
+                    it.blob_off = table_off[kv.first];
+                    it.bytes = table_bytes[kv.first];
+                    it.first = (int)recs.size();
+                    it.count = (int)std::min<size_t>(32, ss.size() - g);
+                    for (size_t j = g; j < g + it.count; ++j) {
+                        const StageInfo& st = b->stages[ss[j]];
+                        DTileRec r{};
+                        r.stage = ss[j];
+                        r.jP = st.tile_off[4 * t + 0]; r.jQ = st.tile_off[4 * t + 1];
+                        r.hA = st.tile_off[4 * t + 2]; r.hV = st.tile_off[4 * t + 3];
+                        recs.push_back(r);
+                    }
+                    titems.push_back(it);
+                    max_smem = std::max(max_smem, tile_smem_bytes(it.bytes, it.count, tt.nB));
+                }
             }
         }
+        ch.t_count = (int)titems.size() - ch.t_first;
+        b->chunks.push_back(ch);
     }
     if (max_smem > (size_t)SMEM_LIMIT_BYTES) throw std::runtime_error("tile working set exceeds shared memory");
     // aux work: generator chunks per stage, then coupling chunks
@@ -221,8 +252,9 @@ static void upload(acopf_batch* b) {
     P = EvalParams{};
     P.topos = b->d_topo.upload(dt);
     P.stages = b->d_stage.upload(ds);
-    P.bus_items = b->d_items.upload(items);
-    P.bus_recs = b->d_recs.upload(recs);
+    P.br_items = b->d_items.upload(bitems);
+    P.tile_items = b->d_titems.upload(titems);
+    P.tile_recs = b->d_recs.upload(recs);
     P.aux_items = b->d_aux.upload(aux);
     P.blob = b->d_blob.upload(blob);
     P.pd = b->d_pd.upload(b->pd);
@@ -238,17 +270,17 @@ static void upload(acopf_batch* b) {
     P.cp_b = reinterpret_cast<const long long*>(b->d_cpb.upload(b->cp_b));
     P.cp_base_first = reinterpret_cast<const signed char*>(b->d_cpf.upload(b->cp_first));
     P.ncp = n_coupling;
-    P.n_bus_items = (int)items.size();
     P.n_aux_items = (int)aux.size();
     P.n_obj = S;
     P.obj_mode = b->obj_mode;
+    P.scratch = static_cast<double*>(b->d_scratch.alloc(sizeof(double) * (size_t)max_scratch));
     P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
     P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
     b->smem = (max_smem + 127) & ~size_t(127);
     b->aux_smem = sizeof(double) * max_leaf;
-    for (auto fn : {acopf_bus_kernel<0u>, acopf_bus_kernel<ACOPF_ALL>})
+    for (auto fn : {acopf_tile_kernel<0u>, acopf_tile_kernel<ACOPF_ALL>})
         cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(bus)");
+                                        (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(tile)");
     if (b->aux_smem > 48 * 1024)
         cuda_check(cudaFuncSetAttribute(acopf_aux_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)b->aux_smem), "cudaFuncSetAttribute(aux)");
@@ -454,18 +486,27 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         P.x = x; P.mult = mult; P.obj_factor = obj_factor; P.what = what;
         P.obj = obj; P.grad = grad; P.cons = cons; P.jval = jval; P.hval = hval;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
-        const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD)) && P.n_bus_items > 0;
         const bool aux = (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
+        const bool branch = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) != 0;
+        const bool tiles = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD)) != 0;
         if (aux) {
             acopf_aux_kernel<<<P.n_aux_items, BLOCK, b->aux_smem, st>>>(P);
             cuda_check(cudaGetLastError(), "acopf_aux_kernel launch");
             b->launches++;
         }
-        if (bus) {
-            if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
-            else acopf_bus_kernel<0u><<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
-            cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
-            b->launches++;
+        for (const auto& ch : b->chunks) {
+            if (branch && ch.b_count) {
+                if (what == ACOPF_ALL) acopf_branch_kernel<ACOPF_ALL><<<ch.b_count, BLOCK, 0, st>>>(P, ch.b_first);
+                else acopf_branch_kernel<0u><<<ch.b_count, BLOCK, 0, st>>>(P, ch.b_first);
+                cuda_check(cudaGetLastError(), "acopf_branch_kernel launch");
+                b->launches++;
+            }
+            if (tiles && ch.t_count) {
+                if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<ch.t_count, BLOCK, b->smem, st>>>(P, ch.t_first);
+                else acopf_tile_kernel<0u><<<ch.t_count, BLOCK, b->smem, st>>>(P, ch.t_first);
+                cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
+                b->launches++;
+            }
         }
     });
 }
