@@ -105,6 +105,7 @@ struct acopf_batch {
     EvalParams params{};
     size_t smem = 0, aux_smem = 0;
     int64_t scratch_budget = 24ll << 20;     // bytes of branch scratch per chunk (L2-resident)
+    size_t tile_group = 1;                   // stages per tile CTA
     struct Chunk { int b_first, b_count, t_first, t_count; };
     std::vector<Chunk> chunks;
     int64_t launches = 0;
@@ -214,12 +215,12 @@ static void upload(acopf_batch* b) {
             for (auto& kv : by_table) {
                 const TileTable& tt = b->tables[kv.first];
                 const std::vector<int>& ss = kv.second;
-                for (size_t g = 0; g < ss.size(); g += 32) {
+                for (size_t g = 0; g < ss.size(); g += b->tile_group) {
                     DTileItem it{};
                     it.blob_off = table_off[kv.first];
                     it.bytes = table_bytes[kv.first];
                     it.first = (int)recs.size();
-                    it.count = (int)std::min<size_t>(32, ss.size() - g);
+                    it.count = (int)std::min<size_t>(b->tile_group, ss.size() - g);
                     for (size_t j = g; j < g + it.count; ++j) {
                         const StageInfo& st = b->stages[ss[j]];
                         DTileRec r{};
