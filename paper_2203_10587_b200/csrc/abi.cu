@@ -75,6 +75,18 @@ struct StageInfo {
     // sizes
     int64_t n = 0, m_eq = 0, m_ineq = 0, nnz_jeq = 0, nnz_jin = 0, nnz_h = 0, hpg_local = 0;
     std::vector<int> tile_off;       // per tile 4 offsets (P, Q, VA, VM), stage-local
+    int rset = -1;                   // removal set (stages with outaged branches)
+};
+
+// Stages that remove the same branches of the same topology share one removal
+// set: which branches sit in patched tiles (their direct positions change), and
+// the piecewise-constant position shift of every other direct entry.
+struct RemSet {
+    int topo = 0;
+    std::vector<int> removed;
+    std::vector<int> patched_tiles;
+    std::vector<int> tile_off;       // stage tile offsets (as in StageInfo)
+    std::vector<int> table;          // per tile table id
 };
 }  // namespace
 
@@ -89,6 +101,10 @@ struct acopf_batch {
     std::vector<TileTable> tables;
     std::map<std::pair<int, std::pair<std::vector<int>, int>>, int> patch_cache;
     std::vector<StageInfo> stages;
+    std::vector<RemSet> rsets;
+    std::map<std::pair<int, std::vector<int>>, int> rset_index;
+    std::vector<std::vector<int>> base_off;      // topo -> per tile 4 offsets (no removals)
+    std::vector<std::vector<int>> dpos_base;     // topo -> [slot * nbr + k] direct position or -1
     std::vector<double> pd, qd, ca, cb, cc;
     // layout
     bool laid_out = false, uploaded = false;
@@ -99,7 +115,7 @@ struct acopf_batch {
     int obj_mode = 0, n_obj = 0;
     // device
     cudaStream_t stream = nullptr;
-    DevBuf d_topo, d_stage, d_items, d_titems, d_recs, d_aux, d_blob, d_scratch, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
+    DevBuf d_topo, d_stage, d_items, d_titems, d_recs, d_aux, d_blob, d_scratch, d_rsets, d_pidx, d_ppos, d_bpt, d_bpd, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
     DevBuf d_cprow, d_cpj, d_cpa, d_cpb, d_cpf, d_objterms, d_counter;
     std::vector<std::unique_ptr<DevBuf>> topo_bufs;
     EvalParams params{};
@@ -145,14 +161,81 @@ static void upload(acopf_batch* b) {
         max_leaf = std::max(max_leaf, T->leaf_start.size());
         dt.push_back(d);
     }
+    // scratch quantities each topology's tile kernel reads (flows always)
+    std::vector<unsigned> qmask(b->topos.size(), (1u << S_PF) | (1u << S_QF) | (1u << S_PT) | (1u << S_QT));
+    for (const TileTable& tt : b->tables) qmask[tt.topo] |= tt.qused;
+    for (size_t i = 0; i < dt.size(); ++i) {
+        dt[i].qmask = qmask[i];
+        b->topo_bufs.emplace_back(new DevBuf());
+        dt[i].dpos = b->topo_bufs.back()->upload(b->dpos_base[i]);
+    }
     // blob of tile tables (each 16-byte aligned, one bulk copy each)
     std::vector<uint8_t> blob;
     std::vector<int64_t> table_off(b->tables.size());
     std::vector<int> table_bytes(b->tables.size());
     for (size_t i = 0; i < b->tables.size(); ++i) {
         table_off[i] = (int64_t)blob.size();
-        b->tables[i].serialise(*b->topos[b->tables[i].topo], blob);
+        b->tables[i].serialise(*b->topos[b->tables[i].topo], qmask[b->tables[i].topo], blob);
         table_bytes[i] = (int)(blob.size() - table_off[i]);
+    }
+    // removal sets: patch rows for branches with direct entries in patched tiles,
+    // and per-segment shift breakpoints for all other direct entries
+    std::vector<DRemSet> drs;
+    std::vector<int> pidx_all, ppos_all, bpt_all, bpd_all;
+    for (const RemSet& R : b->rsets) {
+        const Topo& T = *b->topos[R.topo];
+        const std::vector<int>& base = b->base_off[R.topo];
+        const int ntile = (int)b->base_table[R.topo].size();
+        DRemSet d{};
+        d.pidx_off = (long long)pidx_all.size();
+        d.ppos_off = (long long)ppos_all.size();
+        std::vector<int> pidx(T.nbr, -1), ppos;
+        for (int k : R.removed) pidx[k] = -2;
+        std::vector<char> patched(ntile, 0);
+        for (int t : R.patched_tiles) patched[t] = 1;
+        auto tile_of_bus = [&](int bus) {
+            return int(std::upper_bound(T.tile_b0.begin(), T.tile_b0.end(), bus) - T.tile_b0.begin()) - 1;
+        };
+        // every live branch touching a patched tile gets a patch row: its slots in
+        // patched tiles start as "not direct", the rest as "base + shift"
+        for (int t : R.patched_tiles) {
+            for (int i = T.tile_b0[t]; i < T.tile_b0[t + 1]; ++i) {
+                for (int side = 0; side < 2; ++side) {
+                    const std::vector<int>& ptr = side ? T.to_ptr : T.from_ptr;
+                    const std::vector<int>& lst = side ? T.to_list : T.from_list;
+                    for (int p = ptr[i]; p < ptr[i + 1]; ++p) {
+                        const int k = lst[p];
+                        if (pidx[k] == -2) continue;
+                        if (pidx[k] == -1) {
+                            pidx[k] = (int)(ppos.size() / NDIRECT);
+                            ppos.insert(ppos.end(), NDIRECT, -2);
+                        }
+                        for (int sl = 0; sl < NDIRECT; ++sl) {
+                            const int rowbus = DIRECT_SIDE[sl] == 0 ? T.fo[k] : T.to[k];
+                            if (patched[tile_of_bus(rowbus)]) ppos[(size_t)pidx[k] * NDIRECT + sl] = -1;
+                        }
+                    }
+                }
+            }
+        }
+        for (int t : R.patched_tiles)
+            for (const auto& dr : b->tables[R.table[t]].direct)
+                ppos[(size_t)pidx[dr.k] * NDIRECT + dr.slot] = R.tile_off[4 * t + dr.seg] + dr.lpos;
+        for (int sg = 0; sg < 4; ++sg) {
+            d.bp_off[sg] = (int)bpt_all.size();
+            bpt_all.push_back(base[sg]);
+            bpd_all.push_back(R.tile_off[sg] - base[sg]);
+            for (int t : R.patched_tiles) {
+                if (t + 1 >= ntile) continue;
+                bpt_all.push_back(base[4 * (t + 1) + sg]);
+                bpd_all.push_back(R.tile_off[4 * (t + 1) + sg] - base[4 * (t + 1) + sg]);
+            }
+            d.bp_n[sg] = (int)bpt_all.size() - d.bp_off[sg];
+            if (d.bp_n[sg] > MAXBP) throw std::runtime_error("too many patched tiles in one stage");
+        }
+        pidx_all.insert(pidx_all.end(), pidx.begin(), pidx.end());
+        ppos_all.insert(ppos_all.end(), ppos.begin(), ppos.end());
+        drs.push_back(d);
     }
     // chunks of consecutive stages whose branch scratch fits the L2 budget
     const int64_t budget = b->scratch_budget / 8;       // doubles
@@ -160,7 +243,7 @@ static void upload(acopf_batch* b) {
     std::vector<int64_t> sbase(S, 0);
     int64_t cur = 0, max_scratch = 1;
     for (int s = 0; s < S; ++s) {
-        const int64_t need = (int64_t)SQ * b->topos[b->stages[s].topo]->nbr;
+        const int64_t need = (int64_t)__builtin_popcount(qmask[b->stages[s].topo]) * b->topos[b->stages[s].topo]->nbr;
         if (s == 0 || cur + need > budget) { chunk_begin.push_back(s); cur = 0; }
         sbase[s] = cur;
         cur += need;
@@ -186,6 +269,7 @@ static void upload(acopf_batch* b) {
         remsz.insert(remsz.end(), st.removed_rowsz.begin(), st.removed_rowsz.end());
         d.topo = st.topo;
         d.obj_slot = b->obj_slot[s];
+        d.rset = st.rset;
         d.w = st.w;
     }
     // per chunk: branch items (256 branches of one stage), then tile items
@@ -265,6 +349,11 @@ static void upload(acopf_batch* b) {
     P.cc = b->d_cc.upload(b->cc);
     P.rem_ridx = b->d_rem.upload(rem);
     P.rem_rowsz = b->d_remsz.upload(remsz);
+    P.rsets = b->d_rsets.upload(drs);
+    P.patch_idx = b->d_pidx.upload(pidx_all);
+    P.patch_pos = b->d_ppos.upload(ppos_all);
+    P.bp_thr = b->d_bpt.upload(bpt_all);
+    P.bp_dl = b->d_bpd.upload(bpd_all);
     P.cp_row = reinterpret_cast<const long long*>(b->d_cprow.upload(b->cp_row));
     P.cp_jpos = reinterpret_cast<const long long*>(b->d_cpj.upload(b->cp_jpos));
     P.cp_a = reinterpret_cast<const long long*>(b->d_cpa.upload(b->cp_a));
@@ -345,6 +434,22 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
                 ids.push_back((int)B->tables.size() - 1);
             }
             B->base_table.push_back(ids);
+        }
+        for (int i = 0; i < n_topos; ++i) {
+            const Topo& T = *B->topos[i];
+            const std::vector<int>& ids = B->base_table[i];
+            std::vector<int> off(4 * ids.size());
+            int64_t tot[4] = {0, 0, 0, 0};
+            for (int id : ids) for (int sg = 0; sg < 4; ++sg) tot[sg] += B->tables[id].L[sg];
+            int64_t acc[4] = {0, tot[0], 0, tot[2]};
+            for (size_t t = 0; t < ids.size(); ++t)
+                for (int sg = 0; sg < 4; ++sg) { off[4 * t + sg] = (int)acc[sg]; acc[sg] += B->tables[ids[t]].L[sg]; }
+            std::vector<int> dpos((size_t)NDIRECT * T.nbr, -1);
+            for (size_t t = 0; t < ids.size(); ++t)
+                for (const auto& d : B->tables[ids[t]].direct)
+                    dpos[(size_t)d.slot * T.nbr + d.k] = off[4 * t + d.seg] + d.lpos;
+            B->base_off.push_back(off);
+            B->dpos_base.push_back(dpos);
         }
         B->pd.assign(pd, pd + n_load_values);
         B->qd.assign(qd, qd + n_load_values);
@@ -428,6 +533,21 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
             S.nnz_h = LA + LV + T.ng;
             if (S.nnz_jeq + S.nnz_jin >= (1LL << 31) || S.nnz_h >= (1LL << 31))
                 throw std::runtime_error("stage too large for 32-bit offsets");
+            if (!S.removed.empty()) {
+                auto key = std::make_pair(S.topo, S.removed);
+                auto it = B->rset_index.find(key);
+                if (it == B->rset_index.end()) {
+                    RemSet R;
+                    R.topo = S.topo;
+                    R.removed = S.removed;
+                    R.patched_tiles = touched;
+                    R.tile_off = S.tile_off;
+                    R.table = S.table;
+                    B->rsets.push_back(R);
+                    it = B->rset_index.emplace(key, (int)B->rsets.size() - 1).first;
+                }
+                S.rset = it->second;
+            }
         }
         *out = B.release();
     });

@@ -41,15 +41,23 @@ struct DTopo {
     const double* adm;        // 8 per branch (AoS): gff bff gft bft gtf btf gtt btt
     const int* ridx;          // rated index or -1
     const long long* foff;    // base offset of each rated branch's Sf row in the ineq J block
+    const int* dpos;          // [slot * nbr + k] stage-local position of a direct entry, or -1
     const int* leaf;          // (start, len) pairs of the pairwise sum over ng
     int nleaf;
-    int pad;
+    unsigned qmask;           // scratch quantities the tile kernel reads (compact rows)
+};
+
+constexpr int MAXBP = 32;     // position-shift breakpoints per segment and removal set
+
+struct DRemSet {              // shared by the stages that remove the same branches
+    long long pidx_off, ppos_off;
+    int bp_off[4], bp_n[4];
 };
 
 struct DStage {
     long long var_off, eq_row, ineq_row, jeq_base, jineq_base, h_base;
     long long hpg_local, pd_off, cost_off, rem_off, sbase;
-    int nrem, topo, obj_slot, pad;
+    int nrem, topo, obj_slot, rset;
     double w;
 };
 
@@ -86,6 +94,11 @@ struct EvalParams {
     const double* cc;
     const int* rem_ridx;      // removed rated indices per stage (sorted)
     const int* rem_rowsz;
+    const DRemSet* rsets;
+    const int* patch_idx;     // per removal set and branch: -1 base, -2 removed, >= 0 patch row
+    const int* patch_pos;     // per patch row: NDIRECT positions (-1 none, -2 base + shift)
+    const int* bp_thr;        // breakpoints: base position thresholds and shifts
+    const int* bp_dl;
     const long long* cp_row;
     const long long* cp_jpos;
     const long long* cp_a;
@@ -117,6 +130,15 @@ constexpr int CP_CHUNK = 1024;
 __host__ __device__ constexpr int pos_a(int p) { return p < 4 ? 0 : (p < 7 ? 1 : (p < 9 ? 2 : 3)); }
 __host__ __device__ constexpr int pos_b(int p) { return p < 4 ? p : (p < 7 ? p - 3 : (p < 9 ? p - 5 : 3)); }
 
+// planner.hpp's DIRECT_Q / DIRECT_SEG as constexpr functions (device-usable)
+__host__ __device__ constexpr int direct_q(int d) {
+    return d < 8 ? (d < 4 ? S_JPF + (d & 1 ? 3 : 1) + (d >= 2 ? 4 : 0) : S_JPT + (d & 1 ? 2 : 0) + (d >= 6 ? 4 : 0))
+                 : S_H + (d < 10 ? 1 : d < 12 ? 3 : d < 14 ? 5 : 8);
+}
+__host__ __device__ constexpr int direct_seg(int d) {
+    return d < 8 ? ((d >> 1) & 1) : (d == 11 || d == 13 || d == 14 || d == 15 ? 3 : 2);
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -131,13 +153,30 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 
 template <unsigned WHAT>
 __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P, int item0) {
+    __shared__ int s_thr[4][MAXBP], s_dl[4][MAXBP], s_n[4];
     const DBranchItem it = P.br_items[item0 + blockIdx.x];
     const DStage S = P.stages[it.stage];
     const DTopo T = P.topos[S.topo];
     const int k = it.first + threadIdx.x;
-    if (k >= T.nbr) return;
     const unsigned what = WHAT ? WHAT : P.what;
     const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
+    int pidx = -1;
+    const int* ppos = nullptr;
+    if (S.rset >= 0) {
+        const DRemSet R = P.rsets[S.rset];
+        if (threadIdx.x < 4) s_n[threadIdx.x] = R.bp_n[threadIdx.x];
+        for (int i = threadIdx.x; i < 4 * MAXBP; i += blockDim.x) {
+            const int sg = i / MAXBP, j = i % MAXBP;
+            if (j < R.bp_n[sg]) {
+                s_thr[sg][j] = __ldg(P.bp_thr + R.bp_off[sg] + j);
+                s_dl[sg][j] = __ldg(P.bp_dl + R.bp_off[sg] + j);
+            }
+        }
+        __syncthreads();
+        if (k < T.nbr) pidx = __ldg(P.patch_idx + R.pidx_off + k);
+        ppos = P.patch_pos + R.ppos_off;
+    }
+    if (k >= T.nbr || pidx == -2) return;              // past the end, or outaged in this stage
     const int f = __ldg(T.fo + k), t = __ldg(T.to + k);
     const int r = __ldg(T.ridx + k);
     const double* va = P.x + S.var_off;
@@ -155,7 +194,6 @@ __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P,
         foff = __ldg(T.foff + r);
         for (int i = 0; i < S.nrem; ++i) {
             const int q = __ldg(P.rem_ridx + S.rem_off + i);
-            if (q == r) return;                       // this rated branch is outaged in the stage
             if (q < r) { rs--; foff -= __ldg(P.rem_rowsz + S.rem_off + i); }
         }
     }
@@ -171,6 +209,27 @@ __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P,
             st = __ldg(P.mult + S.ineq_row + 2 * rs + 1);
         }
     }
+    // direct positions: the base layout, or this stage's patch row; entries outside
+    // patched tiles move by the removal set's piecewise-constant shift
+    int dp[NDIRECT];
+#pragma unroll
+    for (int d = 0; d < NDIRECT; ++d) {
+        int pos = __ldg(T.dpos + (long long)d * T.nbr + k);
+        bool shift = S.rset >= 0;
+        if (pidx >= 0) {
+            const int pp = __ldg(ppos + 16LL * pidx + d);
+            if (pp != -2) { pos = pp; shift = false; }
+        }
+        if (shift && pos >= 0) {
+            const int sg = direct_seg(d);
+            int dl = 0;
+            for (int j = 0; j < s_n[sg]; ++j)
+                if (pos >= s_thr[sg][j]) dl = s_dl[sg][j];
+            pos += dl;
+        }
+        dp[d] = pos;
+    }
+
     const double th = vaf - vat;
     double sn, cs;
     acc_sincos(th, &sn, &cs);
@@ -185,10 +244,14 @@ __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P,
     const double qt = ((-btt) * vt) * vt + vv * w2;
     double* sc = P.scratch + S.sbase + k;
     const long long nbr = T.nbr;
-    sc[S_PF * nbr] = pf;
-    sc[S_QF * nbr] = qf;
-    sc[S_PT * nbr] = pt;
-    sc[S_QT * nbr] = qt;
+    const unsigned qm = T.qmask;
+    auto put = [&](int q, double v) {
+        if ((qm >> q) & 1u) __stcg(sc + (long long)__popc(qm & ((1u << q) - 1u)) * nbr, v);
+    };
+    put(S_PF, pf);
+    put(S_QF, qf);
+    put(S_PT, pt);
+    put(S_QT, qt);
     if (r >= 0 && need_c) {
         st_stream(P.cons + S.ineq_row + 2 * rs, pf * pf + qf * qf);
         st_stream(P.cons + S.ineq_row + 2 * rs + 1, pt * pt + qt * qt);
@@ -200,33 +263,40 @@ __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P,
     gpt[0] = vv * w2;    gpt[1] = (-vv) * w2; gpt[2] = vt * u2; gpt[3] = (2.0 * gtt) * vt + vf * u2;
     gqt[0] = (-vv) * u2; gqt[1] = vv * u2;   gqt[2] = vt * w2; gqt[3] = (-2.0 * btt) * vt + vf * w2;
     if (need_j) {
+        double jv[16];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            sc[(S_JPF + i) * nbr] = -gpf[i];
-            sc[(S_JQF + i) * nbr] = -gqf[i];
-            sc[(S_JPT + i) * nbr] = -gpt[i];
-            sc[(S_JQT + i) * nbr] = -gqt[i];
+            jv[S_JPF + i] = -gpf[i];
+            jv[S_JQF + i] = -gqf[i];
+            jv[S_JPT + i] = -gpt[i];
+            jv[S_JQT + i] = -gqt[i];
         }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) put(q, jv[q]);
+        double* jo = P.jval + S.jeq_base;
+#pragma unroll
+        for (int d = 0; d < 8; ++d)
+            if (dp[d] >= 0) st_stream(jo + dp[d], jv[direct_q(d)]);
         if (r >= 0) {
             // dSf = (0 + 2 pf gpf) + 2 qf gqf (builtin sum order), St likewise
-            double d[8];
+            double dd[8];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                d[i] = (0.0 + (2.0 * pf) * gpf[i]) + (2.0 * qf) * gqf[i];
-                d[4 + i] = (0.0 + (2.0 * pt) * gpt[i]) + (2.0 * qt) * gqt[i];
+                dd[i] = (0.0 + (2.0 * pf) * gpf[i]) + (2.0 * qf) * gqf[i];
+                dd[4 + i] = (0.0 + (2.0 * pt) * gpt[i]) + (2.0 * qt) * gqt[i];
             }
             double* out = P.jval + S.jineq_base + foff;
             if (f < t) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) st_stream(out + i, d[i]);
+                for (int i = 0; i < 8; ++i) st_stream(out + i, dd[i]);
             } else if (f > t) {
-                st_stream(out + 0, d[1]); st_stream(out + 1, d[0]); st_stream(out + 2, d[3]); st_stream(out + 3, d[2]);
-                st_stream(out + 4, d[5]); st_stream(out + 5, d[4]); st_stream(out + 6, d[7]); st_stream(out + 7, d[6]);
+                st_stream(out + 0, dd[1]); st_stream(out + 1, dd[0]); st_stream(out + 2, dd[3]); st_stream(out + 3, dd[2]);
+                st_stream(out + 4, dd[5]); st_stream(out + 5, dd[4]); st_stream(out + 6, dd[7]); st_stream(out + 7, dd[6]);
             } else {
-                st_stream(out, d[0] + d[1]);
-                st_stream(out + 1, d[2] + d[3]);
-                st_stream(out + 2, d[4] + d[5]);
-                st_stream(out + 3, d[6] + d[7]);
+                st_stream(out, dd[0] + dd[1]);
+                st_stream(out + 1, dd[2] + dd[3]);
+                st_stream(out + 2, dd[4] + dd[5]);
+                st_stream(out + 3, dd[6] + dd[7]);
             }
         }
     }
@@ -244,6 +314,7 @@ __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P,
         const double hqf[10] = {-vvw, vvw, vtu, vfu, -vvw, -vtu, -vfu, -(2.0 * bff), w, z};
         const double hpt[10] = {-vvu2, vvu2, vtw2, vfw2, -vvu2, -vtw2, -vfw2, z, u2, 2.0 * gtt};
         const double hqt[10] = {-vvw2, vvw2, -vtu2, -vfu2, -vvw2, vtu2, vfu2, z, w2, -(2.0 * btt)};
+        double hv[10];
 #pragma unroll
         for (int p = 0; p < 10; ++p) {
             const int a = pos_a(p), b = pos_b(p);
@@ -252,8 +323,13 @@ __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P,
             v = v + cqt * hqt[p];
             v = v + s2f * (gpf[a] * gpf[b] + gqf[a] * gqf[b]);
             v = v + s2t * (gpt[a] * gpt[b] + gqt[a] * gqt[b]);
-            sc[(S_H + p) * nbr] = v;
+            hv[p] = v;
+            put(S_H + p, v);
         }
+        double* ho = P.hval + S.h_base;
+#pragma unroll
+        for (int d = 8; d < NDIRECT; ++d)
+            if (dp[d] >= 0) st_stream(ho + dp[d], hv[direct_q(d) - S_H]);
     }
 }
 
@@ -264,7 +340,8 @@ struct SRec {                 // per (stage, tile) record, staged in shared memo
     long long var_off, eq_row, pd_off, sbase;
     long long oP, oQ, oA, oV;
     double w;
-    int nb, ng, nbr, pad;
+    int nb, ng, nbr;
+    unsigned qmask;
 };
 
 __device__ __forceinline__ double term(const double* sc, const double* Bq, unsigned ref) {
@@ -302,7 +379,7 @@ __global__ void __launch_bounds__(BLOCK) acopf_tile_kernel(const EvalParams P, i
         o.nb = P.topos[S.topo].nb;
         o.ng = P.topos[S.topo].ng;
         o.nbr = P.topos[S.topo].nbr;
-        o.pad = 0;
+        o.qmask = P.topos[S.topo].qmask;
         recs[i] = o;
     }
     __syncthreads();
@@ -353,12 +430,14 @@ __global__ void __launch_bounds__(BLOCK) acopf_tile_kernel(const EvalParams P, i
             if (need_c) {
                 // p_i: from-end pf (ascending branch), then to-end pt, then the shunt (acopf.py:256-263)
                 double p = 0.0, r = 0.0;
+                const long long cpf = __popc(R.qmask & ((1u << S_PF) - 1u)), cqf = cpf + 1;
+                const long long cpt = cpf + 2, cqt = cpf + 3;   // S_PF..S_QT are consecutive and always kept
                 for (int e = busptr[bl]; e < busptr[bl + 1]; ++e) {
                     const int c = code[e];
                     const long long kk = c >> 1;
                     const int side = c & 1;
-                    p = p + __ldcg(sc + (side ? S_PT : S_PF) * nbr + kk);
-                    r = r + __ldcg(sc + (side ? S_QT : S_QF) * nbr + kk);
+                    p = p + __ldcg(sc + (side ? cpt : cpf) * nbr + kk);
+                    r = r + __ldcg(sc + (side ? cqt : cqf) * nbr + kk);
                 }
                 p = p + (gsi * vmi) * vmi;
                 r = r - (bsi * vmi) * vmi;

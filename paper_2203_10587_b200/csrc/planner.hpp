@@ -256,6 +256,24 @@ inline int scratch_q(int side, int q) {
     return side ? S_QT : S_QF;
 }
 
+// Direct slots: the 16 off-diagonal CSR entries every (non-parallel,
+// non-self-loop) branch owns alone.  The branch kernel stores them in place;
+// only the remaining (diagonal / duplicate-summed / constant) entries go
+// through the tile kernel.  slot -> (scratch quantity, end owning the term,
+// row segment 0 P | 1 Q | 2 VA | 3 VM).
+constexpr int NDIRECT = 16;
+constexpr int DIRECT_Q[NDIRECT] = {S_JPF + 1, S_JPF + 3, S_JQF + 1, S_JQF + 3, S_JPT + 0, S_JPT + 2,
+                                   S_JQT + 0, S_JQT + 2, S_H + 1, S_H + 1, S_H + 3, S_H + 3,
+                                   S_H + 5, S_H + 5, S_H + 8, S_H + 8};
+constexpr int DIRECT_SIDE[NDIRECT] = {0, 0, 0, 0, 1, 1, 1, 1, 0, 1, 0, 1, 1, 0, 0, 1};
+constexpr int DIRECT_SEG[NDIRECT] = {0, 0, 1, 1, 0, 0, 1, 1, 2, 2, 2, 3, 2, 3, 3, 3};
+
+inline int direct_slot(int q, int side) {
+    for (int d = 0; d < NDIRECT; ++d)
+        if (DIRECT_Q[d] == q && DIRECT_SIDE[d] == side) return d;
+    return -1;
+}
+
 // ---------------------------------------------------------------------------
 // Tile tables (serialised into one device blob, bulk-copied to shared memory)
 
@@ -289,13 +307,29 @@ struct TileTable {
     std::vector<uint32_t> mdst[2];
     std::vector<uint32_t> minfo[2];
     std::vector<uint32_t> mref;
+    struct Direct { int k, slot, seg, lpos; };
+    std::vector<Direct> direct;   // entries the branch kernel stores in place (host only)
+    unsigned qused = 0;           // scratch quantities the table references
     int nBQ() const { return BQ * nB + 1; }
-    void serialise(const Topo& T, std::vector<uint8_t>& blob) const;
+    void serialise(const Topo& T, unsigned qmask, std::vector<uint8_t>& blob) const;
 };
+
+// compact scratch row of quantity q under the topology's mask
+inline int compact_q(unsigned qmask, int q) { return __builtin_popcount(qmask & ((1u << q) - 1u)); }
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) const {
+inline void TileTable::serialise(const Topo& T, unsigned qmask, std::vector<uint8_t>& blob) const {
+    // scratch references were built as q * nbr + k; re-index to the compact rows
+    auto remap = [&](std::vector<uint32_t> v) {
+        for (auto& r : v)
+            if (!(r & 0x80000000u)) {
+                uint32_t q = r / (uint32_t)T.nbr, k = r % (uint32_t)T.nbr;
+                r = (uint32_t)compact_q(qmask, (int)q) * (uint32_t)T.nbr + k;
+            }
+        return v;
+    };
+    const std::vector<uint32_t> sref0 = remap(sref[0]), sref1 = remap(sref[1]), mref_c = remap(mref);
     std::vector<int> gptr(1, 0), glist;
     std::vector<double> gs(nB), bs(nB);
     for (int bl = 0; bl < nB; ++bl) {
@@ -341,14 +375,14 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     put(h.o_gs, gs.data(), 8 * (size_t)nB);
     put(h.o_bs, bs.data(), 8 * (size_t)nB);
     put(h.o_sj_dst, sdst[0].data(), 4 * sdst[0].size());
-    put(h.o_sj_ref, sref[0].data(), 4 * sref[0].size());
+    put(h.o_sj_ref, sref0.data(), 4 * sref0.size());
     put(h.o_sh_dst, sdst[1].data(), 4 * sdst[1].size());
-    put(h.o_sh_ref, sref[1].data(), 4 * sref[1].size());
+    put(h.o_sh_ref, sref1.data(), 4 * sref1.size());
     put(h.o_mj_dst, mdst[0].data(), 4 * mdst[0].size());
     put(h.o_mj_info, minfo[0].data(), 4 * minfo[0].size());
     put(h.o_mh_dst, mdst[1].data(), 4 * mdst[1].size());
     put(h.o_mh_info, minfo[1].data(), 4 * minfo[1].size());
-    put(h.o_mref, mref.data(), 4 * mref.size());
+    put(h.o_mref, mref_c.data(), 4 * mref_c.size());
 }
 
 inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
@@ -381,12 +415,23 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             tt.L[s] += (int)row.cols.size();
             for (size_t e = 0; e < row.cols.size(); ++e, ++local) {
                 tt.cols.push_back(row.cols[e]);
+                if (row.tptr[e + 1] - row.tptr[e] == 1 && row.terms[row.tptr[e]].kind == 0) {
+                    const Sym& y = row.terms[row.tptr[e]];
+                    const int d = direct_slot(scratch_q(y.a & 1, y.q), y.a & 1);
+                    if (d >= 0 && DIRECT_SEG[d] == s) {
+                        tt.direct.push_back(TileTable::Direct{y.a >> 1, d, s, (int)local});
+                        continue;
+                    }
+                }
                 std::vector<uint32_t> refs;
                 for (int t = row.tptr[e]; t < row.tptr[e + 1]; ++t) {
                     const Sym& y = row.terms[t];
                     uint32_t ref;
-                    if (y.kind == 0) ref = (uint32_t)(scratch_q(y.a & 1, y.q) * T.nbr + (y.a >> 1));
-                    else if (y.kind == 1) ref = bus_bit | (uint32_t)(BQ * (y.a - b0) + y.q);
+                    if (y.kind == 0) {
+                        const int q = scratch_q(y.a & 1, y.q);
+                        tt.qused |= 1u << q;
+                        ref = (uint32_t)(q * T.nbr + (y.a >> 1));
+                    } else if (y.kind == 1) ref = bus_bit | (uint32_t)(BQ * (y.a - b0) + y.q);
                     else ref = bus_bit | (uint32_t)(BQ * tt.nB);
                     refs.push_back(ref);
                 }
