@@ -75,18 +75,6 @@ struct StageInfo {
     // sizes
     int64_t n = 0, m_eq = 0, m_ineq = 0, nnz_jeq = 0, nnz_jin = 0, nnz_h = 0, hpg_local = 0;
     std::vector<int> tile_off;       // per tile 4 offsets (P, Q, VA, VM), stage-local
-    int rset = -1;                   // removal set (stages with outaged branches)
-};
-
-// Stages that remove the same branches of the same topology share one removal
-// set: which branches sit in patched tiles (their direct positions change), and
-// the piecewise-constant position shift of every other direct entry.
-struct RemSet {
-    int topo = 0;
-    std::vector<int> removed;
-    std::vector<int> patched_tiles;
-    std::vector<int> tile_off;       // stage tile offsets (as in StageInfo)
-    std::vector<int> table;          // per tile table id
 };
 }  // namespace
 
@@ -101,10 +89,6 @@ struct acopf_batch {
     std::vector<TileTable> tables;
     std::map<std::pair<int, std::pair<std::vector<int>, int>>, int> patch_cache;
     std::vector<StageInfo> stages;
-    std::vector<RemSet> rsets;
-    std::map<std::pair<int, std::vector<int>>, int> rset_index;
-    std::vector<std::vector<int>> base_off;      // topo -> per tile 4 offsets (no removals)
-    std::vector<std::vector<int>> dpos_base;     // topo -> [slot * nbr + k] direct position or -1
     std::vector<double> pd, qd, ca, cb, cc;
     // layout
     bool laid_out = false, uploaded = false;
@@ -115,15 +99,11 @@ struct acopf_batch {
     int obj_mode = 0, n_obj = 0;
     // device
     cudaStream_t stream = nullptr;
-    DevBuf d_topo, d_stage, d_items, d_titems, d_recs, d_aux, d_blob, d_scratch, d_rsets, d_pidx, d_ppos, d_bpt, d_bpd, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
+    DevBuf d_topo, d_stage, d_items, d_recs, d_aux, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
     DevBuf d_cprow, d_cpj, d_cpa, d_cpb, d_cpf, d_objterms, d_counter;
     std::vector<std::unique_ptr<DevBuf>> topo_bufs;
     EvalParams params{};
     size_t smem = 0, aux_smem = 0;
-    int64_t scratch_budget = 24ll << 20;     // bytes of branch scratch per chunk (L2-resident)
-    size_t tile_group = 1;                   // stages per tile CTA
-    struct Chunk { int b_first, b_count, t_first, t_count; };
-    std::vector<Chunk> chunks;
     int64_t launches = 0;
     // host staging for eval_host
     DevBuf h_x, h_m, h_obj, h_g, h_c, h_j, h_h;
@@ -140,116 +120,30 @@ static void upload(acopf_batch* b) {
     const int64_t n_coupling = (int64_t)b->cp_row.size();
     if (!b->stream) cuda_check(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "stream");
 
-    // topologies
+    // topologies (only what the aux kernel needs; the bus kernel reads tile tables)
     std::vector<DTopo> dt;
     b->topo_bufs.clear();
     size_t max_leaf = 1;
     for (const Topo* T : b->topos) {
         DTopo d{};
         d.nb = T->nb; d.nbr = T->nbr; d.ng = T->ng; d.nr = T->nr;
-        auto up = [&](const auto& v) {
-            b->topo_bufs.emplace_back(new DevBuf());
-            return b->topo_bufs.back()->upload(v);
-        };
-        d.fo = up(T->fo); d.to = up(T->to); d.adm = up(T->adm); d.ridx = up(T->ridx);
-        std::vector<long long> foff(T->foff.begin(), T->foff.end());
-        d.foff = up(foff);
         std::vector<int> leaf;
         for (size_t l = 0; l < T->leaf_start.size(); ++l) { leaf.push_back(T->leaf_start[l]); leaf.push_back(T->leaf_len[l]); }
-        d.leaf = up(leaf);
+        b->topo_bufs.emplace_back(new DevBuf());
+        d.leaf = b->topo_bufs.back()->upload(leaf);
         d.nleaf = (int)T->leaf_start.size();
         max_leaf = std::max(max_leaf, T->leaf_start.size());
         dt.push_back(d);
     }
-    // scratch quantities each topology's tile kernel reads (flows always)
-    std::vector<unsigned> qmask(b->topos.size(), (1u << S_PF) | (1u << S_QF) | (1u << S_PT) | (1u << S_QT));
-    for (const TileTable& tt : b->tables) qmask[tt.topo] |= tt.qused;
-    for (size_t i = 0; i < dt.size(); ++i) {
-        dt[i].qmask = qmask[i];
-        b->topo_bufs.emplace_back(new DevBuf());
-        dt[i].dpos = b->topo_bufs.back()->upload(b->dpos_base[i]);
-    }
-    // blob of tile tables (each 16-byte aligned, one bulk copy each)
+    // blob of tile tables (each 16-byte aligned, sized for one bulk copy)
     std::vector<uint8_t> blob;
     std::vector<int64_t> table_off(b->tables.size());
     std::vector<int> table_bytes(b->tables.size());
     for (size_t i = 0; i < b->tables.size(); ++i) {
         table_off[i] = (int64_t)blob.size();
-        b->tables[i].serialise(*b->topos[b->tables[i].topo], qmask[b->tables[i].topo], blob);
+        b->tables[i].serialise(*b->topos[b->tables[i].topo], blob);
         table_bytes[i] = (int)(blob.size() - table_off[i]);
     }
-    // removal sets: patch rows for branches with direct entries in patched tiles,
-    // and per-segment shift breakpoints for all other direct entries
-    std::vector<DRemSet> drs;
-    std::vector<int> pidx_all, ppos_all, bpt_all, bpd_all;
-    for (const RemSet& R : b->rsets) {
-        const Topo& T = *b->topos[R.topo];
-        const std::vector<int>& base = b->base_off[R.topo];
-        const int ntile = (int)b->base_table[R.topo].size();
-        DRemSet d{};
-        d.pidx_off = (long long)pidx_all.size();
-        d.ppos_off = (long long)ppos_all.size();
-        std::vector<int> pidx(T.nbr, -1), ppos;
-        for (int k : R.removed) pidx[k] = -2;
-        std::vector<char> patched(ntile, 0);
-        for (int t : R.patched_tiles) patched[t] = 1;
-        auto tile_of_bus = [&](int bus) {
-            return int(std::upper_bound(T.tile_b0.begin(), T.tile_b0.end(), bus) - T.tile_b0.begin()) - 1;
-        };
-        // every live branch touching a patched tile gets a patch row: its slots in
-        // patched tiles start as "not direct", the rest as "base + shift"
-        for (int t : R.patched_tiles) {
-            for (int i = T.tile_b0[t]; i < T.tile_b0[t + 1]; ++i) {
-                for (int side = 0; side < 2; ++side) {
-                    const std::vector<int>& ptr = side ? T.to_ptr : T.from_ptr;
-                    const std::vector<int>& lst = side ? T.to_list : T.from_list;
-                    for (int p = ptr[i]; p < ptr[i + 1]; ++p) {
-                        const int k = lst[p];
-                        if (pidx[k] == -2) continue;
-                        if (pidx[k] == -1) {
-                            pidx[k] = (int)(ppos.size() / NDIRECT);
-                            ppos.insert(ppos.end(), NDIRECT, -2);
-                        }
-                        for (int sl = 0; sl < NDIRECT; ++sl) {
-                            const int rowbus = DIRECT_SIDE[sl] == 0 ? T.fo[k] : T.to[k];
-                            if (patched[tile_of_bus(rowbus)]) ppos[(size_t)pidx[k] * NDIRECT + sl] = -1;
-                        }
-                    }
-                }
-            }
-        }
-        for (int t : R.patched_tiles)
-            for (const auto& dr : b->tables[R.table[t]].direct)
-                ppos[(size_t)pidx[dr.k] * NDIRECT + dr.slot] = R.tile_off[4 * t + dr.seg] + dr.lpos;
-        for (int sg = 0; sg < 4; ++sg) {
-            d.bp_off[sg] = (int)bpt_all.size();
-            bpt_all.push_back(base[sg]);
-            bpd_all.push_back(R.tile_off[sg] - base[sg]);
-            for (int t : R.patched_tiles) {
-                if (t + 1 >= ntile) continue;
-                bpt_all.push_back(base[4 * (t + 1) + sg]);
-                bpd_all.push_back(R.tile_off[4 * (t + 1) + sg] - base[4 * (t + 1) + sg]);
-            }
-            d.bp_n[sg] = (int)bpt_all.size() - d.bp_off[sg];
-            if (d.bp_n[sg] > MAXBP) throw std::runtime_error("too many patched tiles in one stage");
-        }
-        pidx_all.insert(pidx_all.end(), pidx.begin(), pidx.end());
-        ppos_all.insert(ppos_all.end(), ppos.begin(), ppos.end());
-        drs.push_back(d);
-    }
-    // chunks of consecutive stages whose branch scratch fits the L2 budget
-    const int64_t budget = b->scratch_budget / 8;       // doubles
-    std::vector<int> chunk_begin;
-    std::vector<int64_t> sbase(S, 0);
-    int64_t cur = 0, max_scratch = 1;
-    for (int s = 0; s < S; ++s) {
-        const int64_t need = (int64_t)__builtin_popcount(qmask[b->stages[s].topo]) * b->topos[b->stages[s].topo]->nbr;
-        if (s == 0 || cur + need > budget) { chunk_begin.push_back(s); cur = 0; }
-        sbase[s] = cur;
-        cur += need;
-        max_scratch = std::max(max_scratch, cur);
-    }
-    chunk_begin.push_back(S);
     // stages and removed lists
     std::vector<DStage> ds(S);
     std::vector<int> rem, remsz;
@@ -264,62 +158,52 @@ static void upload(acopf_batch* b) {
         d.cost_off = st.cost_off;
         d.rem_off = (long long)rem.size();
         d.nrem = (int)st.removed_rated.size();
-        d.sbase = sbase[s];
         rem.insert(rem.end(), st.removed_rated.begin(), st.removed_rated.end());
         remsz.insert(remsz.end(), st.removed_rowsz.begin(), st.removed_rowsz.end());
         d.topo = st.topo;
         d.obj_slot = b->obj_slot[s];
-        d.rset = st.rset;
         d.w = st.w;
     }
-    // per chunk: branch items (256 branches of one stage), then tile items
-    std::vector<DBranchItem> bitems;
-    std::vector<DTileItem> titems;
-    std::vector<DTileRec> recs;
-    std::vector<std::pair<int, int>> tiles;        // (topo, tile)
+    // bus work: for every tile, the stages sharing one table, in chunks of G
+    int64_t total_recs = 0;
+    for (const StageInfo& st : b->stages) total_recs += (int64_t)st.table.size();
+    const int64_t target_items = 148 * 2 * 6;
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(32, total_recs / target_items));
+    std::vector<DBusItem> items;
+    std::vector<DBusRec> recs;
+    size_t max_smem = 0;
+    std::map<int, std::vector<int>> by_table;     // table id -> stages (in order)
+    std::vector<std::pair<int, int>> tiles;       // (topo, tile)
     for (size_t ti = 0; ti < b->topos.size(); ++ti)
         for (size_t t = 0; t < b->base_table[ti].size(); ++t) tiles.push_back({(int)ti, (int)t});
-    size_t max_smem = 0;
-    b->chunks.clear();
-    std::map<int, std::vector<int>> by_table;
-    for (size_t c = 0; c + 1 < chunk_begin.size(); ++c) {
-        const int s0 = chunk_begin[c], s1 = chunk_begin[c + 1];
-        acopf_batch::Chunk ch{};
-        ch.b_first = (int)bitems.size();
-        for (int s = s0; s < s1; ++s) {
-            const int nbr = b->topos[b->stages[s].topo]->nbr;
-            for (int k = 0; k < nbr; k += BLOCK) bitems.push_back(DBranchItem{s, k});
-        }
-        ch.b_count = (int)bitems.size() - ch.b_first;
-        ch.t_first = (int)titems.size();
+    // stage-group-major order: CTAs running together share one group's x/mult in L2
+    for (int g0 = 0; g0 < S; g0 += G) {
+        const int g1 = std::min(S, g0 + G);
         for (auto [topo, t] : tiles) {
             by_table.clear();
-            for (int s = s0; s < s1; ++s)
+            for (int s = g0; s < g1; ++s)
                 if (b->stages[s].topo == topo) by_table[b->stages[s].table[t]].push_back(s);
             for (auto& kv : by_table) {
-                const TileTable& tt = b->tables[kv.first];
-                const std::vector<int>& ss = kv.second;
-                for (size_t g = 0; g < ss.size(); g += b->tile_group) {
-                    DTileItem it{};
-                    it.blob_off = table_off[kv.first];
-                    it.bytes = table_bytes[kv.first];
-                    it.first = (int)recs.size();
-                    it.count = (int)std::min<size_t>(b->tile_group, ss.size() - g);
-                    for (size_t j = g; j < g + it.count; ++j) {
-                        const StageInfo& st = b->stages[ss[j]];
-                        DTileRec r{};
-                        r.stage = ss[j];
-                        r.jP = st.tile_off[4 * t + 0]; r.jQ = st.tile_off[4 * t + 1];
-                        r.hA = st.tile_off[4 * t + 2]; r.hV = st.tile_off[4 * t + 3];
-                        recs.push_back(r);
-                    }
-                    titems.push_back(it);
-                    max_smem = std::max(max_smem, tile_smem_bytes(it.bytes, it.count, tt.nB));
+                DBusItem it{};
+                it.blob_off = table_off[kv.first];
+                it.bytes = table_bytes[kv.first];
+                it.first = (int)recs.size();
+                it.count = (int)kv.second.size();
+                for (int s : kv.second) {
+                    const StageInfo& st = b->stages[s];
+                    DBusRec r{};
+                    r.stage = s;
+                    r.jP = st.tile_off[4 * t + 0]; r.jQ = st.tile_off[4 * t + 1];
+                    r.hA = st.tile_off[4 * t + 2]; r.hV = st.tile_off[4 * t + 3];
+                    recs.push_back(r);
                 }
+                items.push_back(it);
+                size_t q, gv, gb, rs, fo, rc;
+                const TileTable& tt = b->tables[kv.first];
+                max_smem = std::max(max_smem, bus_smem_layout(table_bytes[kv.first], tt.nQ(), (int)tt.ends.size(),
+                                                              tt.nB, it.count, &q, &gv, &gb, &rs, &fo, &rc));
             }
         }
-        ch.t_count = (int)titems.size() - ch.t_first;
-        b->chunks.push_back(ch);
     }
     if (max_smem > (size_t)SMEM_LIMIT_BYTES) throw std::runtime_error("tile working set exceeds shared memory");
     // aux work: generator chunks per stage, then coupling chunks
@@ -337,9 +221,8 @@ static void upload(acopf_batch* b) {
     P = EvalParams{};
     P.topos = b->d_topo.upload(dt);
     P.stages = b->d_stage.upload(ds);
-    P.br_items = b->d_items.upload(bitems);
-    P.tile_items = b->d_titems.upload(titems);
-    P.tile_recs = b->d_recs.upload(recs);
+    P.bus_items = b->d_items.upload(items);
+    P.bus_recs = b->d_recs.upload(recs);
     P.aux_items = b->d_aux.upload(aux);
     P.blob = b->d_blob.upload(blob);
     P.pd = b->d_pd.upload(b->pd);
@@ -349,28 +232,23 @@ static void upload(acopf_batch* b) {
     P.cc = b->d_cc.upload(b->cc);
     P.rem_ridx = b->d_rem.upload(rem);
     P.rem_rowsz = b->d_remsz.upload(remsz);
-    P.rsets = b->d_rsets.upload(drs);
-    P.patch_idx = b->d_pidx.upload(pidx_all);
-    P.patch_pos = b->d_ppos.upload(ppos_all);
-    P.bp_thr = b->d_bpt.upload(bpt_all);
-    P.bp_dl = b->d_bpd.upload(bpd_all);
     P.cp_row = reinterpret_cast<const long long*>(b->d_cprow.upload(b->cp_row));
     P.cp_jpos = reinterpret_cast<const long long*>(b->d_cpj.upload(b->cp_jpos));
     P.cp_a = reinterpret_cast<const long long*>(b->d_cpa.upload(b->cp_a));
     P.cp_b = reinterpret_cast<const long long*>(b->d_cpb.upload(b->cp_b));
     P.cp_base_first = reinterpret_cast<const signed char*>(b->d_cpf.upload(b->cp_first));
     P.ncp = n_coupling;
+    P.n_bus_items = (int)items.size();
     P.n_aux_items = (int)aux.size();
     P.n_obj = S;
     P.obj_mode = b->obj_mode;
-    P.scratch = static_cast<double*>(b->d_scratch.alloc(sizeof(double) * (size_t)max_scratch));
     P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
     P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
     b->smem = (max_smem + 127) & ~size_t(127);
     b->aux_smem = sizeof(double) * max_leaf;
-    for (auto fn : {acopf_tile_kernel<0u>, acopf_tile_kernel<ACOPF_ALL>})
+    for (auto fn : {acopf_bus_kernel<0u>, acopf_bus_kernel<ACOPF_ALL>})
         cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(tile)");
+                                        (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(bus)");
     if (b->aux_smem > 48 * 1024)
         cuda_check(cudaFuncSetAttribute(acopf_aux_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)b->aux_smem), "cudaFuncSetAttribute(aux)");
@@ -434,22 +312,6 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
                 ids.push_back((int)B->tables.size() - 1);
             }
             B->base_table.push_back(ids);
-        }
-        for (int i = 0; i < n_topos; ++i) {
-            const Topo& T = *B->topos[i];
-            const std::vector<int>& ids = B->base_table[i];
-            std::vector<int> off(4 * ids.size());
-            int64_t tot[4] = {0, 0, 0, 0};
-            for (int id : ids) for (int sg = 0; sg < 4; ++sg) tot[sg] += B->tables[id].L[sg];
-            int64_t acc[4] = {0, tot[0], 0, tot[2]};
-            for (size_t t = 0; t < ids.size(); ++t)
-                for (int sg = 0; sg < 4; ++sg) { off[4 * t + sg] = (int)acc[sg]; acc[sg] += B->tables[ids[t]].L[sg]; }
-            std::vector<int> dpos((size_t)NDIRECT * T.nbr, -1);
-            for (size_t t = 0; t < ids.size(); ++t)
-                for (const auto& d : B->tables[ids[t]].direct)
-                    dpos[(size_t)d.slot * T.nbr + d.k] = off[4 * t + d.seg] + d.lpos;
-            B->base_off.push_back(off);
-            B->dpos_base.push_back(dpos);
         }
         B->pd.assign(pd, pd + n_load_values);
         B->qd.assign(qd, qd + n_load_values);
@@ -533,21 +395,6 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
             S.nnz_h = LA + LV + T.ng;
             if (S.nnz_jeq + S.nnz_jin >= (1LL << 31) || S.nnz_h >= (1LL << 31))
                 throw std::runtime_error("stage too large for 32-bit offsets");
-            if (!S.removed.empty()) {
-                auto key = std::make_pair(S.topo, S.removed);
-                auto it = B->rset_index.find(key);
-                if (it == B->rset_index.end()) {
-                    RemSet R;
-                    R.topo = S.topo;
-                    R.removed = S.removed;
-                    R.patched_tiles = touched;
-                    R.tile_off = S.tile_off;
-                    R.table = S.table;
-                    B->rsets.push_back(R);
-                    it = B->rset_index.emplace(key, (int)B->rsets.size() - 1).first;
-                }
-                S.rset = it->second;
-            }
         }
         *out = B.release();
     });
@@ -607,27 +454,18 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         P.x = x; P.mult = mult; P.obj_factor = obj_factor; P.what = what;
         P.obj = obj; P.grad = grad; P.cons = cons; P.jval = jval; P.hval = hval;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
+        const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD)) && P.n_bus_items > 0;
         const bool aux = (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
-        const bool branch = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) != 0;
-        const bool tiles = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD)) != 0;
         if (aux) {
             acopf_aux_kernel<<<P.n_aux_items, BLOCK, b->aux_smem, st>>>(P);
             cuda_check(cudaGetLastError(), "acopf_aux_kernel launch");
             b->launches++;
         }
-        for (const auto& ch : b->chunks) {
-            if (branch && ch.b_count) {
-                if (what == ACOPF_ALL) acopf_branch_kernel<ACOPF_ALL><<<ch.b_count, BLOCK, 0, st>>>(P, ch.b_first);
-                else acopf_branch_kernel<0u><<<ch.b_count, BLOCK, 0, st>>>(P, ch.b_first);
-                cuda_check(cudaGetLastError(), "acopf_branch_kernel launch");
-                b->launches++;
-            }
-            if (tiles && ch.t_count) {
-                if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<ch.t_count, BLOCK, b->smem, st>>>(P, ch.t_first);
-                else acopf_tile_kernel<0u><<<ch.t_count, BLOCK, b->smem, st>>>(P, ch.t_first);
-                cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
-                b->launches++;
-            }
+        if (bus) {
+            if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
+            else acopf_bus_kernel<0u><<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
+            cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
+            b->launches++;
         }
     });
 }

@@ -1,30 +1,27 @@
-// ACOPF callback evaluation kernels for sm_100a (fp64, no floating atomics,
-// built with -fmad=false so every expression rounds exactly like the
+// Fused ACOPF callback evaluation kernels for sm_100a (fp64, no floating
+// atomics, built with -fmad=false so every expression rounds exactly like the
 // reference's numpy evaluation).
 //
-// Stages are processed in chunks whose branch scratch fits in L2:
-//
-// acopf_branch_kernel -- one thread per (stage, live branch), branch-major:
-//   sincos of the angle difference, the four flows, their 16 partials and all
-//   10 Lagrangian-Hessian positions of the branch's 4x4 block (acopf.py:230-250,
-//   313-369), each computed ONCE per branch; written to the chunk's scratch
-//   (structure of arrays, coalesced).  Rated branches also store their two
-//   |S|^2 constraint values and their Jacobian rows in place (acopf.py:286-287,
-//   300-307; consecutive branches -> consecutive rows).
-//
-// acopf_tile_kernel -- one CTA = (tile of consecutive buses, the chunk's
-//   stages that share the tile's table).  One thread issues a cp.async.bulk
-//   (TMA bulk copy) of the tile's assembly program into shared memory; per
-//   stage it forms the bus-level shunt terms (acopf.py:262-263, 296-297, 366),
-//   the P/Q balance rows in np.add.at order (acopf.py:252-288), and every CSR
-//   value of the tile's J rows P_i/Q_i and H rows VA_i/VM_i as the ordered sum
-//   of its scratch terms (scipy's duplicate order, planner.hpp) -- four
-//   contiguous runs of the output arrays.
+// acopf_bus_kernel -- one CTA = (tile of consecutive buses, group of stages
+// that share the tile's table):
+//   0. one thread issues a cp.async.bulk (TMA bulk copy) of the tile's whole
+//      table -- per-end bus slots / rated index / flow-row offset, SoA branch
+//      admittances, per-bus shunts and generator lists, the scatter map --
+//      into shared memory, completing on an mbarrier;
+//   then for every stage of the group:
+//   A. per branch end: flows, their 16 partials and the 7 Hessian positions
+//      this end owns (acopf.py:230-250, 313-369) into shared memory; rated
+//      ends also store their |S|^2 row value and its Jacobian entries;
+//   A2. per bus: shunt terms (acopf.py:262-263, 296-297, 366);
+//   B. per bus: P/Q balance rows in np.add.at order (acopf.py:252-288); per
+//      CSR entry of the tile's J rows P_i/Q_i and H rows VA_i/VM_i: the
+//      ordered sum of its terms (scipy's duplicate order, planner.hpp),
+//      stored to four contiguous runs (coalesced).
 //
 // acopf_aux_kernel -- generator chunks (gradient, PG Hessian diagonal, the
-//   stage objective by numpy's pairwise sum, the weighted composite sum in
-//   stage order, composer.py:256-258) and coupling-row chunks (child - base
-//   values and +-1 Jacobian entries, composer.py:229-242, 274-276).
+// stage objective by numpy's pairwise sum, the weighted composite sum in
+// stage order, composer.py:256-258) and coupling-row chunks (child - base
+// values and +-1 Jacobian entries, composer.py:229-242, 274-276).
 #pragma once
 #include <cstdint>
 #include "planner.hpp"
@@ -36,41 +33,24 @@ enum : unsigned { W_OBJ = 1u, W_GRAD = 2u, W_CONS = 4u, W_JAC = 8u, W_HESS = 16u
 
 struct DTopo {
     int nb, nbr, ng, nr;
-    const int* fo;
-    const int* to;
-    const double* adm;        // 8 per branch (AoS): gff bff gft bft gtf btf gtt btt
-    const int* ridx;          // rated index or -1
-    const long long* foff;    // base offset of each rated branch's Sf row in the ineq J block
-    const int* dpos;          // [slot * nbr + k] stage-local position of a direct entry, or -1
     const int* leaf;          // (start, len) pairs of the pairwise sum over ng
     int nleaf;
-    unsigned qmask;           // scratch quantities the tile kernel reads (compact rows)
-};
-
-constexpr int MAXBP = 32;     // position-shift breakpoints per segment and removal set
-
-struct DRemSet {              // shared by the stages that remove the same branches
-    long long pidx_off, ppos_off;
-    int bp_off[4], bp_n[4];
+    int pad;
 };
 
 struct DStage {
     long long var_off, eq_row, ineq_row, jeq_base, jineq_base, h_base;
-    long long hpg_local, pd_off, cost_off, rem_off, sbase;
-    int nrem, topo, obj_slot, rset;
+    long long hpg_local, pd_off, cost_off, rem_off;
+    int nrem, topo, obj_slot, pad;
     double w;
 };
 
-struct DBranchItem {          // one CTA of the branch kernel: 256 branches of one stage
-    int stage, first;
-};
-
-struct DTileItem {            // one CTA of the tile kernel
+struct DBusItem {             // one CTA of the bus kernel
     long long blob_off;
     int bytes, first, count, pad;
 };
 
-struct DTileRec {             // (stage, tile) output offsets, stage-local
+struct DBusRec {              // (stage, tile) output offsets, stage-local
     int stage, jP, jQ, hA, hV, pad;
 };
 
@@ -82,9 +62,8 @@ struct DAuxItem {
 struct EvalParams {
     const DTopo* topos;
     const DStage* stages;
-    const DBranchItem* br_items;
-    const DTileItem* tile_items;
-    const DTileRec* tile_recs;
+    const DBusItem* bus_items;
+    const DBusRec* bus_recs;
     const DAuxItem* aux_items;
     const unsigned char* blob;
     const double* pd;
@@ -94,18 +73,13 @@ struct EvalParams {
     const double* cc;
     const int* rem_ridx;      // removed rated indices per stage (sorted)
     const int* rem_rowsz;
-    const DRemSet* rsets;
-    const int* patch_idx;     // per removal set and branch: -1 base, -2 removed, >= 0 patch row
-    const int* patch_pos;     // per patch row: NDIRECT positions (-1 none, -2 base + shift)
-    const int* bp_thr;        // breakpoints: base position thresholds and shifts
-    const int* bp_dl;
     const long long* cp_row;
     const long long* cp_jpos;
     const long long* cp_a;
     const long long* cp_b;
     const signed char* cp_base_first;
     long long ncp;
-    int n_aux_items;
+    int n_bus_items, n_aux_items;
     int n_obj;                // objective stages (chunk-0 generator items)
     int obj_mode;             // 0: f_s into obj[slot]; 1: weighted sum into obj[0]; 2: weighted terms only
     const double* x;
@@ -117,7 +91,6 @@ struct EvalParams {
     double* cons;
     double* jval;
     double* hval;
-    double* scratch;
     double* obj_terms;        // per objective stage: w_s * f_s
     unsigned* counter;
 };
@@ -126,110 +99,124 @@ constexpr int BLOCK = 256;
 constexpr int GEN_CHUNK = 256;
 constexpr int CP_CHUNK = 1024;
 
-// POSITIONS (acopf.py:48-49) as constexpr functions (unrolled loops fold them).
+// POSITIONS (acopf.py:48-49) and the end-slot -> position maps of planner.hpp,
+// as constexpr functions so unrolled device loops fold them to constants.
 __host__ __device__ constexpr int pos_a(int p) { return p < 4 ? 0 : (p < 7 ? 1 : (p < 9 ? 2 : 3)); }
 __host__ __device__ constexpr int pos_b(int p) { return p < 4 ? p : (p < 7 ? p - 3 : (p < 9 ? p - 5 : 3)); }
-
-// planner.hpp's DIRECT_Q / DIRECT_SEG as constexpr functions (device-usable)
-__host__ __device__ constexpr int direct_q(int d) {
-    return d < 8 ? (d < 4 ? S_JPF + (d & 1 ? 3 : 1) + (d >= 2 ? 4 : 0) : S_JPT + (d & 1 ? 2 : 0) + (d >= 6 ? 4 : 0))
-                 : S_H + (d < 10 ? 1 : d < 12 ? 3 : d < 14 ? 5 : 8);
-}
-__host__ __device__ constexpr int direct_seg(int d) {
-    return d < 8 ? ((d >> 1) & 1) : (d == 11 || d == 13 || d == 14 || d == 15 ? 3 : 2);
+__host__ __device__ constexpr int slot_pos_f(int s) { return s < 4 ? s : (s == 4 ? 5 : (s == 5 ? 7 : 8)); }
+__host__ __device__ constexpr int slot_pos_t(int s) {
+    return s == 0 ? 1 : (s == 1 ? 3 : (s <= 4 ? s + 2 : (s == 5 ? 8 : 9)));
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-// Store that should not displace the L2-resident scratch (outputs are written once).
-__device__ __forceinline__ void st_stream(double* p, double v) {
-    asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+// ---------------------------------------------------------------------------
+// bus kernel
+
+struct TileView {
+    const TileHdr* h;
+    const int* code;
+    const int* f;
+    const int* t;
+    const int* ridx;
+    const int* foff;
+    const int* busptr;
+    const int* gptr;
+    const int* glist;
+    const double* gs;
+    const double* bs;
+    const double* adm;
+};
+
+__device__ __forceinline__ double hpos(int p, double cpf, double cqf, double cpt, double cqt,
+                                       double s2f, double s2t, const double* gpf, const double* gqf,
+                                       const double* gpt, const double* gqt, const double* hpf,
+                                       const double* hqf, const double* hpt, const double* hqt) {
+    const int a = pos_a(p), b = pos_b(p);
+    double v = cpf * hpf[p] + cqf * hqf[p];
+    v = v + cpt * hpt[p];
+    v = v + cqt * hqt[p];
+    v = v + s2f * (gpf[a] * gpf[b] + gqf[a] * gqf[b]);
+    v = v + s2t * (gpt[a] * gpt[b] + gqt[a] * gqt[b]);
+    return v;
 }
 
-// ---------------------------------------------------------------------------
-// branch kernel
+// Per (stage, tile) record, staged in shared memory once per CTA.
+struct SRec {
+    long long var_off, eq_row, ineq_row, pd_off, rem_off;
+    long long oP, oQ, oA, oV, jineq;   // absolute output offsets of the tile's segments
+    double w;
+    int nrem, nb, ng, pad;
+};
 
-template <unsigned WHAT>
-__global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P, int item0) {
-    __shared__ int s_thr[4][MAXBP], s_dl[4][MAXBP], s_n[4];
-    const DBranchItem it = P.br_items[item0 + blockIdx.x];
-    const DStage S = P.stages[it.stage];
-    const DTopo T = P.topos[S.topo];
-    const int k = it.first + threadIdx.x;
-    const unsigned what = WHAT ? WHAT : P.what;
-    const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
-    int pidx = -1;
-    const int* ppos = nullptr;
-    if (S.rset >= 0) {
-        const DRemSet R = P.rsets[S.rset];
-        if (threadIdx.x < 4) s_n[threadIdx.x] = R.bp_n[threadIdx.x];
-        for (int i = threadIdx.x; i < 4 * MAXBP; i += blockDim.x) {
-            const int sg = i / MAXBP, j = i % MAXBP;
-            if (j < R.bp_n[sg]) {
-                s_thr[sg][j] = __ldg(P.bp_thr + R.bp_off[sg] + j);
-                s_dl[sg][j] = __ldg(P.bp_dl + R.bp_off[sg] + j);
+constexpr int GV = 10;   // gathered doubles per end: va_f va_t vm_f vm_t mu(Pf Qf Pt Qt) s_f s_t
+constexpr int GB = 5;    // gathered doubles per bus: vm mu_P mu_Q pd qd
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Issue the asynchronous gathers (LDGSTS) of one stage's inputs into shared memory.
+__device__ __forceinline__ void issue_gathers(const EvalParams& P, const SRec& R, const TileView& V, double* Gv,
+                                              double* Gb, int* RS, int* FO, bool need_h, bool need_c) {
+    const TileHdr* H = V.h;
+    const int ne = H->nE, nbt = H->nB, nb = R.nb;
+    const double* x = P.x + R.var_off;
+    const double* mu = P.mult + R.eq_row;
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+        const int f = V.f[e], t = V.t[e], r = V.ridx[e];
+        int rs = r, fo = V.foff[e];
+        if (r >= 0) {
+            for (int i = 0; i < R.nrem; ++i) {
+                if (__ldg(P.rem_ridx + R.rem_off + i) < r) { rs--; fo -= __ldg(P.rem_rowsz + R.rem_off + i); }
             }
         }
-        __syncthreads();
-        if (k < T.nbr) pidx = __ldg(P.patch_idx + R.pidx_off + k);
-        ppos = P.patch_pos + R.ppos_off;
-    }
-    if (k >= T.nbr || pidx == -2) return;              // past the end, or outaged in this stage
-    const int f = __ldg(T.fo + k), t = __ldg(T.to + k);
-    const int r = __ldg(T.ridx + k);
-    const double* va = P.x + S.var_off;
-    const double* vm = va + T.nb;
-    // gathers first, so they are in flight together
-    const double vaf = __ldg(va + f), vat = __ldg(va + t);
-    const double vf = __ldg(vm + f), vt = __ldg(vm + t);
-    const double2* ap = reinterpret_cast<const double2*>(T.adm + 8 * (long long)k);
-    const double2 a01 = __ldg(ap), a23 = __ldg(ap + 1), a45 = __ldg(ap + 2), a67 = __ldg(ap + 3);
-    const double gff = a01.x, bff = a01.y, gft = a23.x, bft = a23.y;
-    const double gtf = a45.x, btf = a45.y, gtt = a67.x, btt = a67.y;
-    int rs = r;
-    long long foff = 0;
-    if (r >= 0) {
-        foff = __ldg(T.foff + r);
-        for (int i = 0; i < S.nrem; ++i) {
-            const int q = __ldg(P.rem_ridx + S.rem_off + i);
-            if (q < r) { rs--; foff -= __ldg(P.rem_rowsz + S.rem_off + i); }
+        RS[e] = rs;
+        FO[e] = fo;
+        cp_async8(Gv + 0 * ne + e, x + f);
+        cp_async8(Gv + 1 * ne + e, x + t);
+        cp_async8(Gv + 2 * ne + e, x + nb + f);
+        cp_async8(Gv + 3 * ne + e, x + nb + t);
+        if (need_h) {
+            cp_async8(Gv + 4 * ne + e, mu + f);
+            cp_async8(Gv + 5 * ne + e, mu + nb + f);
+            cp_async8(Gv + 6 * ne + e, mu + t);
+            cp_async8(Gv + 7 * ne + e, mu + nb + t);
+            if (r >= 0) {
+                const double* mi = P.mult + R.ineq_row + 2 * rs;
+                cp_async8(Gv + 8 * ne + e, mi);
+                cp_async8(Gv + 9 * ne + e, mi + 1);
+            }
         }
     }
-    double mpf = 0.0, mqf = 0.0, mpt = 0.0, mqt = 0.0, sf = 0.0, st = 0.0;
-    if (need_h) {
-        const double* mu = P.mult + S.eq_row;
-        mpf = __ldg(mu + f);
-        mqf = __ldg(mu + T.nb + f);
-        mpt = __ldg(mu + t);
-        mqt = __ldg(mu + T.nb + t);
-        if (r >= 0) {
-            sf = __ldg(P.mult + S.ineq_row + 2 * rs);
-            st = __ldg(P.mult + S.ineq_row + 2 * rs + 1);
+    for (int bl = threadIdx.x; bl < nbt; bl += blockDim.x) {
+        const int i = H->b0 + bl;
+        cp_async8(Gb + 0 * nbt + bl, x + nb + i);
+        if (need_h) {
+            cp_async8(Gb + 1 * nbt + bl, mu + i);
+            cp_async8(Gb + 2 * nbt + bl, mu + nb + i);
+        }
+        if (need_c) {
+            cp_async8(Gb + 3 * nbt + bl, P.pd + R.pd_off + i);
+            cp_async8(Gb + 4 * nbt + bl, P.qd + R.pd_off + i);
         }
     }
-    // direct positions: the base layout, or this stage's patch row; entries outside
-    // patched tiles move by the removal set's piecewise-constant shift
-    int dp[NDIRECT];
-#pragma unroll
-    for (int d = 0; d < NDIRECT; ++d) {
-        int pos = __ldg(T.dpos + (long long)d * T.nbr + k);
-        bool shift = S.rset >= 0;
-        if (pidx >= 0) {
-            const int pp = __ldg(ppos + 16LL * pidx + d);
-            if (pp != -2) { pos = pp; shift = false; }
-        }
-        if (shift && pos >= 0) {
-            const int sg = direct_seg(d);
-            int dl = 0;
-            for (int j = 0; j < s_n[sg]; ++j)
-                if (pos >= s_thr[sg][j]) dl = s_dl[sg][j];
-            pos += dl;
-        }
-        dp[d] = pos;
-    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
+// Phase A for one branch end of one stage (inputs already gathered in shared memory).
+__device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, const TileView& V, const double* Gv,
+                                           int rs, long long foff, int e, double* Q, bool need_j, bool need_h,
+                                           bool need_c) {
+    const int ne = V.h->nE;
+    const int side = V.code[e] & 1;
+    const int f = V.f[e], t = V.t[e];
+    const int r = V.ridx[e];
+    const double vaf = Gv[e], vat = Gv[ne + e], vf = Gv[2 * ne + e], vt = Gv[3 * ne + e];
+    const double gff = V.adm[e], bff = V.adm[ne + e], gft = V.adm[2 * ne + e], bft = V.adm[3 * ne + e];
+    const double gtf = V.adm[4 * ne + e], btf = V.adm[5 * ne + e], gtt = V.adm[6 * ne + e], btt = V.adm[7 * ne + e];
     const double th = vaf - vat;
     double sn, cs;
     acc_sincos(th, &sn, &cs);
@@ -242,20 +229,10 @@ __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P,
     const double qf = ((-bff) * vf) * vf + vv * w;
     const double pt = (gtt * vt) * vt + vv * u2;
     const double qt = ((-btt) * vt) * vt + vv * w2;
-    double* sc = P.scratch + S.sbase + k;
-    const long long nbr = T.nbr;
-    const unsigned qm = T.qmask;
-    auto put = [&](int q, double v) {
-        if ((qm >> q) & 1u) __stcg(sc + (long long)__popc(qm & ((1u << q) - 1u)) * nbr, v);
-    };
-    put(S_PF, pf);
-    put(S_QF, qf);
-    put(S_PT, pt);
-    put(S_QT, qt);
-    if (r >= 0 && need_c) {
-        st_stream(P.cons + S.ineq_row + 2 * rs, pf * pf + qf * qf);
-        st_stream(P.cons + S.ineq_row + 2 * rs + 1, pt * pt + qt * qt);
-    }
+    double* q = Q + EQ * e;
+    q[Q_FP] = side ? pt : pf;
+    q[Q_FQ] = side ? qt : qf;
+    if (r >= 0 && need_c) P.cons[R.ineq_row + 2 * rs + side] = side ? pt * pt + qt * qt : pf * pf + qf * qf;
     if (!(need_j || need_h)) return;
     double gpf[4], gqf[4], gpt[4], gqt[4];
     gpf[0] = (-vv) * w;  gpf[1] = vv * w;    gpf[2] = (2.0 * gff) * vf + vt * u;   gpf[3] = vf * u;
@@ -263,45 +240,29 @@ __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P,
     gpt[0] = vv * w2;    gpt[1] = (-vv) * w2; gpt[2] = vt * u2; gpt[3] = (2.0 * gtt) * vt + vf * u2;
     gqt[0] = (-vv) * u2; gqt[1] = vv * u2;   gqt[2] = vt * w2; gqt[3] = (-2.0 * btt) * vt + vf * w2;
     if (need_j) {
-        double jv[16];
+        double gp[4], gq[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            jv[S_JPF + i] = -gpf[i];
-            jv[S_JQF + i] = -gqf[i];
-            jv[S_JPT + i] = -gpt[i];
-            jv[S_JQT + i] = -gqt[i];
+            gp[i] = side ? gpt[i] : gpf[i];
+            gq[i] = side ? gqt[i] : gqf[i];
+            q[Q_JP + i] = -gp[i];
+            q[Q_JQ + i] = -gq[i];
         }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) put(q, jv[q]);
-        double* jo = P.jval + S.jeq_base;
-#pragma unroll
-        for (int d = 0; d < 8; ++d)
-            if (dp[d] >= 0) st_stream(jo + dp[d], jv[direct_q(d)]);
         if (r >= 0) {
-            // dSf = (0 + 2 pf gpf) + 2 qf gqf (builtin sum order), St likewise
-            double dd[8];
+            const double fp = side ? pt : pf, fq = side ? qt : qf;
+            double d[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                dd[i] = (0.0 + (2.0 * pf) * gpf[i]) + (2.0 * qf) * gqf[i];
-                dd[4 + i] = (0.0 + (2.0 * pt) * gpt[i]) + (2.0 * qt) * gqt[i];
-            }
-            double* out = P.jval + S.jineq_base + foff;
-            if (f < t) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) st_stream(out + i, dd[i]);
-            } else if (f > t) {
-                st_stream(out + 0, dd[1]); st_stream(out + 1, dd[0]); st_stream(out + 2, dd[3]); st_stream(out + 3, dd[2]);
-                st_stream(out + 4, dd[5]); st_stream(out + 5, dd[4]); st_stream(out + 6, dd[7]); st_stream(out + 7, dd[6]);
-            } else {
-                st_stream(out, dd[0] + dd[1]);
-                st_stream(out + 1, dd[2] + dd[3]);
-                st_stream(out + 2, dd[4] + dd[5]);
-                st_stream(out + 3, dd[6] + dd[7]);
-            }
+            for (int i = 0; i < 4; ++i) d[i] = (0.0 + (2.0 * fp) * gp[i]) + (2.0 * fq) * gq[i];
+            double* out = P.jval + R.jineq + foff + (f == t ? 2 : 4) * side;
+            if (f < t) { out[0] = d[0]; out[1] = d[1]; out[2] = d[2]; out[3] = d[3]; }
+            else if (f > t) { out[0] = d[1]; out[1] = d[0]; out[2] = d[3]; out[3] = d[2]; }
+            else { out[0] = d[0] + d[1]; out[1] = d[2] + d[3]; }
         }
     }
     if (need_h) {
-        const double lpf = -mpf, lqf = -mqf, lpt = -mpt, lqt = -mqt;
+        double sf = 0.0, st = 0.0;
+        if (r >= 0) { sf = Gv[8 * ne + e]; st = Gv[9 * ne + e]; }
+        const double lpf = -Gv[4 * ne + e], lqf = -Gv[5 * ne + e], lpt = -Gv[6 * ne + e], lqt = -Gv[7 * ne + e];
         const double s2f = 2.0 * sf, s2t = 2.0 * st;
         const double cpf = lpf + s2f * pf, cqf = lqf + s2f * qf;
         const double cpt = lpt + s2t * pt, cqt = lqt + s2t * qt;
@@ -314,46 +275,40 @@ __global__ void __launch_bounds__(BLOCK) acopf_branch_kernel(const EvalParams P,
         const double hqf[10] = {-vvw, vvw, vtu, vfu, -vvw, -vtu, -vfu, -(2.0 * bff), w, z};
         const double hpt[10] = {-vvu2, vvu2, vtw2, vfw2, -vvu2, -vtw2, -vfw2, z, u2, 2.0 * gtt};
         const double hqt[10] = {-vvw2, vvw2, -vtu2, -vfu2, -vvw2, vtu2, vfu2, z, w2, -(2.0 * btt)};
-        double hv[10];
+        if (side == 0) {
 #pragma unroll
-        for (int p = 0; p < 10; ++p) {
-            const int a = pos_a(p), b = pos_b(p);
-            double v = cpf * hpf[p] + cqf * hqf[p];
-            v = v + cpt * hpt[p];
-            v = v + cqt * hqt[p];
-            v = v + s2f * (gpf[a] * gpf[b] + gqf[a] * gqf[b]);
-            v = v + s2t * (gpt[a] * gpt[b] + gqt[a] * gqt[b]);
-            hv[p] = v;
-            put(S_H + p, v);
+            for (int s = 0; s < 7; ++s)
+                q[Q_H + s] = hpos(slot_pos_f(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
+        } else {
+#pragma unroll
+            for (int s = 0; s < 7; ++s)
+                q[Q_H + s] = hpos(slot_pos_t(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
         }
-        double* ho = P.hval + S.h_base;
-#pragma unroll
-        for (int d = 8; d < NDIRECT; ++d)
-            if (dp[d] >= 0) st_stream(ho + dp[d], hv[direct_q(d) - S_H]);
     }
 }
 
-// ---------------------------------------------------------------------------
-// tile (assembly) kernel
-
-struct SRec {                 // per (stage, tile) record, staged in shared memory
-    long long var_off, eq_row, pd_off, sbase;
-    long long oP, oQ, oA, oV;
-    double w;
-    int nb, ng, nbr;
-    unsigned qmask;
-};
-
-__device__ __forceinline__ double term(const double* sc, const double* Bq, unsigned ref) {
-    return (ref & 0x80000000u) ? Bq[ref & 0x7fffffffu] : __ldcg(sc + ref);
+// Dynamic shared memory of one bus CTA (must match the host's bus_smem_bytes).
+__host__ __device__ __forceinline__ size_t bus_smem_layout(int table_bytes, int nQ, int nE, int nB, int count,
+                                                           size_t* o_q, size_t* o_gv, size_t* o_gb, size_t* o_rs,
+                                                           size_t* o_fo, size_t* o_rec) {
+    size_t off = (size_t)table_bytes;
+    *o_q = off;   off += 8 * (size_t)nQ;
+    *o_gv = off;  off += 8 * (size_t)GV * nE;
+    *o_gb = off;  off += 8 * (size_t)GB * nB;
+    *o_rs = off;  off += 4 * (size_t)nE;
+    *o_fo = off;  off += 4 * (size_t)nE;
+    off = (off + 15) & ~size_t(15);
+    *o_rec = off; off += sizeof(SRec) * (size_t)count;
+    return off;
 }
 
 template <unsigned WHAT>
-__global__ void __launch_bounds__(BLOCK) acopf_tile_kernel(const EvalParams P, int item0) {
+__global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
-    const DTileItem it = P.tile_items[item0 + blockIdx.x];
-    const TileHdr* H = reinterpret_cast<const TileHdr*>(smem);
+    const DBusItem it = P.bus_items[blockIdx.x];
+    const unsigned char* src = P.blob + it.blob_off;
+    // ---- 0. bulk copy of the tile table into shared memory ----------------
     if (threadIdx.x == 0) {
         const unsigned b = smem_u32(&bar);
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
@@ -362,26 +317,11 @@ __global__ void __launch_bounds__(BLOCK) acopf_tile_kernel(const EvalParams P, i
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 smem_u32(smem)),
-            "l"(P.blob + it.blob_off), "r"(it.bytes), "r"(b)
+            "l"(src), "r"(it.bytes), "r"(b)
             : "memory");
     }
-    // stage records (while the table is in flight)
-    SRec* recs = reinterpret_cast<SRec*>(smem + it.bytes);
-    double* Bq = reinterpret_cast<double*>(smem + it.bytes + sizeof(SRec) * it.count);
-    for (int i = threadIdx.x; i < it.count; i += blockDim.x) {
-        const DTileRec R = P.tile_recs[it.first + i];
-        const DStage S = P.stages[R.stage];
-        SRec o;
-        o.var_off = S.var_off; o.eq_row = S.eq_row; o.pd_off = S.pd_off; o.sbase = S.sbase;
-        o.oP = S.jeq_base + R.jP; o.oQ = S.jeq_base + R.jQ;
-        o.oA = S.h_base + R.hA; o.oV = S.h_base + R.hV;
-        o.w = S.w;
-        o.nb = P.topos[S.topo].nb;
-        o.ng = P.topos[S.topo].ng;
-        o.nbr = P.topos[S.topo].nbr;
-        o.qmask = P.topos[S.topo].qmask;
-        recs[i] = o;
-    }
+    // stage records: thread i loads record i while the table is in flight
+    const TileHdr* H = reinterpret_cast<const TileHdr*>(smem);
     __syncthreads();
     {
         const unsigned b = smem_u32(&bar);
@@ -394,98 +334,134 @@ __global__ void __launch_bounds__(BLOCK) acopf_tile_kernel(const EvalParams P, i
                 : "memory");
         }
     }
+    size_t o_q, o_gv, o_gb, o_rs, o_fo, o_rec;
+    bus_smem_layout(H->bytes, H->nQ, H->nE, H->nB, it.count, &o_q, &o_gv, &o_gb, &o_rs, &o_fo, &o_rec);
+    double* Q = reinterpret_cast<double*>(smem + o_q);
+    double* Gv = reinterpret_cast<double*>(smem + o_gv);
+    double* Gb = reinterpret_cast<double*>(smem + o_gb);
+    int* RS = reinterpret_cast<int*>(smem + o_rs);
+    int* FO = reinterpret_cast<int*>(smem + o_fo);
+    SRec* recs = reinterpret_cast<SRec*>(smem + o_rec);
+    for (int i = threadIdx.x; i < it.count; i += blockDim.x) {
+        const DBusRec R = P.bus_recs[it.first + i];
+        const DStage S = P.stages[R.stage];
+        SRec o;
+        o.var_off = S.var_off; o.eq_row = S.eq_row; o.ineq_row = S.ineq_row; o.pd_off = S.pd_off;
+        o.rem_off = S.rem_off; o.nrem = S.nrem; o.w = S.w;
+        o.oP = S.jeq_base + R.jP; o.oQ = S.jeq_base + R.jQ;
+        o.oA = S.h_base + R.hA; o.oV = S.h_base + R.hV;
+        o.jineq = S.jineq_base;
+        o.nb = P.topos[S.topo].nb;
+        o.ng = P.topos[S.topo].ng;
+        o.pad = 0;
+        recs[i] = o;
+    }
+    TileView V;
+    V.h = H;
+    V.code = reinterpret_cast<const int*>(smem + H->o_code);
+    V.f = reinterpret_cast<const int*>(smem + H->o_f);
+    V.t = reinterpret_cast<const int*>(smem + H->o_t);
+    V.ridx = reinterpret_cast<const int*>(smem + H->o_ridx);
+    V.foff = reinterpret_cast<const int*>(smem + H->o_foff);
+    V.busptr = reinterpret_cast<const int*>(smem + H->o_busptr);
+    V.gptr = reinterpret_cast<const int*>(smem + H->o_gptr);
+    V.glist = reinterpret_cast<const int*>(smem + H->o_glist);
+    V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
+    V.bs = reinterpret_cast<const double*>(smem + H->o_bs);
+    V.adm = reinterpret_cast<const double*>(smem + H->o_adm);
+    // WHAT != 0: the mask is a compile-time constant (the all-callbacks path)
     const unsigned what = WHAT ? WHAT : P.what;
     const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
+    const int qbus = EQ * H->nE;
     const int nbt = H->nB;
-    const int* busptr = reinterpret_cast<const int*>(smem + H->o_busptr);
-    const int* code = reinterpret_cast<const int*>(smem + H->o_code);
-    const int* gptr = reinterpret_cast<const int*>(smem + H->o_gptr);
-    const int* glist = reinterpret_cast<const int*>(smem + H->o_glist);
-    const double* gs = reinterpret_cast<const double*>(smem + H->o_gs);
-    const double* bs = reinterpret_cast<const double*>(smem + H->o_bs);
-    const unsigned* mref = reinterpret_cast<const unsigned*>(smem + H->o_mref);
-    if (threadIdx.x == 0) Bq[BQ * nbt] = 1.0;
+    if (threadIdx.x == 0) Q[qbus + BQ * nbt] = 1.0;
+    __syncthreads();
+    issue_gathers(P, recs[0], V, Gv, Gb, RS, FO, need_h, need_c);
 
     for (int ri = 0; ri < it.count; ++ri) {
-        const SRec R = recs[ri];
-        const double* sc = P.scratch + R.sbase;
-        const int nb = R.nb;
-        const long long nbr = R.nbr;
-        const double* x = P.x + R.var_off;
-        // bus-level terms and the balance rows (which need only scratch flows)
+        const SRec& R = recs[ri];
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        // ---- A: branch ends ------------------------------------------------
+        if (need_j || need_h || need_c)
+            for (int e = threadIdx.x; e < H->nE; e += blockDim.x)
+                branch_end(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c);
+        // ---- A2: bus-level terms -----------------------------------------------
         for (int bl = threadIdx.x; bl < nbt; bl += blockDim.x) {
             const int i = H->b0 + bl;
-            const double vmi = __ldg(x + nb + i), gsi = gs[bl], bsi = bs[bl];
-            double* qb = Bq + BQ * bl;
+            const double vmi = Gb[bl], gsi = V.gs[bl], bsi = V.bs[bl];
+            double* qb = Q + qbus + BQ * bl;
             qb[0] = (-2.0 * gsi) * vmi;
             qb[1] = (2.0 * bsi) * vmi;
-            if (need_h) {
-                const double* mu = P.mult + R.eq_row;
-                qb[2] = 2.0 * ((-__ldg(mu + i) * gsi) - (-__ldg(mu + nb + i) * bsi));
-            }
+            if (need_h) qb[2] = 2.0 * ((-Gb[nbt + bl] * gsi) - (-Gb[2 * nbt + bl] * bsi));
             if (what & W_GRAD) {
-                st_stream(P.grad + R.var_off + i, R.w * 0.0);
-                st_stream(P.grad + R.var_off + nb + i, R.w * 0.0);
-            }
-            if (need_c) {
-                // p_i: from-end pf (ascending branch), then to-end pt, then the shunt (acopf.py:256-263)
-                double p = 0.0, r = 0.0;
-                const long long cpf = __popc(R.qmask & ((1u << S_PF) - 1u)), cqf = cpf + 1;
-                const long long cpt = cpf + 2, cqt = cpf + 3;   // S_PF..S_QT are consecutive and always kept
-                for (int e = busptr[bl]; e < busptr[bl + 1]; ++e) {
-                    const int c = code[e];
-                    const long long kk = c >> 1;
-                    const int side = c & 1;
-                    p = p + __ldcg(sc + (side ? cpt : cpf) * nbr + kk);
-                    r = r + __ldcg(sc + (side ? cqt : cqf) * nbr + kk);
-                }
-                p = p + (gsi * vmi) * vmi;
-                r = r - (bsi * vmi) * vmi;
-                double cp = -(__ldg(P.pd + R.pd_off + i) + p);
-                double cq = -(__ldg(P.qd + R.pd_off + i) + r);
-                const double* pgv = x + 2 * nb;
-                for (int gi = gptr[bl]; gi < gptr[bl + 1]; ++gi) {
-                    const int g = glist[gi];
-                    cp = cp + __ldg(pgv + g);
-                    cq = cq + __ldg(pgv + R.ng + g);
-                }
-                st_stream(P.cons + R.eq_row + i, cp);
-                st_stream(P.cons + R.eq_row + nb + i, cq);
+                P.grad[R.var_off + i] = R.w * 0.0;
+                P.grad[R.var_off + R.nb + i] = R.w * 0.0;
             }
         }
         __syncthreads();
+        // the staging buffers are free again: gather the next stage's inputs
+        // while this stage's balance rows and scatter sums are stored
+        double vm_c = 0.0, pd_c = 0.0, qd_c = 0.0;
+        const int blc = threadIdx.x;
+        if (need_c && blc < nbt) { vm_c = Gb[blc]; pd_c = Gb[3 * nbt + blc]; qd_c = Gb[4 * nbt + blc]; }
+        if (ri + 1 < it.count) {
+            __syncthreads();
+            issue_gathers(P, recs[ri + 1], V, Gv, Gb, RS, FO, need_h, need_c);
+        }
+        // ---- B: balance rows, then the scatter-map sums -------------------------
+        if (need_c) {
+            const double* pgv = P.x + R.var_off + 2 * R.nb;
+            const double* qgv = pgv + R.ng;
+            for (int bl = threadIdx.x; bl < nbt; bl += blockDim.x) {
+                const int i = H->b0 + bl;
+                const double vmi = bl == blc ? vm_c : 0.0;
+                double p = 0.0, r = 0.0;
+                for (int e = V.busptr[bl]; e < V.busptr[bl + 1]; ++e) {
+                    p = p + Q[EQ * e + Q_FP];
+                    r = r + Q[EQ * e + Q_FQ];
+                }
+                p = p + (V.gs[bl] * vmi) * vmi;
+                r = r - (V.bs[bl] * vmi) * vmi;
+                double cp = -(pd_c + p);
+                double cq = -(qd_c + r);
+                for (int gi = V.gptr[bl]; gi < V.gptr[bl + 1]; ++gi) {
+                    const int g = V.glist[gi];
+                    cp = cp + __ldg(pgv + g);
+                    cq = cq + __ldg(qgv + g);
+                }
+                P.cons[R.eq_row + i] = cp;
+                P.cons[R.eq_row + R.nb + i] = cq;
+            }
+        }
+        const unsigned short* mterms = reinterpret_cast<const unsigned short*>(smem + H->o_mterms);
         for (int cls = 0; cls < 2; ++cls) {
             if (cls == 0 ? !need_j : !need_h) continue;
             double* o0 = cls == 0 ? P.jval + R.oP : P.hval + R.oA;
             double* o1 = cls == 0 ? P.jval + R.oQ : P.hval + R.oV;
             const int ns = cls == 0 ? H->nSJ : H->nSH;
             const unsigned* sdst = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_sj_dst : H->o_sh_dst));
-            const unsigned* sref = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_sj_ref : H->o_sh_ref));
+            const unsigned short* sterm =
+                reinterpret_cast<const unsigned short*>(smem + (cls == 0 ? H->o_sj_term : H->o_sh_term));
             for (int i = threadIdx.x; i < ns; i += blockDim.x) {
                 const unsigned d = sdst[i];
                 double* o = (d & 0x80000000u) ? o1 : o0;
-                st_stream(o + (d & 0x7fffffffu), term(sc, Bq, sref[i]));
+                o[d & 0x7fffffffu] = Q[sterm[i]];
             }
             const int nm = cls == 0 ? H->nMJ : H->nMH;
             const unsigned* mdst = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_mj_dst : H->o_mh_dst));
             const unsigned* minfo = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_mj_info : H->o_mh_info));
             for (int i = threadIdx.x; i < nm; i += blockDim.x) {
                 const unsigned d = mdst[i], info = minfo[i];
-                const unsigned* tp = mref + (info >> 10);
+                const unsigned short* tp = mterms + (info >> 10);
                 const int c = (int)(info & 1023u);
-                double v = term(sc, Bq, tp[0]);
-                for (int k = 1; k < c; ++k) v = v + term(sc, Bq, tp[k]);
+                double v = Q[tp[0]];
+                for (int k = 1; k < c; ++k) v = v + Q[tp[k]];
                 double* o = (d & 0x80000000u) ? o1 : o0;
-                st_stream(o + (d & 0x7fffffffu), v);
+                o[d & 0x7fffffffu] = v;
             }
         }
-        __syncthreads();
     }
-}
-
-// Dynamic shared memory of one tile CTA.
-__host__ __device__ __forceinline__ size_t tile_smem_bytes(int table_bytes, int count, int nB) {
-    return (size_t)table_bytes + sizeof(SRec) * (size_t)count + 8 * (size_t)(BQ * nB + 1);
 }
 
 // ---------------------------------------------------------------------------

@@ -51,8 +51,8 @@ constexpr int HSLOT_T[10] = {-1, 0, -1, 1, 2, 3, 4, -1, 5, 6};
 constexpr int POS_OF_SLOT_F[7] = {0, 1, 2, 3, 5, 7, 8};
 constexpr int POS_OF_SLOT_T[7] = {1, 3, 4, 5, 6, 8, 9};
 
-constexpr int TILE_MAX_ENDS = 384;   // soft cap; a single high-degree bus may exceed it
-constexpr int TILE_MAX_BUSES = 128;   // <= kernel block size (one bus per thread)
+constexpr int TILE_MAX_ENDS = 192;   // soft cap; a single high-degree bus may exceed it
+constexpr int TILE_MAX_BUSES = 96;    // <= kernel block size (one bus per thread)
 constexpr int SMEM_LIMIT_BYTES = 220 * 1024;
 
 // symbolic term: what a COO entry's value is made of
@@ -236,102 +236,61 @@ inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
 }
 
 // ---------------------------------------------------------------------------
-// Branch scratch record: the branch kernel writes, per (stage, live branch),
-// 30 doubles (structure of arrays over the topology's branches); the tile
-// (assembly) kernel reads them through the scatter map.
-constexpr int SQ = 30;
-constexpr int S_JPF = 0;    // 0..3   -dPf/d(VA_f, VA_t, VM_f, VM_t)
-constexpr int S_JQF = 4;    // 4..7   -dQf/d(...)
-constexpr int S_JPT = 8;    // 8..11  -dPt/d(...)
-constexpr int S_JQT = 12;   // 12..15 -dQt/d(...)
-constexpr int S_H = 16;     // 16..25 Lagrangian-Hessian value of POSITIONS[p]
-constexpr int S_PF = 26, S_QF = 27, S_PT = 28, S_QT = 29;
+// Tile tables (serialised into one device blob)
 
-// scratch quantity of an end-quantity symbol (planner slot -> scratch row)
-inline int scratch_q(int side, int q) {
-    if (q >= Q_JP && q < Q_JP + 4) return (side ? S_JPT : S_JPF) + (q - Q_JP);
-    if (q >= Q_JQ && q < Q_JQ + 4) return (side ? S_JQT : S_JQF) + (q - Q_JQ);
-    if (q >= Q_H && q < Q_H + 7) return S_H + (side ? POS_OF_SLOT_T[q - Q_H] : POS_OF_SLOT_F[q - Q_H]);
-    if (q == Q_FP) return side ? S_PT : S_PF;
-    return side ? S_QT : S_QF;
-}
-
-// Direct slots: the 16 off-diagonal CSR entries every (non-parallel,
-// non-self-loop) branch owns alone.  The branch kernel stores them in place;
-// only the remaining (diagonal / duplicate-summed / constant) entries go
-// through the tile kernel.  slot -> (scratch quantity, end owning the term,
-// row segment 0 P | 1 Q | 2 VA | 3 VM).
-constexpr int NDIRECT = 16;
-constexpr int DIRECT_Q[NDIRECT] = {S_JPF + 1, S_JPF + 3, S_JQF + 1, S_JQF + 3, S_JPT + 0, S_JPT + 2,
-                                   S_JQT + 0, S_JQT + 2, S_H + 1, S_H + 1, S_H + 3, S_H + 3,
-                                   S_H + 5, S_H + 5, S_H + 8, S_H + 8};
-constexpr int DIRECT_SIDE[NDIRECT] = {0, 0, 0, 0, 1, 1, 1, 1, 0, 1, 0, 1, 1, 0, 0, 1};
-constexpr int DIRECT_SEG[NDIRECT] = {0, 0, 1, 1, 0, 0, 1, 1, 2, 2, 2, 3, 2, 3, 3, 3};
-
-inline int direct_slot(int q, int side) {
-    for (int d = 0; d < NDIRECT; ++d)
-        if (DIRECT_Q[d] == q && DIRECT_SIDE[d] == side) return d;
-    return -1;
-}
-
-// ---------------------------------------------------------------------------
-// Tile tables (serialised into one device blob, bulk-copied to shared memory)
-
-struct TileHdr {            // 128 bytes; offsets in bytes from the header start
-    int32_t b0, nB, nE, ngl;          // first bus, buses, ends, generator ids
+struct TileHdr {            // 192 bytes; offsets in bytes from the header start
+    int32_t b0, nB, nE, nQ;           // first bus, buses, ends, shared doubles for quantities
     int32_t LP, LQ, LHA, LHV;         // entries of the four row segments
-    int32_t bytes, nSJ, nSH, nMJ;     // serialised size, single-term J / H, multi-term J entries
-    int32_t nMH, nMT, o_busptr, o_code;
-    int32_t o_gptr, o_glist, o_gs, o_bs;
-    int32_t o_sj_dst, o_sj_ref, o_sh_dst, o_sh_ref;
-    int32_t o_mj_dst, o_mj_info, o_mh_dst, o_mh_info;
-    int32_t o_mref, pad0, pad1, pad2;
+    int32_t ngl, bytes, nSJ, nSH;     // generator ids, serialised size, single-term J / H entries
+    int32_t nMJ, nMH, nMT, pad0;      // multi-term J / H entries, their term count
+    int32_t o_code, o_f, o_t, o_ridx;
+    int32_t o_foff, o_busptr, o_gptr, o_glist;
+    int32_t o_gs, o_bs, o_adm, o_sj_dst;
+    int32_t o_sj_term, o_sh_dst, o_sh_term, o_mj_dst;
+    int32_t o_mj_info, o_mh_dst, o_mh_info, o_mterms;
+    int32_t pad[12];
 };
-static_assert(sizeof(TileHdr) == 128, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
 
-// A tile's assembly program.  Entry destinations: bit 31 selects the second
-// segment (Q rows of J, VM rows of H), the rest is the local position.  Term
-// references: bit 31 clear = scratch row * nbr + branch; bit 31 set = bus-level
-// quantity (BQ per bus, then the constant 1.0).  Multi-term entries carry
-// (first term << 10 | count) and are sorted by decreasing count.
+// A tile's complete working set, copied to shared memory in one bulk copy:
+// per-end topology (bus slots, rated index, flow-row offset, SoA admittances),
+// per-bus shunts and generator lists, and the scatter map split into classes:
+//   single-term entries  dst (bit 31: Q row / VM row segment, else P / VA)
+//                        + the one quantity slot;
+//   multi-term entries   dst + (first term << 10 | term count), sorted by
+//                        decreasing count: warps run uniform trip counts and
+//                        the longest sums start first.
 struct TileTable {
     int topo = 0;
     int b0 = 0, nB = 0;
-    std::vector<int> ends;        // k*2+side, per bus: from-ends then to-ends (balance-row order)
+    std::vector<int> ends;        // k*2+side, per bus: from-ends then to-ends
     std::vector<int> busptr;      // nB+1
     int L[4] = {0, 0, 0, 0};      // entries in P, Q, VA, VM segments
     std::vector<int> cols;        // stage-local column per entry (pattern export)
     std::vector<int> rowlen;      // entries per row, 4 segments x nB rows
     std::vector<uint32_t> sdst[2];      // [0] J, [1] H
-    std::vector<uint32_t> sref[2];
+    std::vector<uint16_t> sterm[2];
     std::vector<uint32_t> mdst[2];
     std::vector<uint32_t> minfo[2];
-    std::vector<uint32_t> mref;
-    struct Direct { int k, slot, seg, lpos; };
-    std::vector<Direct> direct;   // entries the branch kernel stores in place (host only)
-    unsigned qused = 0;           // scratch quantities the table references
-    int nBQ() const { return BQ * nB + 1; }
-    void serialise(const Topo& T, unsigned qmask, std::vector<uint8_t>& blob) const;
+    std::vector<uint16_t> mterms;
+    int nQ() const { return EQ * (int)ends.size() + BQ * nB + 1; }
+    void serialise(const Topo& T, std::vector<uint8_t>& blob) const;
 };
-
-// compact scratch row of quantity q under the topology's mask
-inline int compact_q(unsigned qmask, int q) { return __builtin_popcount(qmask & ((1u << q) - 1u)); }
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-inline void TileTable::serialise(const Topo& T, unsigned qmask, std::vector<uint8_t>& blob) const {
-    // scratch references were built as q * nbr + k; re-index to the compact rows
-    auto remap = [&](std::vector<uint32_t> v) {
-        for (auto& r : v)
-            if (!(r & 0x80000000u)) {
-                uint32_t q = r / (uint32_t)T.nbr, k = r % (uint32_t)T.nbr;
-                r = (uint32_t)compact_q(qmask, (int)q) * (uint32_t)T.nbr + k;
-            }
-        return v;
-    };
-    const std::vector<uint32_t> sref0 = remap(sref[0]), sref1 = remap(sref[1]), mref_c = remap(mref);
-    std::vector<int> gptr(1, 0), glist;
-    std::vector<double> gs(nB), bs(nB);
+inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) const {
+    const int nE = (int)ends.size();
+    std::vector<int> f(nE), t(nE), ridx(nE), foff(nE), gptr(1, 0), glist;
+    std::vector<double> adm(8 * (size_t)nE), gs(nB), bs(nB);
+    for (int e = 0; e < nE; ++e) {
+        int k = ends[e] >> 1;
+        f[e] = T.fo[k];
+        t[e] = T.to[k];
+        ridx[e] = T.ridx[k];
+        foff[e] = T.ridx[k] >= 0 ? (int)T.foff[T.ridx[k]] : 0;
+        for (int q = 0; q < 8; ++q) adm[(size_t)q * nE + e] = T.adm[8 * (size_t)k + q];
+    }
     for (int bl = 0; bl < nB; ++bl) {
         int i = b0 + bl;
         gs[bl] = T.gs[i];
@@ -340,49 +299,60 @@ inline void TileTable::serialise(const Topo& T, unsigned qmask, std::vector<uint
         gptr.push_back((int)glist.size());
     }
     TileHdr h{};
-    h.b0 = b0; h.nB = nB; h.nE = (int)ends.size(); h.ngl = (int)glist.size();
+    h.b0 = b0; h.nB = nB; h.nE = nE; h.nQ = nQ();
     h.LP = L[0]; h.LQ = L[1]; h.LHA = L[2]; h.LHV = L[3];
+    h.ngl = (int)glist.size();
     h.nSJ = (int)sdst[0].size(); h.nSH = (int)sdst[1].size();
     h.nMJ = (int)mdst[0].size(); h.nMH = (int)mdst[1].size();
-    h.nMT = (int)mref.size();
+    h.nMT = (int)mterms.size();
     size_t off = sizeof(TileHdr);
     auto take = [&](size_t n) { int o = (int)off; off = align16(off + n); return o; };
+    h.o_code = take(4 * (size_t)nE);
+    h.o_f = take(4 * (size_t)nE);
+    h.o_t = take(4 * (size_t)nE);
+    h.o_ridx = take(4 * (size_t)nE);
+    h.o_foff = take(4 * (size_t)nE);
     h.o_busptr = take(4 * busptr.size());
-    h.o_code = take(4 * ends.size());
     h.o_gptr = take(4 * gptr.size());
     h.o_glist = take(4 * glist.size());
     h.o_gs = take(8 * (size_t)nB);
     h.o_bs = take(8 * (size_t)nB);
+    h.o_adm = take(8 * adm.size());
     h.o_sj_dst = take(4 * sdst[0].size());
-    h.o_sj_ref = take(4 * sref[0].size());
+    h.o_sj_term = take(2 * sterm[0].size());
     h.o_sh_dst = take(4 * sdst[1].size());
-    h.o_sh_ref = take(4 * sref[1].size());
+    h.o_sh_term = take(2 * sterm[1].size());
     h.o_mj_dst = take(4 * mdst[0].size());
     h.o_mj_info = take(4 * minfo[0].size());
     h.o_mh_dst = take(4 * mdst[1].size());
     h.o_mh_info = take(4 * minfo[1].size());
-    h.o_mref = take(4 * mref.size());
+    h.o_mterms = take(2 * mterms.size());
     h.bytes = (int)off;
     size_t base = blob.size();
     blob.resize(base + off, 0);
     uint8_t* p = blob.data() + base;
     std::memcpy(p, &h, sizeof h);
     auto put = [&](int o, const void* src, size_t n) { if (n) std::memcpy(p + o, src, n); };
+    put(h.o_code, ends.data(), 4 * (size_t)nE);
+    put(h.o_f, f.data(), 4 * (size_t)nE);
+    put(h.o_t, t.data(), 4 * (size_t)nE);
+    put(h.o_ridx, ridx.data(), 4 * (size_t)nE);
+    put(h.o_foff, foff.data(), 4 * (size_t)nE);
     put(h.o_busptr, busptr.data(), 4 * busptr.size());
-    put(h.o_code, ends.data(), 4 * ends.size());
     put(h.o_gptr, gptr.data(), 4 * gptr.size());
     put(h.o_glist, glist.data(), 4 * glist.size());
     put(h.o_gs, gs.data(), 8 * (size_t)nB);
     put(h.o_bs, bs.data(), 8 * (size_t)nB);
+    put(h.o_adm, adm.data(), 8 * adm.size());
     put(h.o_sj_dst, sdst[0].data(), 4 * sdst[0].size());
-    put(h.o_sj_ref, sref0.data(), 4 * sref0.size());
+    put(h.o_sj_term, sterm[0].data(), 2 * sterm[0].size());
     put(h.o_sh_dst, sdst[1].data(), 4 * sdst[1].size());
-    put(h.o_sh_ref, sref1.data(), 4 * sref1.size());
+    put(h.o_sh_term, sterm[1].data(), 2 * sterm[1].size());
     put(h.o_mj_dst, mdst[0].data(), 4 * mdst[0].size());
     put(h.o_mj_info, minfo[0].data(), 4 * minfo[0].size());
     put(h.o_mh_dst, mdst[1].data(), 4 * mdst[1].size());
     put(h.o_mh_info, minfo[1].data(), 4 * minfo[1].size());
-    put(h.o_mref, mref_c.data(), 4 * mref_c.size());
+    put(h.o_mterms, mterms.data(), 2 * mterms.size());
 }
 
 inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
@@ -391,19 +361,29 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     tt.b0 = b0;
     tt.nB = b1 - b0;
     std::vector<Row> rows(4 * tt.nB);
+    std::unordered_map<int, int> end_pos;
     tt.busptr.push_back(0);
     for (int i = b0; i < b1; ++i) {
-        for (int p = T.from_ptr[i]; p < T.from_ptr[i + 1]; ++p)
-            if (live(T.from_list[p])) tt.ends.push_back(2 * T.from_list[p]);
-        for (int p = T.to_ptr[i]; p < T.to_ptr[i + 1]; ++p)
-            if (live(T.to_list[p])) tt.ends.push_back(2 * T.to_list[p] + 1);
+        for (int p = T.from_ptr[i]; p < T.from_ptr[i + 1]; ++p) {
+            int k = T.from_list[p];
+            if (!live(k)) continue;
+            end_pos[2 * k] = (int)tt.ends.size();
+            tt.ends.push_back(2 * k);
+        }
+        for (int p = T.to_ptr[i]; p < T.to_ptr[i + 1]; ++p) {
+            int k = T.to_list[p];
+            if (!live(k)) continue;
+            end_pos[2 * k + 1] = (int)tt.ends.size();
+            tt.ends.push_back(2 * k + 1);
+        }
         tt.busptr.push_back((int)tt.ends.size());
         Row r4[4];
         build_bus_rows(T, i, live, r4);
         for (int s = 0; s < 4; ++s) rows[s * tt.nB + (i - b0)] = std::move(r4[s]);
     }
-    const uint32_t bus_bit = 0x80000000u;
-    struct Multi { uint32_t dst; std::vector<uint32_t> t; };
+    const int nE = (int)tt.ends.size();
+    // classify entries: single-term gather-stores and multi-term sums
+    struct Multi { uint32_t dst; std::vector<uint16_t> t; };
     std::vector<Multi> multi[2];
     for (int s = 0; s < 4; ++s) {
         const int cls = s / 2;                    // 0: J (P, Q rows), 1: H (VA, VM rows)
@@ -415,31 +395,20 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             tt.L[s] += (int)row.cols.size();
             for (size_t e = 0; e < row.cols.size(); ++e, ++local) {
                 tt.cols.push_back(row.cols[e]);
-                if (row.tptr[e + 1] - row.tptr[e] == 1 && row.terms[row.tptr[e]].kind == 0) {
-                    const Sym& y = row.terms[row.tptr[e]];
-                    const int d = direct_slot(scratch_q(y.a & 1, y.q), y.a & 1);
-                    if (d >= 0 && DIRECT_SEG[d] == s) {
-                        tt.direct.push_back(TileTable::Direct{y.a >> 1, d, s, (int)local});
-                        continue;
-                    }
-                }
-                std::vector<uint32_t> refs;
+                std::vector<uint16_t> slots;
                 for (int t = row.tptr[e]; t < row.tptr[e + 1]; ++t) {
                     const Sym& y = row.terms[t];
-                    uint32_t ref;
-                    if (y.kind == 0) {
-                        const int q = scratch_q(y.a & 1, y.q);
-                        tt.qused |= 1u << q;
-                        ref = (uint32_t)(q * T.nbr + (y.a >> 1));
-                    } else if (y.kind == 1) ref = bus_bit | (uint32_t)(BQ * (y.a - b0) + y.q);
-                    else ref = bus_bit | (uint32_t)(BQ * tt.nB);
-                    refs.push_back(ref);
+                    int slot;
+                    if (y.kind == 0) slot = EQ * end_pos.at(y.a) + y.q;
+                    else if (y.kind == 1) slot = EQ * nE + BQ * (y.a - b0) + y.q;
+                    else slot = EQ * nE + BQ * tt.nB;
+                    slots.push_back((uint16_t)slot);
                 }
-                if (refs.size() == 1) {
+                if (slots.size() == 1) {
                     tt.sdst[cls].push_back(segbit | local);
-                    tt.sref[cls].push_back(refs[0]);
+                    tt.sterm[cls].push_back(slots[0]);
                 } else {
-                    multi[cls].push_back(Multi{segbit | local, refs});
+                    multi[cls].push_back(Multi{segbit | local, slots});
                 }
             }
         }
@@ -450,14 +419,15 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         for (const Multi& m : multi[cls]) {
             if (m.t.size() >= 1024) throw std::runtime_error("entry with >= 1024 duplicate terms");
             tt.mdst[cls].push_back(m.dst);
-            tt.minfo[cls].push_back(((uint32_t)tt.mref.size() << 10) | (uint32_t)m.t.size());
-            tt.mref.insert(tt.mref.end(), m.t.begin(), m.t.end());
+            tt.minfo[cls].push_back(((uint32_t)tt.mterms.size() << 10) | (uint32_t)m.t.size());
+            tt.mterms.insert(tt.mterms.end(), m.t.begin(), m.t.end());
         }
     }
-    size_t approx = 128 + 4 * tt.ends.size() + 40 * (size_t)tt.nB + 8 * tt.cols.size() + 4 * tt.mref.size() + 512;
+    // shared memory = serialised table + quantity array (checked again at upload)
+    size_t approx = 192 + 84 * (size_t)nE + 24 * (size_t)tt.nB + 6 * tt.cols.size() + 2 * tt.mterms.size() +
+                    8 * (size_t)tt.nQ() + 512;
     if (approx > (size_t)SMEM_LIMIT_BYTES)
         throw std::runtime_error("bus degree too high for one tile's shared memory");
-    if ((size_t)SQ * T.nbr >= 0x80000000u) throw std::runtime_error("topology too large for scratch references");
     return tt;
 }
 
