@@ -128,7 +128,6 @@ struct TileView {
     const double* gs;
     const double* bs;
     const double* adm;
-    const unsigned* edst;
 };
 
 __device__ __forceinline__ double hpos(int p, double cpf, double cqf, double cpt, double cqt,
@@ -246,19 +245,8 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, c
         for (int i = 0; i < 4; ++i) {
             gp[i] = side ? gpt[i] : gpf[i];
             gq[i] = side ? gqt[i] : gqf[i];
-        }
-        // direct slots of an end are the off-diagonal partials: odd columns for a
-        // from-end (VA_t, VM_t), even ones for a to-end; stored in place
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const double v = i < 4 ? -gp[i] : -gq[i - 4];
-            const unsigned dst = ((i & 1) != side) ? V.edst[(i >> 1) * ne + e] : NO_DST;
-            if (dst != NO_DST) {
-                double* o = (dst & 0x80000000u) ? P.jval + R.oQ : P.jval + R.oP;
-                o[dst & 0x7fffffffu] = v;
-            } else {
-                q[Q_JP + i] = v;
-            }
+            q[Q_JP + i] = -gp[i];
+            q[Q_JQ + i] = -gq[i];
         }
         if (r >= 0) {
             const double fp = side ? pt : pf, fq = side ? qt : qf;
@@ -287,27 +275,14 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, c
         const double hqf[10] = {-vvw, vvw, vtu, vfu, -vvw, -vtu, -vfu, -(2.0 * bff), w, z};
         const double hpt[10] = {-vvu2, vvu2, vtw2, vfw2, -vvu2, -vtw2, -vfw2, z, u2, 2.0 * gtt};
         const double hqt[10] = {-vvw2, vvw2, -vtu2, -vfu2, -vvw2, vtu2, vfu2, z, w2, -(2.0 * btt)};
-        // direct H slots: from-end slots 1,3,4,6 / to-end slots 0,1,3,5 (planner DIR_SLOT_*)
-        double* oA = P.hval + R.oA;
-        double* oV = P.hval + R.oV;
         if (side == 0) {
 #pragma unroll
-            for (int s = 0; s < 7; ++s) {
-                const double v = hpos(slot_pos_f(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
-                const int j = s == 1 ? 4 : s == 3 ? 5 : s == 4 ? 6 : s == 6 ? 7 : -1;
-                const unsigned dst = j >= 0 ? V.edst[j * ne + e] : NO_DST;
-                if (dst != NO_DST) ((dst & 0x80000000u) ? oV : oA)[dst & 0x7fffffffu] = v;
-                else q[Q_H + s] = v;
-            }
+            for (int s = 0; s < 7; ++s)
+                q[Q_H + s] = hpos(slot_pos_f(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
         } else {
 #pragma unroll
-            for (int s = 0; s < 7; ++s) {
-                const double v = hpos(slot_pos_t(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
-                const int j = s == 0 ? 4 : s == 1 ? 5 : s == 3 ? 6 : s == 5 ? 7 : -1;
-                const unsigned dst = j >= 0 ? V.edst[j * ne + e] : NO_DST;
-                if (dst != NO_DST) ((dst & 0x80000000u) ? oV : oA)[dst & 0x7fffffffu] = v;
-                else q[Q_H + s] = v;
-            }
+            for (int s = 0; s < 7; ++s)
+                q[Q_H + s] = hpos(slot_pos_t(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
         }
     }
 }
@@ -394,7 +369,6 @@ __global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P)
     V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
     V.bs = reinterpret_cast<const double*>(smem + H->o_bs);
     V.adm = reinterpret_cast<const double*>(smem + H->o_adm);
-    V.edst = reinterpret_cast<const unsigned*>(smem + H->o_edst);
     // WHAT != 0: the mask is a compile-time constant (the all-callbacks path)
     const unsigned what = WHAT ? WHAT : P.what;
     const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;

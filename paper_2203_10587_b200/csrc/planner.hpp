@@ -51,14 +51,6 @@ constexpr int HSLOT_T[10] = {-1, 0, -1, 1, 2, 3, 4, -1, 5, 6};
 constexpr int POS_OF_SLOT_F[7] = {0, 1, 2, 3, 5, 7, 8};
 constexpr int POS_OF_SLOT_T[7] = {1, 3, 4, 5, 6, 8, 9};
 
-// Direct slots: the 8 off-diagonal entries a branch end owns alone (no parallel
-// twin, no self-loop).  Phase A stores them straight from registers; their
-// quantity slot per side, in order: J (P row: 2, Q row: 2), then H (4).
-constexpr int NDIR = 8;
-constexpr uint32_t NO_DST = 0xFFFFFFFFu;
-constexpr int DIR_SLOT_F[NDIR] = {Q_JP + 1, Q_JP + 3, Q_JQ + 1, Q_JQ + 3, Q_H + 1, Q_H + 3, Q_H + 4, Q_H + 6};
-constexpr int DIR_SLOT_T[NDIR] = {Q_JP + 0, Q_JP + 2, Q_JQ + 0, Q_JQ + 2, Q_H + 0, Q_H + 1, Q_H + 3, Q_H + 5};
-
 constexpr int TILE_MAX_ENDS = 192;   // soft cap; a single high-degree bus may exceed it
 constexpr int TILE_MAX_BUSES = 96;    // <= kernel block size (one bus per thread)
 constexpr int SMEM_LIMIT_BYTES = 220 * 1024;
@@ -250,7 +242,7 @@ struct TileHdr {            // 192 bytes; offsets in bytes from the header start
     int32_t b0, nB, nE, nQ;           // first bus, buses, ends, shared doubles for quantities
     int32_t LP, LQ, LHA, LHV;         // entries of the four row segments
     int32_t ngl, bytes, nSJ, nSH;     // generator ids, serialised size, single-term J / H entries
-    int32_t nMJ, nMH, nMT, o_edst;    // multi-term J / H entries, their term count, direct dsts
+    int32_t nMJ, nMH, nMT, pad0;      // multi-term J / H entries, their term count
     int32_t o_code, o_f, o_t, o_ridx;
     int32_t o_foff, o_busptr, o_gptr, o_glist;
     int32_t o_gs, o_bs, o_adm, o_sj_dst;
@@ -281,7 +273,6 @@ struct TileTable {
     std::vector<uint32_t> mdst[2];
     std::vector<uint32_t> minfo[2];
     std::vector<uint16_t> mterms;
-    std::vector<uint32_t> edst;   // [j * nE + e]: destination of end e's j-th direct slot, or NO_DST
     int nQ() const { return EQ * (int)ends.size() + BQ * nB + 1; }
     void serialise(const Topo& T, std::vector<uint8_t>& blob) const;
 };
@@ -336,7 +327,6 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     h.o_mh_dst = take(4 * mdst[1].size());
     h.o_mh_info = take(4 * minfo[1].size());
     h.o_mterms = take(2 * mterms.size());
-    h.o_edst = take(4 * edst.size());
     h.bytes = (int)off;
     size_t base = blob.size();
     blob.resize(base + off, 0);
@@ -363,7 +353,6 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     put(h.o_mh_dst, mdst[1].data(), 4 * mdst[1].size());
     put(h.o_mh_info, minfo[1].data(), 4 * minfo[1].size());
     put(h.o_mterms, mterms.data(), 2 * mterms.size());
-    put(h.o_edst, edst.data(), 4 * edst.size());
 }
 
 inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
@@ -393,8 +382,7 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         for (int s = 0; s < 4; ++s) rows[s * tt.nB + (i - b0)] = std::move(r4[s]);
     }
     const int nE = (int)tt.ends.size();
-    tt.edst.assign((size_t)NDIR * nE, NO_DST);
-    // classify entries: direct (stored by phase A), single-term gather-stores, multi-term sums
+    // classify entries: single-term gather-stores and multi-term sums
     struct Multi { uint32_t dst; std::vector<uint16_t> t; };
     std::vector<Multi> multi[2];
     for (int s = 0; s < 4; ++s) {
@@ -415,16 +403,6 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
                     else if (y.kind == 1) slot = EQ * nE + BQ * (y.a - b0) + y.q;
                     else slot = EQ * nE + BQ * tt.nB;
                     slots.push_back((uint16_t)slot);
-                }
-                if (slots.size() == 1 && row.terms[row.tptr[e]].kind == 0) {
-                    const Sym& y = row.terms[row.tptr[e]];
-                    const int* dslot = (y.a & 1) ? DIR_SLOT_T : DIR_SLOT_F;
-                    int j = 0;
-                    while (j < NDIR && dslot[j] != y.q) ++j;
-                    if (j < NDIR && (j < 4) == (cls == 0)) {
-                        tt.edst[(size_t)j * nE + end_pos.at(y.a)] = segbit | local;
-                        continue;
-                    }
                 }
                 if (slots.size() == 1) {
                     tt.sdst[cls].push_back(segbit | local);
