@@ -79,13 +79,32 @@ def workload_desc(cfg: int, points: int) -> dict:
     }[cfg]
 
 
-def build_ours(cfg: int, points: int, device: int, seed0: int):
-    """(evaluator, x [host], mult [host], units per step, topology list)."""
+def _composite_args(cfg: int):
+    from paper_2203_10587_b200 import synthetic as syn
+    from paper_2203_10587_b200.types import CouplingMode
+    if cfg == 2:
+        base, ctgs = syn.config2_inputs()
+        return "scopf", (base, ctgs, CouplingMode()), None
+    if cfg == 3:
+        return "multiperiod", (syn.config3_periods(), 15.0), None
+    base, scens, ctgs = syn.config4_inputs()
+    per_scen = len(ctgs) + 1
+    return "general", (scens, ctgs, [base], CouplingMode(), 30.0), per_scen
+
+
+class Runner:
+    """One benchmark step = one evaluation of the workload on this rank's GPU."""
+
+    def __init__(self, ev, x_h, m_h, units, sharded=None):
+        self.ev, self.x_h, self.m_h, self.units, self.sharded = ev, x_h, m_h, units, sharded
+
+
+def build_ours(cfg: int, points: int, device: int, seed0: int, dist=None, rank=0, world=1):
+    """Runner for config cfg on cuda:device (sharded over ranks for composites when world > 1)."""
     from paper_2203_10587_b200 import synthetic as syn
     from paper_2203_10587_b200 import BatchEvaluator, compose_general, compose_multiperiod, compose_scopf
     from paper_2203_10587_b200.packer import PackedCase, Topology
     from paper_2203_10587_b200.stage import stage_plan
-    from paper_2203_10587_b200.types import CouplingMode
     if cfg == 1:
         case = syn.config_case(1)
         topo = Topology(PackedCase(case))
@@ -98,19 +117,26 @@ def build_ours(cfg: int, points: int, device: int, seed0: int):
             x, m = syn.random_point(kinds, xl, xu, m1, seed0 + i)
             xs.append(x)
             ms.append(m)
-        return ev, np.concatenate(xs), np.concatenate(ms), points
-    if cfg == 2:
-        base, ctgs = syn.config2_inputs()
-        p, imap = compose_scopf(base, ctgs, CouplingMode(), device=device)
-    elif cfg == 3:
-        p, imap = compose_multiperiod(syn.config3_periods(), 15.0, device=device)
-    else:
-        base, scens, ctgs = syn.config4_inputs()
-        p, imap = compose_general(scens, ctgs, [base], CouplingMode(), 30.0, device=device)
+        return Runner(ev, np.concatenate(xs), np.concatenate(ms), points)
+    kind, args, per_scen = _composite_args(cfg)
+    if world > 1:
+        from paper_2203_10587_b200.dispatch import ShardedComposite
+        from paper_2203_10587_b200.lattice import composite_spec
+        spec = composite_spec(kind, *args)
+        align = None if per_scen is None else [k // per_scen for k in range(len(spec.plans))]
+        sc = ShardedComposite(spec, dist, rank, world, device=f"cuda:{device}", align=align)
+        kinds = syn.variable_kinds(spec.stage_dims[sc.plan.s0:sc.plan.s1])
+        rng = np.random.default_rng(seed0)
+        xl, xu = np.zeros(len(kinds)), np.ones(len(kinds))
+        x, _ = syn.random_point(kinds, xl + 0.1, xu, 1, seed0)
+        x = np.concatenate([x, np.zeros(sc.n_x - sc.plan.n_loc)])
+        return Runner(sc.ev, x, rng.standard_normal(sc.ev.m), 1, sharded=sc)
+    fn = {"scopf": compose_scopf, "multiperiod": compose_multiperiod, "general": compose_general}[kind]
+    p, imap = fn(*args, device=device)
     ev = p.evaluator
     kinds = syn.variable_kinds([(pl.topo.nb, pl.topo.ng) for pl in ev.plans])
     x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, seed0)
-    return ev, x, mult, 1
+    return Runner(ev, x, mult, 1)
 
 
 def algorithmic_bytes(ev) -> int:
@@ -264,7 +290,9 @@ def main():
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    ev, x_h, m_h, units = build_ours(args.config, args.points, local, seed0=1_000_000 * (rank + 1))
+    run = build_ours(args.config, args.points, local, seed0=1_000_000 * (rank + 1), dist=dist if world > 1 else None,
+                     rank=rank, world=world)
+    ev, x_h, m_h, units, sc = run.ev, run.x_h, run.m_h, run.units, run.sharded
     x = torch.from_numpy(x_h).to(dev)
     mult = torch.from_numpy(m_h).to(dev)
     out = ev.alloc()
@@ -275,8 +303,14 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     from paper_2203_10587_b200 import _lib as L
 
+    def step():
+        if sc is None:
+            ev.eval_device(x, mult, 1.0, L.ALL, out=out, stream=sptr)
+        else:
+            sc.evaluate(x, mult, 1.0, L.ALL, out=out, stream=sptr)
+
     for _ in range(max(args.warmup, 0)):
-        ev.eval_device(x, mult, 1.0, L.ALL, out=out, stream=sptr)
+        step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -288,7 +322,7 @@ def main():
         for k in range(args.steps):
             flush.zero_()
             starts[k].record(stream)
-            ev.eval_device(x, mult, 1.0, L.ALL, out=out, stream=sptr)
+            step()
             ends[k].record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
@@ -300,17 +334,22 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    value = units * world * args.steps / (total_ms / 1000.0)
+    # config 1: every rank evaluates its own batch (weak); composites: one composite over all ranks (strong)
+    value = (units * world if sc is None else units) * args.steps / (total_ms / 1000.0)
 
     # roofline of the (single) evaluation kernel
     bytes_step = algorithmic_bytes(ev)
+    if world > 1 and sc is not None:
+        b = torch.tensor([float(bytes_step)], dtype=torch.float64, device=dev)
+        dist.all_reduce(b)              # the whole composite's bytes
+        bytes_step = int(b.item())
     kernel_ms = statistics.mean(step_ms)
     peaks_path = os.path.join(HERE, "MEASURED_PEAKS.json")
     if os.path.exists(peaks_path):
         peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured"
     else:
         peak, peak_src = FALLBACK_HBM_GBS, "fallback"
-    achieved = bytes_step / (kernel_ms / 1000.0) / 1e9
+    achieved = bytes_step / (kernel_ms / 1000.0) / 1e9 / (world if sc is not None else 1)
     traffic = None
     tpath = os.path.join(HERE, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -318,7 +357,7 @@ def main():
 
     # end to end through the C ABI with pinned host buffers (H2D + eval + D2H per step)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and sc is None:
         xp = torch.from_numpy(x_h).pin_memory()
         mp_ = torch.from_numpy(m_h).pin_memory()
         hout = {k: torch.empty(v.numel(), dtype=torch.float64).pin_memory() for k, v in out.items()}
@@ -350,12 +389,14 @@ def main():
         cfg = workload_desc(args.config, args.points)
         cfg.update(points_per_step=units if args.config == 1 else None, stages_per_step=len(ev.plans),
                    l2="256 MiB buffer written between timed steps (untimed)",
-                   parallelism=f"replicas x{world}" if world > 1 else "single GPU",
+                   parallelism=(f"replicas x{world}" if sc is None else f"stage shards x{world} (NCCL halo + objective)")
+                   if world > 1 else "single GPU",
                    algorithmic_bytes_per_step=bytes_step)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8d)",
+            "scaling": "weak" if (args.config == 1 or world == 1) else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, SURVEY §8d)",
             "config": cfg,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -22,7 +22,7 @@ allocator/stream plumbing; all arithmetic happens in the CUDA kernel).
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -48,13 +48,13 @@ class Coupling:
     """Coupling rows in flat-buffer coordinates (composer.py:229-242)."""
     row: np.ndarray                   # cons row
     col_a: np.ndarray                 # x index of the child quantity
-    col_b: np.ndarray                 # x index of the base quantity
-    is_eq: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=bool))
+    col_b: np.ndarray                 # x index of the base quantity (may point into a halo)
+    base_first: np.ndarray | None = None   # base column sorts first (default: col_b < col_a)
 
 
 class BatchEvaluator:
     def __init__(self, plans, *, device: int = 0, layout: str = "independent",
-                 coupling: Coupling | None = None, n_pins: int = 0):
+                 coupling: Coupling | None = None, n_pins: int = 0, obj_terms: bool = False):
         if layout not in ("independent", "composite"):
             raise ValueError("layout must be 'independent' or 'composite'")
         self.plans = list(plans)
@@ -121,6 +121,7 @@ class BatchEvaluator:
         sizes = np.zeros((S, 6), dtype=np.int64)
         L.check(lib.acopf_batch_stage_sizes(h, L.ptr(sizes, ctypes.c_int64)))
         self.sizes = sizes
+        self.obj_terms = obj_terms
         self._layout(coupling, n_pins)
 
     # -- layout ---------------------------------------------------------------
@@ -164,7 +165,10 @@ class BatchEvaluator:
             jeq_base = prefix(jeq)[:-1]
             jin_base = jeq_all + 2 * n_pins + prefix(jin)[:-1]
             self.nnz_j = jeq_all + 2 * n_pins + int(jin.sum()) + 2 * n_box
-            obj_mode, obj_slot, self.n_obj = L.OBJ_WEIGHTED, np.arange(S), 1
+            if self.obj_terms:
+                obj_mode, obj_slot, self.n_obj = L.OBJ_TERMS, np.arange(S), S
+            else:
+                obj_mode, obj_slot, self.n_obj = L.OBJ_WEIGHTED, np.arange(S), 1
             cp = coupling
         self.var_off = var_off[:-1]
         self.eq_row, self.ineq_row = np.asarray(eq_row), np.asarray(ineq_row)
@@ -180,7 +184,7 @@ class BatchEvaluator:
                             int(jeq.sum()) + 2 * n_pins + int(jin.sum()) + 2 * (rows - self.m_eq - int(mineq.sum())))
             jpos = L.i64(jpos)
             ca, cb = L.i64(cp.col_a), L.i64(cp.col_b)
-            first = np.ascontiguousarray(cb < ca, dtype=np.int8)
+            first = np.ascontiguousarray(cb < ca if cp.base_first is None else cp.base_first, dtype=np.int8)
         else:
             rows = jpos = ca = cb = L.i64(np.zeros(1))
             first = np.zeros(1, dtype=np.int8)

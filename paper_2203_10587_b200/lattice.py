@@ -23,6 +23,8 @@ are materialised lazily (they hold a NetworkCase / dicts per element).
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 from .errors import EmptyScenarioSet, InvalidPlan, IslandingDetected, TopologyMismatch
@@ -134,6 +136,23 @@ def _bridges(pc: PackedCase) -> set:
     return out
 
 
+@dataclass
+class CompositeSpec:
+    """A composite lattice without its evaluator (used for sharding across GPUs)."""
+    plans: list
+    cp: dict                  # coupling rows: kind, stage_a/b, gen, bus, bound, row, col_a/b (global)
+    n_pins: int
+    n_s: np.ndarray           # per-stage n, m_eq, m_ineq
+    meq_s: np.ndarray
+    mineq_s: np.ndarray
+    var_off: np.ndarray
+    eq_off: np.ndarray
+    ineq_off: np.ndarray
+    m_eq: int
+    m_ineq: int
+    stage_dims: list          # (nb, ng) per stage
+
+
 class _Stage:
     __slots__ = ("s_pos", "c_pos", "t", "scen", "ctg", "weight", "topo", "removed", "pt",
                  "pmin", "pmax", "gen_live", "case_gen_live")
@@ -238,7 +257,8 @@ class _Lattice:
 
     # -- assembly -------------------------------------------------------------------
 
-    def assemble(self):
+    def spec(self) -> "CompositeSpec":
+        """Stage plans, offsets and coupling rows -- everything but the evaluator."""
         st = self.stages
         ns = len(st)
         plans = []
@@ -299,6 +319,18 @@ class _Lattice:
         cp = dict(kind=cat(kind_code, np.int8), stage_a=cat(sa, np.int64), stage_b=cat(sb, np.int64),
                   gen=cat(gen, np.int64), bus=cat(bus, np.int64), bound=cat(bound, np.float64),
                   row=cat(row, np.int64), col_a=cat(col_a, np.int64), col_b=cat(col_b, np.int64))
+        return CompositeSpec(plans=plans, cp=cp, n_pins=n_pins, n_s=n_s, meq_s=meq_s, mineq_s=mineq_s,
+                             var_off=var_off, eq_off=eq_off, ineq_off=ineq_off, m_eq=m_eq, m_ineq=m_ineq,
+                             stage_dims=[(s.topo.nb, s.topo.ng) for s in st])
+
+    def assemble(self):
+        sp = self.spec()
+        st = self.stages
+        ns = len(st)
+        plans, cp, n_pins = sp.plans, sp.cp, sp.n_pins
+        n_s, meq_s, mineq_s = sp.n_s, sp.meq_s, sp.mineq_s
+        var_off, eq_off, ineq_off = sp.var_off, sp.eq_off, sp.ineq_off
+        nv, m_eq, m_ineq = int(n_s.sum()), sp.m_eq, sp.m_ineq
         self.cp = cp
         ev = BatchEvaluator(plans, device=self.device, layout="composite",
                             coupling=Coupling(row=cp["row"], col_a=cp["col_a"], col_b=cp["col_b"]),
@@ -406,7 +438,7 @@ def _ctg_order(ctgs):
     return [None] if ctgs is None else [None] + list(ctgs.by_id())
 
 
-def _general_impl(scenarios, ctgs, periods, mode, dt_minutes, name, device):
+def _general_impl(scenarios, ctgs, periods, mode, dt_minutes, name, device, spec_only=False):
     if not periods:
         raise InvalidPlan("at least one period is required")
     nt = len(periods)
@@ -441,7 +473,7 @@ def _general_impl(scenarios, ctgs, periods, mode, dt_minutes, name, device):
             lat.mode_rows(idx[(si, ci, 0)], idx[(si, 0, 0)], mode)
         if si > 0:
             lat.scenario_rows(idx[(si, 0, 0)], idx[(0, 0, 0)], mode)
-    return lat.assemble()
+    return lat.spec() if spec_only else lat.assemble()
 
 
 def compose_multiperiod(cases, dt_minutes: float, *, device: int = 0):
@@ -501,3 +533,22 @@ def compose_sopf_flat(base, scenarios, ctgs, mode, *, device: int = 0):
         lat.mode_rows(k, 0, mode, box_kind=CONTINGENCY_BOX if ci > 0 else SCENARIO_BOX,
                       scale=mode.contingency_scale if ci > 0 else mode.scenario_scale)
     return lat.assemble()
+
+
+def composite_spec(kind: str, *args, **kw) -> CompositeSpec:
+    """The lattice of compose_<kind>(*args) without building an evaluator.
+
+    kind: "multiperiod" (cases, dt), "scopf" (base, ctgs, mode), "general"
+    (scenarios, ctgs, periods, mode, dt).  Used by :mod:`dispatch` to shard
+    the stages over ranks.
+    """
+    if kind == "multiperiod":
+        cases, dt = args
+        return _general_impl(None, None, list(cases), CouplingMode(), dt, "tcopf", 0, spec_only=True)
+    if kind == "scopf":
+        base, ctgs, mode = args
+        return _general_impl(None, ctgs, [base], mode, 30.0, "scopf", 0, spec_only=True)
+    if kind == "general":
+        scens, ctgs, periods, mode, dt = args
+        return _general_impl(scens, ctgs, list(periods), mode, dt, "general", 0, spec_only=True)
+    raise ValueError(f"unknown composite kind {kind!r}")

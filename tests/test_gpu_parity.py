@@ -253,3 +253,34 @@ def test_disconnected_and_bad_inputs():
     p, _ = pkg.build_acopf(case)
     with pytest.raises(ValueError):
         p.constraints(np.zeros(p.n + 1))
+
+
+def test_sharded_path_single_rank_nccl():
+    """ShardedComposite on one NCCL rank == the unsharded composite, bitwise (collectives on GPU)."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2203_10587_b200.dispatch import ShardedComposite
+    from paper_2203_10587_b200.lattice import composite_spec
+    base, ctgs = syn.config2_inputs(n_ctg=9, nb=200, n_chords=60, ng=40)
+    spec = composite_spec("scopf", base, ctgs, CouplingMode())
+    p, _ = pkg.compose_scopf(base, ctgs, CouplingMode())
+    kinds = syn.variable_kinds(spec.stage_dims)
+    x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 9)
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        sc = ShardedComposite(spec, dist, 0, 1, device="cuda:0")
+        xd = sc.alloc_x()
+        xd[:sc.plan.n_loc] = torch.from_numpy(x).cuda()
+        out, obj = sc.evaluate(xd, torch.from_numpy(mult).cuda(), 1.25, L.ALL)
+        torch.cuda.synchronize()
+        ref = p.evaluator.eval_host(x, mult, 1.25, L.ALL)
+        assert obj == float(ref["obj"][0])
+        for k in ("grad", "cons", "jac", "hess"):
+            assert C.bit_diffs(out[k].cpu().numpy()[:len(ref[k])], ref[k]) == 0, k
+    finally:
+        dist.destroy_process_group()
