@@ -15,7 +15,7 @@ import numpy as np
 from .errors import DeviceError
 
 LIB_NAME = "libacopf_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("ACOPF_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 OBJ, GRAD, CONS, JAC, HESS = 1, 2, 4, 8, 16
 ALL = 31

@@ -37,19 +37,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(os.path.join(CSRC, d)) <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
     table = os.path.join(CSRC, "sincos_table.h")
     gen = os.path.join(CSRC, "gen_sincos_table.py")
     if force or not os.path.exists(table) or os.path.getmtime(table) < os.path.getmtime(gen):
         subprocess.run([sys.executable, gen, table], check=True)
-    if not force and up_to_date():
+    target = out or OUT
+    if not force and not defines and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT] + [os.path.join(CSRC, s) for s in SOURCES]
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", target] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    return OUT
+    return target
 
 
 if __name__ == "__main__":

@@ -108,8 +108,13 @@ struct acopf_batch {
     // host staging for eval_host
     DevBuf h_x, h_m, h_obj, h_g, h_c, h_j, h_h;
 
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ~acopf_batch() {
         if (stream) cudaStreamDestroy(stream);
+        if (aux_stream) cudaStreamDestroy(aux_stream);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
     }
 };
 
@@ -119,6 +124,9 @@ static void upload(acopf_batch* b) {
     const int S = (int)b->stages.size();
     const int64_t n_coupling = (int64_t)b->cp_row.size();
     if (!b->stream) cuda_check(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "stream");
+    if (!b->aux_stream) cuda_check(cudaStreamCreateWithFlags(&b->aux_stream, cudaStreamNonBlocking), "stream");
+    if (!b->ev_fork) cuda_check(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming), "event");
+    if (!b->ev_join) cuda_check(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming), "event");
 
     // topologies (only what the aux kernel needs; the bus kernel reads tile tables)
     std::vector<DTopo> dt;
@@ -456,16 +464,26 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
         const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD)) && P.n_bus_items > 0;
         const bool aux = (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
+        // the generator/coupling kernel runs concurrently on a forked stream
+        const bool fork = aux && bus;
+        if (fork) {
+            cuda_check(cudaEventRecord(b->ev_fork, st), "event record");
+            cuda_check(cudaStreamWaitEvent(b->aux_stream, b->ev_fork, 0), "stream wait");
+        }
         if (aux) {
-            acopf_aux_kernel<<<P.n_aux_items, BLOCK, b->aux_smem, st>>>(P);
+            acopf_aux_kernel<<<P.n_aux_items, BLOCK, b->aux_smem, fork ? b->aux_stream : st>>>(P);
             cuda_check(cudaGetLastError(), "acopf_aux_kernel launch");
             b->launches++;
         }
         if (bus) {
-            if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
-            else acopf_bus_kernel<0u><<<P.n_bus_items, BLOCK, b->smem, st>>>(P);
+            if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P);
+            else acopf_bus_kernel<0u><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P);
             cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
             b->launches++;
+        }
+        if (fork) {
+            cuda_check(cudaEventRecord(b->ev_join, b->aux_stream), "event record");
+            cuda_check(cudaStreamWaitEvent(st, b->ev_join, 0), "stream wait");
         }
     });
 }

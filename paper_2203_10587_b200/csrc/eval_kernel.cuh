@@ -95,7 +95,14 @@ struct EvalParams {
     unsigned* counter;
 };
 
-constexpr int BLOCK = 256;
+#ifndef ACOPF_BUS_BLOCK
+#define ACOPF_BUS_BLOCK 256
+#endif
+#ifndef ACOPF_BUS_MINB
+#define ACOPF_BUS_MINB 2
+#endif
+constexpr int BLOCK = 256;                     // aux kernel
+constexpr int BUS_BLOCK = ACOPF_BUS_BLOCK;     // bus kernel (>= TILE_MAX_BUSES: one bus per thread)
 constexpr int GEN_CHUNK = 256;
 constexpr int CP_CHUNK = 1024;
 
@@ -303,7 +310,7 @@ __host__ __device__ __forceinline__ size_t bus_smem_layout(int table_bytes, int 
 }
 
 template <unsigned WHAT>
-__global__ void __launch_bounds__(BLOCK, 2) acopf_bus_kernel(const EvalParams P) {
+__global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(const EvalParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
     const DBusItem it = P.bus_items[blockIdx.x];

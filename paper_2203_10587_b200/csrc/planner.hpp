@@ -51,8 +51,14 @@ constexpr int HSLOT_T[10] = {-1, 0, -1, 1, 2, 3, 4, -1, 5, 6};
 constexpr int POS_OF_SLOT_F[7] = {0, 1, 2, 3, 5, 7, 8};
 constexpr int POS_OF_SLOT_T[7] = {1, 3, 4, 5, 6, 8, 9};
 
-constexpr int TILE_MAX_ENDS = 192;   // soft cap; a single high-degree bus may exceed it
-constexpr int TILE_MAX_BUSES = 96;    // <= kernel block size (one bus per thread)
+#ifndef ACOPF_TILE_ENDS
+#define ACOPF_TILE_ENDS 192
+#endif
+#ifndef ACOPF_TILE_BUSES
+#define ACOPF_TILE_BUSES 96
+#endif
+constexpr int TILE_MAX_ENDS = ACOPF_TILE_ENDS;    // soft cap; a single high-degree bus may exceed it
+constexpr int TILE_MAX_BUSES = ACOPF_TILE_BUSES;  // <= bus kernel block size (one bus per thread)
 constexpr int SMEM_LIMIT_BYTES = 220 * 1024;
 
 // symbolic term: what a COO entry's value is made of
