@@ -206,11 +206,10 @@ static void upload(acopf_batch* b) {
                     recs.push_back(r);
                 }
                 items.push_back(it);
-                size_t q, sg, gv, gb, rs, fo, rc;
+                size_t q, gv, gb, rs, fo, rc;
                 const TileTable& tt = b->tables[kv.first];
-                const int nent = tt.L[0] + tt.L[1] + tt.L[2] + tt.L[3];
                 max_smem = std::max(max_smem, bus_smem_layout(table_bytes[kv.first], tt.nQ(), (int)tt.ends.size(),
-                                                              tt.nB, it.count, nent, &q, &sg, &gv, &gb, &rs, &fo, &rc));
+                                                              tt.nB, it.count, &q, &gv, &gb, &rs, &fo, &rc));
             }
         }
     }

@@ -135,15 +135,7 @@ struct TileView {
     const double* gs;
     const double* bs;
     const double* adm;
-    const unsigned* edst;
-    double* stg;              // staging copy of the tile's four output segments
-    const int* sbase;         // (shared) staging index of each segment's first entry, this stage
 };
-
-// staging index of an entry destination (segment << 30 | local)
-__device__ __forceinline__ int stg_index(const TileView& V, unsigned dst) {
-    return V.sbase[dst >> 30] + (int)(dst & 0x3FFFFFFFu);
-}
 
 __device__ __forceinline__ double hpos(int p, double cpf, double cqf, double cpt, double cqt,
                                        double s2f, double s2t, const double* gpf, const double* gqf,
@@ -260,15 +252,8 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, c
         for (int i = 0; i < 4; ++i) {
             gp[i] = side ? gpt[i] : gpf[i];
             gq[i] = side ? gqt[i] : gqf[i];
-        }
-        // an end's direct slots are its off-diagonal partials: odd columns for a
-        // from-end (VA_t, VM_t), even ones for a to-end; they go straight to staging
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const double v = i < 4 ? -gp[i] : -gq[i - 4];
-            const unsigned dst = ((i & 1) != side) ? V.edst[(i >> 1) * ne + e] : NO_DST;
-            if (dst != NO_DST) V.stg[stg_index(V, dst)] = v;
-            else q[Q_JP + i] = v;
+            q[Q_JP + i] = -gp[i];
+            q[Q_JQ + i] = -gq[i];
         }
         if (r >= 0) {
             const double fp = side ? pt : pf, fq = side ? qt : qf;
@@ -297,37 +282,24 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, c
         const double hqf[10] = {-vvw, vvw, vtu, vfu, -vvw, -vtu, -vfu, -(2.0 * bff), w, z};
         const double hpt[10] = {-vvu2, vvu2, vtw2, vfw2, -vvu2, -vtw2, -vfw2, z, u2, 2.0 * gtt};
         const double hqt[10] = {-vvw2, vvw2, -vtu2, -vfu2, -vvw2, vtu2, vfu2, z, w2, -(2.0 * btt)};
-        // direct H slots: from-end slots 1,3,4,6 / to-end slots 0,1,3,5 (planner DIR_SLOT_*)
         if (side == 0) {
 #pragma unroll
-            for (int s = 0; s < 7; ++s) {
-                const double v = hpos(slot_pos_f(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
-                const int j = s == 1 ? 4 : s == 3 ? 5 : s == 4 ? 6 : s == 6 ? 7 : -1;
-                const unsigned dst = j >= 0 ? V.edst[j * ne + e] : NO_DST;
-                if (dst != NO_DST) V.stg[stg_index(V, dst)] = v;
-                else q[Q_H + s] = v;
-            }
+            for (int s = 0; s < 7; ++s)
+                q[Q_H + s] = hpos(slot_pos_f(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
         } else {
 #pragma unroll
-            for (int s = 0; s < 7; ++s) {
-                const double v = hpos(slot_pos_t(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
-                const int j = s == 0 ? 4 : s == 1 ? 5 : s == 3 ? 6 : s == 5 ? 7 : -1;
-                const unsigned dst = j >= 0 ? V.edst[j * ne + e] : NO_DST;
-                if (dst != NO_DST) V.stg[stg_index(V, dst)] = v;
-                else q[Q_H + s] = v;
-            }
+            for (int s = 0; s < 7; ++s)
+                q[Q_H + s] = hpos(slot_pos_t(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
         }
     }
 }
 
 // Dynamic shared memory of one bus CTA (must match the host's bus_smem_bytes).
 __host__ __device__ __forceinline__ size_t bus_smem_layout(int table_bytes, int nQ, int nE, int nB, int count,
-                                                           int nEntries, size_t* o_q, size_t* o_stg, size_t* o_gv,
-                                                           size_t* o_gb, size_t* o_rs, size_t* o_fo, size_t* o_rec) {
+                                                           size_t* o_q, size_t* o_gv, size_t* o_gb, size_t* o_rs,
+                                                           size_t* o_fo, size_t* o_rec) {
     size_t off = (size_t)table_bytes;
     *o_q = off;   off += 8 * (size_t)nQ;
-    off = (off + 15) & ~size_t(15);
-    *o_stg = off; off += 8 * (size_t)(nEntries + 8);
     *o_gv = off;  off += 8 * (size_t)GV * nE;
     *o_gb = off;  off += 8 * (size_t)GB * nB;
     *o_rs = off;  off += 4 * (size_t)nE;
@@ -369,12 +341,9 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
                 : "memory");
         }
     }
-    size_t o_q, o_stg, o_gv, o_gb, o_rs, o_fo, o_rec;
-    const int nEntries = H->LP + H->LQ + H->LHA + H->LHV;
-    bus_smem_layout(H->bytes, H->nQ, H->nE, H->nB, it.count, nEntries, &o_q, &o_stg, &o_gv, &o_gb, &o_rs, &o_fo,
-                    &o_rec);
+    size_t o_q, o_gv, o_gb, o_rs, o_fo, o_rec;
+    bus_smem_layout(H->bytes, H->nQ, H->nE, H->nB, it.count, &o_q, &o_gv, &o_gb, &o_rs, &o_fo, &o_rec);
     double* Q = reinterpret_cast<double*>(smem + o_q);
-    double* stg = reinterpret_cast<double*>(smem + o_stg);
     double* Gv = reinterpret_cast<double*>(smem + o_gv);
     double* Gb = reinterpret_cast<double*>(smem + o_gb);
     int* RS = reinterpret_cast<int*>(smem + o_rs);
@@ -407,9 +376,6 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
     V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
     V.bs = reinterpret_cast<const double*>(smem + H->o_bs);
     V.adm = reinterpret_cast<const double*>(smem + H->o_adm);
-    V.edst = reinterpret_cast<const unsigned*>(smem + H->o_edst);
-    V.stg = stg;
-    __shared__ int s_sbase_buf[2][4];        // by stage parity (phase C of stage s-1 may still read)
     // WHAT != 0: the mask is a compile-time constant (the all-callbacks path)
     const unsigned what = WHAT ? WHAT : P.what;
     const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
@@ -421,19 +387,6 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
 
     for (int ri = 0; ri < it.count; ++ri) {
         const SRec& R = recs[ri];
-        // staging bases with the parity of the segments' global element offsets, so
-        // every segment's interior moves as a 16-byte aligned bulk copy
-        int* s_sbase = s_sbase_buf[ri & 1];
-        V.sbase = s_sbase;
-        if (threadIdx.x == 0) {
-            int b = (int)(R.oP & 1);
-            s_sbase[0] = b;
-            b += H->LP; b += (int)((R.oQ - b) & 1); s_sbase[1] = b;
-            b += H->LQ; b += (int)((R.oA - b) & 1); s_sbase[2] = b;
-            b += H->LHA; b += (int)((R.oV - b) & 1); s_sbase[3] = b;
-        }
-        // the previous stage's bulk stores must have read the staging copy
-        if (threadIdx.x < 4) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         // ---- A: branch ends ------------------------------------------------
@@ -454,8 +407,8 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
             }
         }
         __syncthreads();
-        // the gather buffers are free again: gather the next stage's inputs
-        // while this stage's balance rows and summed entries are formed
+        // the staging buffers are free again: gather the next stage's inputs
+        // while this stage's balance rows and scatter sums are stored
         double vm_c = 0.0, pd_c = 0.0, qd_c = 0.0;
         const int blc = threadIdx.x;
         if (need_c && blc < nbt) { vm_c = Gb[blc]; pd_c = Gb[3 * nbt + blc]; qd_c = Gb[4 * nbt + blc]; }
@@ -463,7 +416,7 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
             __syncthreads();
             issue_gathers(P, recs[ri + 1], V, Gv, Gb, RS, FO, need_h, need_c);
         }
-        // ---- B: balance rows, then the duplicate-summed entries -------------------
+        // ---- B: balance rows, then the scatter-map sums -------------------------
         if (need_c) {
             const double* pgv = P.x + R.var_off + 2 * R.nb;
             const double* qgv = pgv + R.ng;
@@ -491,6 +444,17 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
         const unsigned short* mterms = reinterpret_cast<const unsigned short*>(smem + H->o_mterms);
         for (int cls = 0; cls < 2; ++cls) {
             if (cls == 0 ? !need_j : !need_h) continue;
+            double* o0 = cls == 0 ? P.jval + R.oP : P.hval + R.oA;
+            double* o1 = cls == 0 ? P.jval + R.oQ : P.hval + R.oV;
+            const int ns = cls == 0 ? H->nSJ : H->nSH;
+            const unsigned* sdst = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_sj_dst : H->o_sh_dst));
+            const unsigned short* sterm =
+                reinterpret_cast<const unsigned short*>(smem + (cls == 0 ? H->o_sj_term : H->o_sh_term));
+            for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+                const unsigned d = sdst[i];
+                double* o = (d & 0x80000000u) ? o1 : o0;
+                o[d & 0x7fffffffu] = Q[sterm[i]];
+            }
             const int nm = cls == 0 ? H->nMJ : H->nMH;
             const unsigned* mdst = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_mj_dst : H->o_mh_dst));
             const unsigned* minfo = reinterpret_cast<const unsigned*>(smem + (cls == 0 ? H->o_mj_info : H->o_mh_info));
@@ -500,30 +464,11 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
                 const int c = (int)(info & 1023u);
                 double v = Q[tp[0]];
                 for (int k = 1; k < c; ++k) v = v + Q[tp[k]];
-                stg[stg_index(V, d)] = v;
-            }
-        }
-        // ---- C: the staging copy leaves as four bulk stores ----------------------
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (threadIdx.x < 4) {
-            const int sg = threadIdx.x;
-            if (sg < 2 ? need_j : need_h) {
-                const long long go = sg == 0 ? R.oP : sg == 1 ? R.oQ : sg == 2 ? R.oA : R.oV;
-                double* gbase = (sg < 2 ? P.jval : P.hval) + go;
-                const double* sbase = stg + s_sbase[sg];
-                int n = sg == 0 ? H->LP : sg == 1 ? H->LQ : sg == 2 ? H->LHA : H->LHV, lo = 0;
-                if (n > 0 && (reinterpret_cast<uintptr_t>(gbase) & 15)) { gbase[0] = sbase[0]; lo = 1; n--; }
-                if (n & 1) { gbase[lo + n - 1] = sbase[lo + n - 1]; n--; }
-                if (n > 0)
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gbase + lo),
-                                 "r"(smem_u32(sbase + lo)), "r"(8 * n)
-                                 : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                double* o = (d & 0x80000000u) ? o1 : o0;
+                o[d & 0x7fffffffu] = v;
             }
         }
     }
-    if (threadIdx.x < 4) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------

@@ -242,33 +242,30 @@ inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
 }
 
 // ---------------------------------------------------------------------------
-// Tile tables (serialised into one device blob, bulk-copied to shared memory)
-//
-// Entry destinations are (segment << 30 | position within the tile's run of
-// that segment); segments 0..3 = J rows P_i, J rows Q_i, H rows VA_i, H rows
-// VM_i.  The kernel assembles each segment in a shared-memory staging copy and
-// writes it out with one TMA bulk store.
+// Tile tables (serialised into one device blob)
 
-// Direct slots: the 8 off-diagonal entries a branch end owns alone (no parallel
-// twin, no self-loop); phase A writes them into the staging copy.  Quantity
-// slot per side, in order: J (P row: 2, Q row: 2), then H (4).
-constexpr int NDIR = 8;
-constexpr uint32_t NO_DST = 0xFFFFFFFFu;
-constexpr int DIR_SLOT_F[NDIR] = {Q_JP + 1, Q_JP + 3, Q_JQ + 1, Q_JQ + 3, Q_H + 1, Q_H + 3, Q_H + 4, Q_H + 6};
-constexpr int DIR_SLOT_T[NDIR] = {Q_JP + 0, Q_JP + 2, Q_JQ + 0, Q_JQ + 2, Q_H + 0, Q_H + 1, Q_H + 3, Q_H + 5};
-
-struct TileHdr {            // 128 bytes; offsets in bytes from the header start
+struct TileHdr {            // 192 bytes; offsets in bytes from the header start
     int32_t b0, nB, nE, nQ;           // first bus, buses, ends, shared doubles for quantities
     int32_t LP, LQ, LHA, LHV;         // entries of the four row segments
-    int32_t ngl, bytes, nMJ, nMH;     // generator ids, serialised size, summed J / H entries
-    int32_t nMT, o_code, o_f, o_t;    // summed terms
-    int32_t o_ridx, o_foff, o_busptr, o_gptr;
-    int32_t o_glist, o_gs, o_bs, o_adm;
-    int32_t o_edst, o_mj_dst, o_mj_info, o_mh_dst;
-    int32_t o_mh_info, o_mterms, pad0, pad1;
+    int32_t ngl, bytes, nSJ, nSH;     // generator ids, serialised size, single-term J / H entries
+    int32_t nMJ, nMH, nMT, pad0;      // multi-term J / H entries, their term count
+    int32_t o_code, o_f, o_t, o_ridx;
+    int32_t o_foff, o_busptr, o_gptr, o_glist;
+    int32_t o_gs, o_bs, o_adm, o_sj_dst;
+    int32_t o_sj_term, o_sh_dst, o_sh_term, o_mj_dst;
+    int32_t o_mj_info, o_mh_dst, o_mh_info, o_mterms;
+    int32_t pad[12];
 };
-static_assert(sizeof(TileHdr) == 128, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
 
+// A tile's complete working set, copied to shared memory in one bulk copy:
+// per-end topology (bus slots, rated index, flow-row offset, SoA admittances),
+// per-bus shunts and generator lists, and the scatter map split into classes:
+//   single-term entries  dst (bit 31: Q row / VM row segment, else P / VA)
+//                        + the one quantity slot;
+//   multi-term entries   dst + (first term << 10 | term count), sorted by
+//                        decreasing count: warps run uniform trip counts and
+//                        the longest sums start first.
 struct TileTable {
     int topo = 0;
     int b0 = 0, nB = 0;
@@ -277,28 +274,28 @@ struct TileTable {
     int L[4] = {0, 0, 0, 0};      // entries in P, Q, VA, VM segments
     std::vector<int> cols;        // stage-local column per entry (pattern export)
     std::vector<int> rowlen;      // entries per row, 4 segments x nB rows
-    std::vector<uint32_t> edst;   // [j * nE + e]: destination of end e's j-th direct slot, or NO_DST
-    std::vector<uint32_t> mdst[2];      // summed entries ([0] J, [1] H): destination
-    std::vector<uint32_t> minfo[2];     //                 (first term << 10 | term count)
-    std::vector<uint16_t> mterms;       // shared-memory quantity slot per term
+    std::vector<uint32_t> sdst[2];      // [0] J, [1] H
+    std::vector<uint16_t> sterm[2];
+    std::vector<uint32_t> mdst[2];
+    std::vector<uint32_t> minfo[2];
+    std::vector<uint16_t> mterms;
     int nQ() const { return EQ * (int)ends.size() + BQ * nB + 1; }
-    int nE() const { return (int)ends.size(); }
     void serialise(const Topo& T, std::vector<uint8_t>& blob) const;
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) const {
-    const int ne = nE();
-    std::vector<int> f(ne), t(ne), ridx(ne), foff(ne), gptr(1, 0), glist;
-    std::vector<double> adm(8 * (size_t)ne), gs(nB), bs(nB);
-    for (int e = 0; e < ne; ++e) {
+    const int nE = (int)ends.size();
+    std::vector<int> f(nE), t(nE), ridx(nE), foff(nE), gptr(1, 0), glist;
+    std::vector<double> adm(8 * (size_t)nE), gs(nB), bs(nB);
+    for (int e = 0; e < nE; ++e) {
         int k = ends[e] >> 1;
         f[e] = T.fo[k];
         t[e] = T.to[k];
         ridx[e] = T.ridx[k];
         foff[e] = T.ridx[k] >= 0 ? (int)T.foff[T.ridx[k]] : 0;
-        for (int q = 0; q < 8; ++q) adm[(size_t)q * ne + e] = T.adm[8 * (size_t)k + q];
+        for (int q = 0; q < 8; ++q) adm[(size_t)q * nE + e] = T.adm[8 * (size_t)k + q];
     }
     for (int bl = 0; bl < nB; ++bl) {
         int i = b0 + bl;
@@ -308,25 +305,29 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
         gptr.push_back((int)glist.size());
     }
     TileHdr h{};
-    h.b0 = b0; h.nB = nB; h.nE = ne; h.nQ = nQ();
+    h.b0 = b0; h.nB = nB; h.nE = nE; h.nQ = nQ();
     h.LP = L[0]; h.LQ = L[1]; h.LHA = L[2]; h.LHV = L[3];
     h.ngl = (int)glist.size();
+    h.nSJ = (int)sdst[0].size(); h.nSH = (int)sdst[1].size();
     h.nMJ = (int)mdst[0].size(); h.nMH = (int)mdst[1].size();
     h.nMT = (int)mterms.size();
     size_t off = sizeof(TileHdr);
     auto take = [&](size_t n) { int o = (int)off; off = align16(off + n); return o; };
-    h.o_code = take(4 * (size_t)ne);
-    h.o_f = take(4 * (size_t)ne);
-    h.o_t = take(4 * (size_t)ne);
-    h.o_ridx = take(4 * (size_t)ne);
-    h.o_foff = take(4 * (size_t)ne);
+    h.o_code = take(4 * (size_t)nE);
+    h.o_f = take(4 * (size_t)nE);
+    h.o_t = take(4 * (size_t)nE);
+    h.o_ridx = take(4 * (size_t)nE);
+    h.o_foff = take(4 * (size_t)nE);
     h.o_busptr = take(4 * busptr.size());
     h.o_gptr = take(4 * gptr.size());
     h.o_glist = take(4 * glist.size());
     h.o_gs = take(8 * (size_t)nB);
     h.o_bs = take(8 * (size_t)nB);
     h.o_adm = take(8 * adm.size());
-    h.o_edst = take(4 * edst.size());
+    h.o_sj_dst = take(4 * sdst[0].size());
+    h.o_sj_term = take(2 * sterm[0].size());
+    h.o_sh_dst = take(4 * sdst[1].size());
+    h.o_sh_term = take(2 * sterm[1].size());
     h.o_mj_dst = take(4 * mdst[0].size());
     h.o_mj_info = take(4 * minfo[0].size());
     h.o_mh_dst = take(4 * mdst[1].size());
@@ -338,18 +339,21 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     uint8_t* p = blob.data() + base;
     std::memcpy(p, &h, sizeof h);
     auto put = [&](int o, const void* src, size_t n) { if (n) std::memcpy(p + o, src, n); };
-    put(h.o_code, ends.data(), 4 * (size_t)ne);
-    put(h.o_f, f.data(), 4 * (size_t)ne);
-    put(h.o_t, t.data(), 4 * (size_t)ne);
-    put(h.o_ridx, ridx.data(), 4 * (size_t)ne);
-    put(h.o_foff, foff.data(), 4 * (size_t)ne);
+    put(h.o_code, ends.data(), 4 * (size_t)nE);
+    put(h.o_f, f.data(), 4 * (size_t)nE);
+    put(h.o_t, t.data(), 4 * (size_t)nE);
+    put(h.o_ridx, ridx.data(), 4 * (size_t)nE);
+    put(h.o_foff, foff.data(), 4 * (size_t)nE);
     put(h.o_busptr, busptr.data(), 4 * busptr.size());
     put(h.o_gptr, gptr.data(), 4 * gptr.size());
     put(h.o_glist, glist.data(), 4 * glist.size());
     put(h.o_gs, gs.data(), 8 * (size_t)nB);
     put(h.o_bs, bs.data(), 8 * (size_t)nB);
     put(h.o_adm, adm.data(), 8 * adm.size());
-    put(h.o_edst, edst.data(), 4 * edst.size());
+    put(h.o_sj_dst, sdst[0].data(), 4 * sdst[0].size());
+    put(h.o_sj_term, sterm[0].data(), 2 * sterm[0].size());
+    put(h.o_sh_dst, sdst[1].data(), 4 * sdst[1].size());
+    put(h.o_sh_term, sterm[1].data(), 2 * sterm[1].size());
     put(h.o_mj_dst, mdst[0].data(), 4 * mdst[0].size());
     put(h.o_mj_info, minfo[0].data(), 4 * minfo[0].size());
     put(h.o_mh_dst, mdst[1].data(), 4 * mdst[1].size());
@@ -384,11 +388,12 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         for (int s = 0; s < 4; ++s) rows[s * tt.nB + (i - b0)] = std::move(r4[s]);
     }
     const int nE = (int)tt.ends.size();
-    tt.edst.assign((size_t)NDIR * nE, NO_DST);
+    // classify entries: single-term gather-stores and multi-term sums
     struct Multi { uint32_t dst; std::vector<uint16_t> t; };
     std::vector<Multi> multi[2];
     for (int s = 0; s < 4; ++s) {
         const int cls = s / 2;                    // 0: J (P, Q rows), 1: H (VA, VM rows)
+        const uint32_t segbit = (s & 1) ? 0x80000000u : 0u;
         uint32_t local = 0;
         for (int r = 0; r < tt.nB; ++r) {
             const Row& row = rows[s * tt.nB + r];
@@ -396,17 +401,6 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             tt.L[s] += (int)row.cols.size();
             for (size_t e = 0; e < row.cols.size(); ++e, ++local) {
                 tt.cols.push_back(row.cols[e]);
-                const uint32_t dst = ((uint32_t)s << 30) | local;
-                if (row.tptr[e + 1] - row.tptr[e] == 1 && row.terms[row.tptr[e]].kind == 0) {
-                    const Sym& y = row.terms[row.tptr[e]];
-                    const int* dslot = (y.a & 1) ? DIR_SLOT_T : DIR_SLOT_F;
-                    int j = 0;
-                    while (j < NDIR && dslot[j] != y.q) ++j;
-                    if (j < NDIR && (j < 4) == (cls == 0)) {
-                        tt.edst[(size_t)j * nE + end_pos.at(y.a)] = dst;
-                        continue;
-                    }
-                }
                 std::vector<uint16_t> slots;
                 for (int t = row.tptr[e]; t < row.tptr[e + 1]; ++t) {
                     const Sym& y = row.terms[t];
@@ -416,7 +410,12 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
                     else slot = EQ * nE + BQ * tt.nB;
                     slots.push_back((uint16_t)slot);
                 }
-                multi[cls].push_back(Multi{dst, slots});
+                if (slots.size() == 1) {
+                    tt.sdst[cls].push_back(segbit | local);
+                    tt.sterm[cls].push_back(slots[0]);
+                } else {
+                    multi[cls].push_back(Multi{segbit | local, slots});
+                }
             }
         }
     }
@@ -430,10 +429,9 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             tt.mterms.insert(tt.mterms.end(), m.t.begin(), m.t.end());
         }
     }
-    for (int s = 0; s < 4; ++s)
-        if (tt.L[s] >= (1 << 30)) throw std::runtime_error("tile segment too long");
-    size_t approx = 128 + 116 * (size_t)nE + 40 * (size_t)tt.nB + 8 * tt.cols.size() + 2 * tt.mterms.size() +
-                    8 * (size_t)tt.nQ() + 96 * (size_t)nE + 1024;
+    // shared memory = serialised table + quantity array (checked again at upload)
+    size_t approx = 192 + 84 * (size_t)nE + 24 * (size_t)tt.nB + 6 * tt.cols.size() + 2 * tt.mterms.size() +
+                    8 * (size_t)tt.nQ() + 512;
     if (approx > (size_t)SMEM_LIMIT_BYTES)
         throw std::runtime_error("bus degree too high for one tile's shared memory");
     return tt;
