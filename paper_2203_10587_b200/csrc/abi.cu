@@ -108,11 +108,16 @@ struct acopf_batch {
     // host staging for eval_host
     DevBuf h_x, h_m, h_obj, h_g, h_c, h_j, h_h;
 
+    // host-buffer pipeline (independent layouts): chunks of whole stage groups
+    struct Pipe { int s0, s1, bus_first, bus_count, aux_first, aux_count; };
+    std::vector<Pipe> pipe;
+    cudaStream_t pipe_streams[3] = {nullptr, nullptr, nullptr};
     cudaStream_t aux_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ~acopf_batch() {
         if (stream) cudaStreamDestroy(stream);
         if (aux_stream) cudaStreamDestroy(aux_stream);
+        for (auto& ps : pipe_streams) if (ps) cudaStreamDestroy(ps);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
     }
@@ -216,10 +221,34 @@ static void upload(acopf_batch* b) {
     if (max_smem > (size_t)SMEM_LIMIT_BYTES) throw std::runtime_error("tile working set exceeds shared memory");
     // aux work: generator chunks per stage, then coupling chunks
     std::vector<DAuxItem> aux;
+    std::vector<int> aux_first_of_stage(S + 1, 0);
     for (int s = 0; s < S; ++s) {
         const Topo& T = *b->topos[b->stages[s].topo];
         int nch = std::max(1, (T.ng + GEN_CHUNK - 1) / GEN_CHUNK);
+        aux_first_of_stage[s] = (int)aux.size();
         for (int c = 0; c < nch; ++c) aux.push_back(DAuxItem{0, s, c, 0});
+    }
+    aux_first_of_stage[S] = (int)aux.size();
+    // pipeline chunks for host-buffer evaluation of independent layouts: about 4
+    // chunks of whole stage groups (bus items are stage-group-major)
+    b->pipe.clear();
+    if (b->obj_mode == 0 && n_coupling == 0 && S >= 2) {
+        const int ngroups = (S + G - 1) / G;
+        const int per = std::max(1, (ngroups + 3) / 4);
+        int item = 0;
+        for (int g0 = 0; g0 < ngroups; g0 += per) {
+            acopf_batch::Pipe pc{};
+            pc.s0 = g0 * G;
+            pc.s1 = std::min(S, (g0 + per) * G);
+            pc.bus_first = item;
+            while (item < (int)items.size() && recs[items[item].first].stage < pc.s1) ++item;
+            pc.bus_count = item - pc.bus_first;
+            pc.aux_first = aux_first_of_stage[pc.s0];
+            pc.aux_count = aux_first_of_stage[pc.s1] - pc.aux_first;
+            b->pipe.push_back(pc);
+        }
+        for (auto& ps : b->pipe_streams)
+            if (!ps) cuda_check(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking), "stream");
     }
     const int n_cp = (int)((n_coupling + CP_CHUNK - 1) / CP_CHUNK);
     for (int c = 0; c < n_cp; ++c) aux.push_back(DAuxItem{1, 0, c, 0});
@@ -471,13 +500,13 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
             cuda_check(cudaStreamWaitEvent(b->aux_stream, b->ev_fork, 0), "stream wait");
         }
         if (aux) {
-            acopf_aux_kernel<<<P.n_aux_items, BLOCK, b->aux_smem, fork ? b->aux_stream : st>>>(P);
+            acopf_aux_kernel<<<P.n_aux_items, BLOCK, b->aux_smem, fork ? b->aux_stream : st>>>(P, 0);
             cuda_check(cudaGetLastError(), "acopf_aux_kernel launch");
             b->launches++;
         }
         if (bus) {
-            if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P);
-            else acopf_bus_kernel<0u><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P);
+            if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P, 0);
+            else acopf_bus_kernel<0u><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P, 0);
             cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
             b->launches++;
         }
@@ -513,6 +542,58 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
         double* dh = ensure(b->h_h, nh);
         if (!b->uploaded) upload(b);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
+        if (b->pipe.size() > 1 && x && nx) {
+            // chunk c: H2D of its inputs, its kernels, D2H of its outputs, on stream c % 3;
+            // copies of one chunk overlap the kernels and copies of the others
+            const EvalParams base = b->params;
+            EvalParams P = base;
+            P.x = dx; P.mult = mult ? dm : nullptr; P.obj_factor = obj_factor; P.what = what;
+            P.obj = dobj; P.grad = dg; P.cons = dc; P.jval = dj; P.hval = dh;
+            cudaEvent_t start;
+            cuda_check(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
+            cuda_check(cudaEventRecord(start, st), "event record");
+            const int S = (int)b->stages.size();
+            auto lo = [&](int s, int k, int64_t total) -> int64_t { return s >= S ? total : b->off6[6 * s + k]; };
+            auto m_lo = [&](int s) -> int64_t { return s >= S ? nm : b->off6[6 * s + 1]; };
+            for (size_t c = 0; c < b->pipe.size(); ++c) {
+                const auto& pc = b->pipe[c];
+                cudaStream_t cs = b->pipe_streams[c % 3];
+                cuda_check(cudaStreamWaitEvent(cs, start, 0), "stream wait");
+                const int64_t x0 = lo(pc.s0, 0, nx), x1 = lo(pc.s1, 0, nx);
+                const int64_t m0 = m_lo(pc.s0), m1 = m_lo(pc.s1);
+                const int64_t j0 = lo(pc.s0, 3, nj), j1 = lo(pc.s1, 3, nj);
+                const int64_t h0 = lo(pc.s0, 5, nh), h1 = lo(pc.s1, 5, nh);
+                cuda_check(cudaMemcpyAsync(dx + x0, x + x0, 8 * (x1 - x0), cudaMemcpyHostToDevice, cs), "H2D x");
+                if (mult && nm) cuda_check(cudaMemcpyAsync(dm + m0, mult + m0, 8 * (m1 - m0), cudaMemcpyHostToDevice, cs), "H2D mult");
+                if (pc.aux_count) {
+                    acopf_aux_kernel<<<pc.aux_count, BLOCK, b->aux_smem, cs>>>(P, pc.aux_first);
+                    cuda_check(cudaGetLastError(), "acopf_aux_kernel launch");
+                    b->launches++;
+                }
+                if (pc.bus_count && (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD))) {
+                    if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<pc.bus_count, BUS_BLOCK, b->smem, cs>>>(P, pc.bus_first);
+                    else acopf_bus_kernel<0u><<<pc.bus_count, BUS_BLOCK, b->smem, cs>>>(P, pc.bus_first);
+                    cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
+                    b->launches++;
+                }
+                if ((what & ACOPF_OBJ) && obj) cuda_check(cudaMemcpyAsync(obj + pc.s0, dobj + pc.s0, 8 * (pc.s1 - pc.s0), cudaMemcpyDeviceToHost, cs), "D2H obj");
+                if ((what & ACOPF_GRAD) && grad) cuda_check(cudaMemcpyAsync(grad + x0, dg + x0, 8 * (x1 - x0), cudaMemcpyDeviceToHost, cs), "D2H grad");
+                if ((what & ACOPF_CONS) && cons) cuda_check(cudaMemcpyAsync(cons + m0, dc + m0, 8 * (m1 - m0), cudaMemcpyDeviceToHost, cs), "D2H cons");
+                if ((what & ACOPF_JAC) && jval) cuda_check(cudaMemcpyAsync(jval + j0, dj + j0, 8 * (j1 - j0), cudaMemcpyDeviceToHost, cs), "D2H jac");
+                if ((what & ACOPF_HESS) && hval) cuda_check(cudaMemcpyAsync(hval + h0, dh + h0, 8 * (h1 - h0), cudaMemcpyDeviceToHost, cs), "D2H hess");
+            }
+            // join the pipeline back into the caller's stream, then wait
+            for (int k = 0; k < 3 && k < (int)b->pipe.size(); ++k) {
+                cudaEvent_t done;
+                cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
+                cuda_check(cudaEventRecord(done, b->pipe_streams[k]), "event record");
+                cuda_check(cudaStreamWaitEvent(st, done, 0), "stream wait");
+                cudaEventDestroy(done);
+            }
+            cudaEventDestroy(start);
+            cuda_check(cudaStreamSynchronize(st), "stream sync");
+            return;
+        }
         if (x && nx) cuda_check(cudaMemcpyAsync(dx, x, 8 * nx, cudaMemcpyHostToDevice, st), "H2D x");
         if (mult && nm) cuda_check(cudaMemcpyAsync(dm, mult, 8 * nm, cudaMemcpyHostToDevice, st), "H2D mult");
         if (acopf_batch_eval(b, dx, obj_factor, mult ? dm : nullptr, what, dobj, dg, dc, dj, dh, st) != 0)

@@ -310,10 +310,10 @@ __host__ __device__ __forceinline__ size_t bus_smem_layout(int table_bytes, int 
 }
 
 template <unsigned WHAT>
-__global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(const EvalParams P) {
+__global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(const EvalParams P, int item0) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
-    const DBusItem it = P.bus_items[blockIdx.x];
+    const DBusItem it = P.bus_items[item0 + blockIdx.x];
     const unsigned char* src = P.blob + it.blob_off;
     // ---- 0. bulk copy of the tile table into shared memory ----------------
     if (threadIdx.x == 0) {
@@ -569,9 +569,9 @@ __device__ void coupling_chunk(const EvalParams& P, int chunk) {
     }
 }
 
-__global__ void __launch_bounds__(BLOCK) acopf_aux_kernel(const EvalParams P) {
+__global__ void __launch_bounds__(BLOCK) acopf_aux_kernel(const EvalParams P, int item0) {
     extern __shared__ __align__(16) double leaves[];
-    const DAuxItem it = P.aux_items[blockIdx.x];
+    const DAuxItem it = P.aux_items[item0 + blockIdx.x];
     if (it.kind == 0) gen_chunk(P, it.stage, it.chunk, leaves);
     else coupling_chunk(P, it.chunk);
 }
