@@ -284,3 +284,68 @@ def test_sharded_path_single_rank_nccl():
             assert C.bit_diffs(out[k].cpu().numpy()[:len(ref[k])], ref[k]) == 0, k
     finally:
         dist.destroy_process_group()
+
+
+def _check_composite_samples(p, imap, stages, seed):
+    """Sampled stage blocks vs the oracle (gate) and vs standalone GPU stages (bitwise)."""
+    kinds = syn.variable_kinds([(len(l.va), len(l.pg)) for l in imap.layouts])
+    x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, seed)
+    ev = p.evaluator
+    out = ev.eval_host(x, mult, 1.0, L.ALL)
+    # composite objective = ((0 + w_0 f_0) + w_1 f_1) + ... over all stages (composer.py:256-258)
+    terms_ev = pkg.BatchEvaluator(ev.plans, layout="composite", coupling=None, obj_terms=True)
+    t = terms_ev.eval_host(x, None, 1.0, L.OBJ)["obj"]
+    acc = 0.0
+    for v in t:
+        acc = acc + float(v)
+    assert acc == float(out["obj"][0])
+    ip, ix = ev.pattern("J")
+    hp, hx = ev.pattern("H")
+    misses = 0
+    for k in stages:
+        case = imap.stages[k].case
+        o = StageOracle(case)
+        lay = imap.layouts[k]
+        a, b = imap.var_offset[k], imap.var_offset[k] + lay.n_vars
+        e0, i0 = imap.eq_offset[k], p.m_eq + imap.ineq_offset[k]
+        mk = np.concatenate([mult[e0:e0 + lay.n_eq], mult[i0:i0 + lay.n_ineq]])
+        xs = x[a:b]
+        # constraints of the stage block
+        cs = np.concatenate([out["cons"][e0:e0 + lay.n_eq], out["cons"][i0:i0 + lay.n_ineq]])
+        misses += C.gate_misses(cs, o.constraints(xs))
+        # J rows of the stage (eq then ineq), H rows of the stage
+        rows = np.r_[e0:e0 + lay.n_eq, i0:i0 + lay.n_ineq]
+        Jd = np.concatenate([out["jac"][ip[r]:ip[r + 1]] for r in rows])
+        Hd = out["hess"][hp[a]:hp[b]]
+        Jo = o.jacobian(xs)
+        Ho = o.lagrangian_hessian(xs, 1.0 * imap.weights[k], mk)
+        assert len(Jd) == Jo.nnz and len(Hd) == Ho.nnz
+        misses += C.gate_misses(Jd, Jo.data) + C.gate_misses(Hd, Ho.data)
+        g = out["grad"][a:b]
+        misses += C.gate_misses(g, imap.weights[k] * o.gradient(xs))
+    # coupling rows read child - base
+    for r in list(imap.coupling_rows)[:50]:
+        child = imap.var_offset[r.stage_a] + imap.layouts[r.stage_a].pg[r.gen]
+        base_ = imap.var_offset[r.stage_b] + imap.layouts[r.stage_b].pg[r.gen]
+        assert out["cons"][r.row] == x[child] - x[base_]
+    return misses
+
+
+@pytest.mark.slow
+def test_config2_full_composite_samples():
+    """BASELINE config 2 at full size (1,025 stages): sampled stages vs the oracle."""
+    base, ctgs = syn.config2_inputs()
+    p, imap = pkg.compose_scopf(base, ctgs, CouplingMode())
+    misses = _check_composite_samples(p, imap, [0, 1, 513, 1024], 31)
+    _record("oracle:cfg2-full-samples", gate_misses=misses)
+    assert misses == 0
+
+
+@pytest.mark.slow
+def test_config4_full_composite_samples():
+    """BASELINE config 4 at full size (1,024 stages, 25k buses): sampled stages vs the oracle."""
+    base, scens, ctgs = syn.config4_inputs()
+    p, imap = pkg.compose_general(scens, ctgs, [base], CouplingMode(), 30.0)
+    misses = _check_composite_samples(p, imap, [0, 1, 32, 33, 1023], 41)
+    _record("oracle:cfg4-full-samples", gate_misses=misses)
+    assert misses == 0
