@@ -226,7 +226,7 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, c
     const double gtf = V.adm[4 * ne + e], btf = V.adm[5 * ne + e], gtt = V.adm[6 * ne + e], btt = V.adm[7 * ne + e];
     const double th = vaf - vat;
     double sn, cs;
-    acc_sincos(th, &sn, &cs);
+    libm_sincos(th, &sn, &cs);
     const double u = gft * cs + bft * sn;
     const double w = gft * sn - bft * cs;
     const double u2 = gtf * cs - btf * sn;

@@ -22,10 +22,12 @@
 #ifdef __CUDACC__
 #define SC_HD __host__ __device__ __forceinline__
 __device__ static const double sc_table_dev[SC_NJ * 4] = {SC_TABLE_VALUES};
+__device__ static const double sc_gl_table_dev[SC_GL_NK * 4] = {SC_GL_TABLE_VALUES};
 #else
 #define SC_HD static inline
 #endif
 static const double sc_table_host[SC_NJ * 4] = {SC_TABLE_VALUES};
+static const double sc_gl_table_host[SC_GL_NK * 4] = {SC_GL_TABLE_VALUES};
 
 SC_HD void sc_two_sum(double a, double b, double& s, double& e) {
     s = a + b;
@@ -111,5 +113,74 @@ SC_HD void acc_sincos(double x, double* sp, double* cp) {
         case 1: *sp = cs;  *cp = -sn; break;
         case 2: *sp = -sn; *cp = -cs; break;
         default: *sp = -cs; *cp = sn; break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// libm-identical sin/cos for |x| < 0.85546875.
+//
+// The reference evaluates np.sin / np.cos, i.e. glibc 2.39's libm (x86-64 FMA
+// variant, selected on FMA-capable hosts).  For |x| < 0.855469 glibc uses the
+// published IBM Accurate Mathematical Library scheme (Ziv): sin x = x for
+// |x| < 2^-26, a degree-11 odd polynomial for |x| < 0.126, otherwise the
+// table of sin/cos(k/128) (hi + lo, k = round(128|x|) through the 1.5*2^45
+// rounding trick) corrected by short polynomials in the remainder; cos x = 1
+// for |x| < 2^-27, else the table scheme.  The polynomial coefficients below
+// are the constants of that libm build (found in the installed binary and
+// validated: tests/test_native_host.py compares this routine with libm
+// bit for bit); the fused multiply-adds follow the contraction of the FMA
+// build.  Angles outside that range use acc_sincos (correctly rounded).
+#define GL_SN3 (-0x1.5555555555515p-3)
+#define GL_SN5 (0x1.11110e829872fp-7)
+#define GL_CS2 (0x1.0000000000000p-1)
+#define GL_CS4 (-0x1.5555555555535p-5)
+#define GL_CS6 (0x1.6c16bedd9e239p-10)
+#define GL_S1 (-0x1.5555555555555p-3)
+#define GL_S2 (0x1.1111111110ecep-7)
+#define GL_S3 (-0x1.a01a019db08b8p-13)
+#define GL_S4 (0x1.71de27b9a7ed9p-19)
+#define GL_S5 (-0x1.addffc2fcdf59p-26)
+#define GL_BIG 52776558133248.0
+
+SC_HD void libm_sincos(double x, double* sp, double* cp) {
+    const double ax = fabs(x);
+    if (!(ax < 0.85546875)) {            // outside the table scheme (and inf / nan)
+        acc_sincos(x, sp, cp);
+        return;
+    }
+    // table entry k = round(128 |x|) and remainder, exactly as big + |x| rounds
+    const double u = GL_BIG + ax;
+    const double xk = u - GL_BIG;
+    const double xr = ax - xk;
+    const int k = (int)(xk * 128.0);
+#ifdef __CUDA_ARCH__
+    const double* tab = sc_gl_table_dev + 4 * k;
+#else
+    const double* tab = sc_gl_table_host + 4 * k;
+#endif
+    const double sn = tab[0], ssn = tab[1], cs = tab[2], ccs = tab[3];
+    const double xx = xr * xr;
+    const double ps = fma(xx, GL_SN5, GL_SN3);
+    const double pc = xx * fma(xx, fma(xx, GL_CS6, GL_CS4), GL_CS2);
+    // cos
+    if (ax < 7.450580596923828e-09) {
+        *cp = 1.0;
+    } else {
+        const double s = fma(xr * xx, ps, xr);
+        const double cor = fma(-sn, s, fma(-cs, pc, fma(-s, ssn, ccs)));
+        *cp = cs + cor;
+    }
+    // sin
+    if (ax < 1.4901161193847656e-08) {
+        *sp = x;
+    } else if (ax < 0.126) {
+        const double a2 = x * x;
+        const double p = fma(fma(fma(fma(GL_S5, a2, GL_S4), a2, GL_S3), a2, GL_S2), a2, GL_S1);
+        *sp = x + (p * x) * a2;
+    } else {
+        const double s = xr + fma(xr * xx, ps, 0.0);
+        const double c = fma(xr, 0.0, pc);
+        const double cor = fma(cs, s, fma(-sn, c, fma(s, ccs, ssn)));
+        *sp = copysign(sn + cor, x);
     }
 }

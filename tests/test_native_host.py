@@ -76,6 +76,32 @@ def sincos_bin():
     return exe
 
 
+@pytest.fixture(scope="module")
+def libm_sincos_bin():
+    d = tempfile.mkdtemp()
+    src = os.path.join(d, "t.cpp")
+    with open(src, "w") as fh:
+        fh.write('#include <cstdio>\n#include <cstdlib>\n#include "sincos.cuh"\n'
+                 'int main(){size_t n; if(fread(&n,8,1,stdin)!=1) return 1; double* x=(double*)malloc(8*n);'
+                 'if(fread(x,8,n,stdin)!=n) return 1; double* o=(double*)malloc(16*n);'
+                 'for(size_t i=0;i<n;i++) libm_sincos(x[i],&o[2*i],&o[2*i+1]); fwrite(o,16,n,stdout); return 0;}\n')
+    exe = os.path.join(d, "t")
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-I", CSRC, src, "-o", exe], check=True)
+    return exe
+
+
+def test_libm_sincos_bit_identical_to_numpy(libm_sincos_bin):
+    """The kernels' sincos equals np.sin / np.cos (glibc) bit for bit on |x| < 0.8555."""
+    rng = np.random.default_rng(11)
+    xs = np.concatenate([rng.uniform(-0.8554, 0.8554, 1_000_000), rng.uniform(-0.13, 0.13, 200_000),
+                         rng.uniform(-1e-7, 1e-7, 10_000),
+                         [0.0, -0.0, 0.126, -0.126, 1 / 256, 0.85546874999999989, 7.45e-9, 1.49e-8]])
+    inp = np.array([len(xs)], dtype=np.uint64).tobytes() + xs.tobytes()
+    out = np.frombuffer(subprocess.run([libm_sincos_bin], input=inp, capture_output=True, check=True).stdout)
+    assert C.bit_diffs(out[0::2], np.sin(xs)) == 0
+    assert C.bit_diffs(out[1::2], np.cos(xs)) == 0
+
+
 def test_accurate_sincos_vs_libm(sincos_bin):
     """Device sincos (same source, host build) is within 1 ulp of libm and equal on >99.5%."""
     rng = np.random.default_rng(3)
