@@ -393,8 +393,15 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
         if (need_j || need_h || need_c)
             for (int e = threadIdx.x; e < H->nE; e += blockDim.x)
                 branch_end(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c);
-        // ---- A2: bus-level terms -----------------------------------------------
-        for (int bl = threadIdx.x; bl < nbt; bl += blockDim.x) {
+        // ---- A2: bus-level terms ---------------------------------------------------
+        // bus bl belongs to thread blockDim-1-bl (the threads without a branch end
+        // when the tile has fewer ends than threads); it also keeps the bus's
+        // staged inputs in registers for its balance rows, so the staging buffers
+        // can be refilled right after the next barrier
+        const int blc = (int)blockDim.x - 1 - (int)threadIdx.x;
+        double vm_c = 0.0, pd_c = 0.0, qd_c = 0.0;
+        if (blc < nbt) {
+            const int bl = blc;
             const int i = H->b0 + bl;
             const double vmi = Gb[bl], gsi = V.gs[bl], bsi = V.bs[bl];
             double* qb = Q + qbus + BQ * bl;
@@ -405,24 +412,20 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
                 P.grad[R.var_off + i] = R.w * 0.0;
                 P.grad[R.var_off + R.nb + i] = R.w * 0.0;
             }
+            if (need_c) { vm_c = vmi; pd_c = Gb[3 * nbt + bl]; qd_c = Gb[4 * nbt + bl]; }
         }
         __syncthreads();
         // the staging buffers are free again: gather the next stage's inputs
         // while this stage's balance rows and scatter sums are stored
-        double vm_c = 0.0, pd_c = 0.0, qd_c = 0.0;
-        const int blc = threadIdx.x;
-        if (need_c && blc < nbt) { vm_c = Gb[blc]; pd_c = Gb[3 * nbt + blc]; qd_c = Gb[4 * nbt + blc]; }
-        if (ri + 1 < it.count) {
-            __syncthreads();
-            issue_gathers(P, recs[ri + 1], V, Gv, Gb, RS, FO, need_h, need_c);
-        }
+        if (ri + 1 < it.count) issue_gathers(P, recs[ri + 1], V, Gv, Gb, RS, FO, need_h, need_c);
         // ---- B: balance rows, then the scatter-map sums -------------------------
         if (need_c) {
             const double* pgv = P.x + R.var_off + 2 * R.nb;
             const double* qgv = pgv + R.ng;
-            for (int bl = threadIdx.x; bl < nbt; bl += blockDim.x) {
+            if (blc < nbt) {
+                const int bl = blc;
                 const int i = H->b0 + bl;
-                const double vmi = bl == blc ? vm_c : 0.0;
+                const double vmi = vm_c;
                 double p = 0.0, r = 0.0;
                 for (int e = V.busptr[bl]; e < V.busptr[bl + 1]; ++e) {
                     p = p + Q[EQ * e + Q_FP];

@@ -57,6 +57,9 @@ constexpr int POS_OF_SLOT_T[7] = {1, 3, 4, 5, 6, 8, 9};
 #ifndef ACOPF_TILE_BUSES
 #define ACOPF_TILE_BUSES 96
 #endif
+#if ACOPF_TILE_BUSES > 256
+#error "one bus per thread: ACOPF_TILE_BUSES must not exceed the bus kernel block"
+#endif
 constexpr int TILE_MAX_ENDS = ACOPF_TILE_ENDS;    // soft cap; a single high-degree bus may exceed it
 constexpr int TILE_MAX_BUSES = ACOPF_TILE_BUSES;  // <= bus kernel block size (one bus per thread)
 constexpr int SMEM_LIMIT_BYTES = 220 * 1024;
