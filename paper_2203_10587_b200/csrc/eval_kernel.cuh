@@ -130,6 +130,7 @@ struct TileView {
     const int* ridx;
     const int* foff;
     const int* busptr;
+    const int* bend;
     const int* gptr;
     const int* glist;
     const double* gs;
@@ -214,11 +215,12 @@ __device__ __forceinline__ void issue_gathers(const EvalParams& P, const SRec& R
 }
 
 // Phase A for one branch end of one stage (inputs already gathered in shared memory).
+template <int SIDE>
 __device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, const TileView& V, const double* Gv,
                                            int rs, long long foff, int e, double* Q, bool need_j, bool need_h,
                                            bool need_c) {
     const int ne = V.h->nE;
-    const int side = V.code[e] & 1;
+    constexpr int side = SIDE;         // ends are stored from-ends first: warp-uniform
     const int f = V.f[e], t = V.t[e];
     const int r = V.ridx[e];
     const double vaf = Gv[e], vat = Gv[ne + e], vf = Gv[2 * ne + e], vt = Gv[3 * ne + e];
@@ -282,7 +284,7 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, c
         const double hqf[10] = {-vvw, vvw, vtu, vfu, -vvw, -vtu, -vfu, -(2.0 * bff), w, z};
         const double hpt[10] = {-vvu2, vvu2, vtw2, vfw2, -vvu2, -vtw2, -vfw2, z, u2, 2.0 * gtt};
         const double hqt[10] = {-vvw2, vvw2, -vtu2, -vfu2, -vvw2, vtu2, vfu2, z, w2, -(2.0 * btt)};
-        if (side == 0) {
+        if constexpr (SIDE == 0) {
 #pragma unroll
             for (int s = 0; s < 7; ++s)
                 q[Q_H + s] = hpos(slot_pos_f(s), cpf, cqf, cpt, cqt, s2f, s2t, gpf, gqf, gpt, gqt, hpf, hqf, hpt, hqt);
@@ -371,6 +373,7 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
     V.ridx = reinterpret_cast<const int*>(smem + H->o_ridx);
     V.foff = reinterpret_cast<const int*>(smem + H->o_foff);
     V.busptr = reinterpret_cast<const int*>(smem + H->o_busptr);
+    V.bend = reinterpret_cast<const int*>(smem + H->o_bend);
     V.gptr = reinterpret_cast<const int*>(smem + H->o_gptr);
     V.glist = reinterpret_cast<const int*>(smem + H->o_glist);
     V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
@@ -391,8 +394,10 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
         __syncthreads();
         // ---- A: branch ends ------------------------------------------------
         if (need_j || need_h || need_c)
-            for (int e = threadIdx.x; e < H->nE; e += blockDim.x)
-                branch_end(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c);
+            for (int e = threadIdx.x; e < H->nE; e += blockDim.x) {
+                if (e < H->nF) branch_end<0>(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c);
+                else branch_end<1>(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c);
+            }
         // ---- A2: bus-level terms ---------------------------------------------------
         // bus bl belongs to thread blockDim-1-bl (the threads without a branch end
         // when the tile has fewer ends than threads); it also keeps the bus's
@@ -427,7 +432,8 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
                 const int i = H->b0 + bl;
                 const double vmi = vm_c;
                 double p = 0.0, r = 0.0;
-                for (int e = V.busptr[bl]; e < V.busptr[bl + 1]; ++e) {
+                for (int j = V.busptr[bl]; j < V.busptr[bl + 1]; ++j) {
+                    const int e = V.bend[j];       // from-ends by branch, then to-ends (np.add.at order)
                     p = p + Q[EQ * e + Q_FP];
                     r = r + Q[EQ * e + Q_FQ];
                 }

@@ -251,13 +251,14 @@ struct TileHdr {            // 192 bytes; offsets in bytes from the header start
     int32_t b0, nB, nE, nQ;           // first bus, buses, ends, shared doubles for quantities
     int32_t LP, LQ, LHA, LHV;         // entries of the four row segments
     int32_t ngl, bytes, nSJ, nSH;     // generator ids, serialised size, single-term J / H entries
-    int32_t nMJ, nMH, nMT, pad0;      // multi-term J / H entries, their term count
+    int32_t nMJ, nMH, nMT, nF;        // multi-term J / H entries, their term count, from-ends
     int32_t o_code, o_f, o_t, o_ridx;
     int32_t o_foff, o_busptr, o_gptr, o_glist;
     int32_t o_gs, o_bs, o_adm, o_sj_dst;
     int32_t o_sj_term, o_sh_dst, o_sh_term, o_mj_dst;
     int32_t o_mj_info, o_mh_dst, o_mh_info, o_mterms;
-    int32_t pad[12];
+    int32_t o_bend;
+    int32_t pad[11];
 };
 static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
 
@@ -272,8 +273,10 @@ static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
 struct TileTable {
     int topo = 0;
     int b0 = 0, nB = 0;
-    std::vector<int> ends;        // k*2+side, per bus: from-ends then to-ends
-    std::vector<int> busptr;      // nB+1
+    std::vector<int> ends;        // k*2+side: all from-ends (bus order), then all to-ends
+    int nF = 0;                   // from-ends
+    std::vector<int> busptr;      // nB+1, into bend
+    std::vector<int> bend;        // per bus: its from-ends then to-ends (end indices)
     int L[4] = {0, 0, 0, 0};      // entries in P, Q, VA, VM segments
     std::vector<int> cols;        // stage-local column per entry (pattern export)
     std::vector<int> rowlen;      // entries per row, 4 segments x nB rows
@@ -314,6 +317,7 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     h.nSJ = (int)sdst[0].size(); h.nSH = (int)sdst[1].size();
     h.nMJ = (int)mdst[0].size(); h.nMH = (int)mdst[1].size();
     h.nMT = (int)mterms.size();
+    h.nF = nF;
     size_t off = sizeof(TileHdr);
     auto take = [&](size_t n) { int o = (int)off; off = align16(off + n); return o; };
     h.o_code = take(4 * (size_t)nE);
@@ -322,6 +326,7 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     h.o_ridx = take(4 * (size_t)nE);
     h.o_foff = take(4 * (size_t)nE);
     h.o_busptr = take(4 * busptr.size());
+    h.o_bend = take(4 * bend.size());
     h.o_gptr = take(4 * gptr.size());
     h.o_glist = take(4 * glist.size());
     h.o_gs = take(8 * (size_t)nB);
@@ -348,6 +353,7 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     put(h.o_ridx, ridx.data(), 4 * (size_t)nE);
     put(h.o_foff, foff.data(), 4 * (size_t)nE);
     put(h.o_busptr, busptr.data(), 4 * busptr.size());
+    put(h.o_bend, bend.data(), 4 * bend.size());
     put(h.o_gptr, gptr.data(), 4 * gptr.size());
     put(h.o_glist, glist.data(), 4 * glist.size());
     put(h.o_gs, gs.data(), 8 * (size_t)nB);
@@ -371,21 +377,27 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     tt.nB = b1 - b0;
     std::vector<Row> rows(4 * tt.nB);
     std::unordered_map<int, int> end_pos;
+    // ends: all from-ends of the tile first (so a warp sees one side), then all to-ends
+    for (int i = b0; i < b1; ++i)
+        for (int p = T.from_ptr[i]; p < T.from_ptr[i + 1]; ++p)
+            if (live(T.from_list[p])) {
+                end_pos[2 * T.from_list[p]] = (int)tt.ends.size();
+                tt.ends.push_back(2 * T.from_list[p]);
+            }
+    tt.nF = (int)tt.ends.size();
+    for (int i = b0; i < b1; ++i)
+        for (int p = T.to_ptr[i]; p < T.to_ptr[i + 1]; ++p)
+            if (live(T.to_list[p])) {
+                end_pos[2 * T.to_list[p] + 1] = (int)tt.ends.size();
+                tt.ends.push_back(2 * T.to_list[p] + 1);
+            }
     tt.busptr.push_back(0);
     for (int i = b0; i < b1; ++i) {
-        for (int p = T.from_ptr[i]; p < T.from_ptr[i + 1]; ++p) {
-            int k = T.from_list[p];
-            if (!live(k)) continue;
-            end_pos[2 * k] = (int)tt.ends.size();
-            tt.ends.push_back(2 * k);
-        }
-        for (int p = T.to_ptr[i]; p < T.to_ptr[i + 1]; ++p) {
-            int k = T.to_list[p];
-            if (!live(k)) continue;
-            end_pos[2 * k + 1] = (int)tt.ends.size();
-            tt.ends.push_back(2 * k + 1);
-        }
-        tt.busptr.push_back((int)tt.ends.size());
+        for (int p = T.from_ptr[i]; p < T.from_ptr[i + 1]; ++p)
+            if (live(T.from_list[p])) tt.bend.push_back(end_pos.at(2 * T.from_list[p]));
+        for (int p = T.to_ptr[i]; p < T.to_ptr[i + 1]; ++p)
+            if (live(T.to_list[p])) tt.bend.push_back(end_pos.at(2 * T.to_list[p] + 1));
+        tt.busptr.push_back((int)tt.bend.size());
         Row r4[4];
         build_bus_rows(T, i, live, r4);
         for (int s = 0; s < 4; ++s) rows[s * tt.nB + (i - b0)] = std::move(r4[s]);
