@@ -15,6 +15,9 @@
  *                          of every stage at once, device buffers     (acopf.py:266-373,
  *                                                                     composer.py:256-311)
  *   acopf_batch_eval_host  same with host buffers (H2D + eval + D2H on the handle's stream)
+ *   acopf_batch_flows      per-branch flows and per-bus network injections of every stage
+ *                          (pu) -- the device half of extract_solution / residuals_at /
+ *                          solution_from_case                        (acopf.py:448-546, 230-264)
  *   acopf_batch_pattern    CSR indptr/indices of J or H (stage or composite) -- the fixed
  *                          pattern scipy would produce (acopf.py:308-311, 370-373)
  *   acopf_last_error       error text (Python raises DeviceError / Disconnected ...)
@@ -103,6 +106,18 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
                           const double* mult, int64_t nm, uint32_t what, double* obj, int64_t nobj,
                           double* grad, int64_t ngrad, double* cons, int64_t ncons, double* jval,
                           int64_t nj, double* hval, int64_t nh, void* stream);
+
+/* Branch flows and network injections of every stage at x (device pointers),
+ * per-unit, exactly as Engine.first_order / Engine.injections compute them
+ * (acopf.py:230-264).  Stage s (in batch order) owns
+ *   flows[F_s + 0*nbr + k], [F_s + 1*nbr + k], [F_s + 2*nbr + k], [F_s + 3*nbr + k]
+ *       = pf, qf, pt, qt of topology branch k (nbr = the stage topology's branches;
+ *         F_s = sum over earlier stages of 4*nbr); branches a contingency removes
+ *         are not written (the caller zero-fills);
+ *   inj[I_s + i], inj[I_s + nb + i] = p, q of bus i, shunts included
+ *       (I_s = sum over earlier stages of 2*nb).
+ * Needs set_layout (x is read at each stage's var_off). */
+int acopf_batch_flows(acopf_batch* b, const double* x, double* flows, double* inj, void* stream);
 
 /* CSR pattern of one stage (stage >= 0; rows: that stage's constraints or
  * variables; columns stage-local) or of the whole laid-out batch (stage = -1,

@@ -45,6 +45,7 @@ _SIGNATURES = {
     "acopf_batch_eval_host": (c_int32, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_int64, c_uint32,
                                         c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
                                         c_int64, c_void_p, c_int64, c_void_p]),
+    "acopf_batch_flows": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "acopf_batch_pattern": (c_int32, [c_void_p, c_int32, c_int32, c_int64, _i64p, _i32p]),
     "acopf_batch_launches": (c_int64, [c_void_p]),
     "acopf_canonical_order": (c_int32, [c_int64, _i32p, _i32p]),

@@ -160,6 +160,7 @@ static void upload(acopf_batch* b) {
     // stages and removed lists
     std::vector<DStage> ds(S);
     std::vector<int> rem, remsz;
+    long long fl_off = 0, inj_off = 0;
     for (int s = 0; s < S; ++s) {
         const StageInfo& st = b->stages[s];
         DStage& d = ds[s];
@@ -176,6 +177,9 @@ static void upload(acopf_batch* b) {
         d.topo = st.topo;
         d.obj_slot = b->obj_slot[s];
         d.w = st.w;
+        d.fl_off = fl_off; d.inj_off = inj_off;
+        fl_off += 4LL * b->topos[st.topo]->nbr;
+        inj_off += 2LL * b->topos[st.topo]->nb;
     }
     // bus work: for every tile, the stages sharing one table, in chunks of G
     int64_t total_recs = 0;
@@ -513,6 +517,25 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         if (fork) {
             cuda_check(cudaEventRecord(b->ev_join, b->aux_stream), "event record");
             cuda_check(cudaStreamWaitEvent(st, b->ev_join, 0), "stream wait");
+        }
+    });
+}
+
+int acopf_batch_flows(acopf_batch* b, const double* x, double* flows, double* inj, void* stream) {
+    return guard([&] {
+        if (!b->laid_out) throw std::runtime_error("acopf_batch_set_layout was not called");
+        if (!b->uploaded) upload(b);
+        if (!x || !flows || !inj) throw std::runtime_error("x/flows/inj is NULL");
+        cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
+        EvalParams P = b->params;
+        P.x = x; P.mult = nullptr; P.obj_factor = 0.0; P.what = W_FLOWS;
+        P.obj = P.grad = P.cons = P.jval = P.hval = nullptr;
+        P.flows = flows; P.inj = inj;
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
+        if (P.n_bus_items > 0) {
+            acopf_bus_kernel<0u><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P, 0);
+            cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
+            b->launches++;
         }
     });
 }

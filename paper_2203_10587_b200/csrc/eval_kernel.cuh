@@ -29,7 +29,7 @@
 
 namespace acopf {
 
-enum : unsigned { W_OBJ = 1u, W_GRAD = 2u, W_CONS = 4u, W_JAC = 8u, W_HESS = 16u };
+enum : unsigned { W_OBJ = 1u, W_GRAD = 2u, W_CONS = 4u, W_JAC = 8u, W_HESS = 16u, W_FLOWS = 32u };
 
 struct DTopo {
     int nb, nbr, ng, nr;
@@ -43,6 +43,7 @@ struct DStage {
     long long hpg_local, pd_off, cost_off, rem_off;
     int nrem, topo, obj_slot, pad;
     double w;
+    long long fl_off, inj_off;    // flows (4 x nbr) and injections (2 x nb) of W_FLOWS
 };
 
 struct DBusItem {             // one CTA of the bus kernel
@@ -92,6 +93,8 @@ struct EvalParams {
     double* jval;
     double* hval;
     double* obj_terms;        // per objective stage: w_s * f_s
+    double* flows;            // W_FLOWS: per stage pf, qf, pt, qt by topology branch (pu)
+    double* inj;              // W_FLOWS: per stage p, q network injections by bus (pu)
     unsigned* counter;
 };
 
@@ -156,7 +159,8 @@ struct SRec {
     long long var_off, eq_row, ineq_row, pd_off, rem_off;
     long long oP, oQ, oA, oV, jineq;   // absolute output offsets of the tile's segments
     double w;
-    int nrem, nb, ng, pad;
+    long long fl_off, inj_off;
+    int nrem, nb, ng, nbr;
 };
 
 constexpr int GV = 10;   // gathered doubles per end: va_f va_t vm_f vm_t mu(Pf Qf Pt Qt) s_f s_t
@@ -218,7 +222,7 @@ __device__ __forceinline__ void issue_gathers(const EvalParams& P, const SRec& R
 template <int SIDE>
 __device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, const TileView& V, const double* Gv,
                                            int rs, long long foff, int e, double* Q, bool need_j, bool need_h,
-                                           bool need_c) {
+                                           bool need_c, bool need_f) {
     const int ne = V.h->nE;
     constexpr int side = SIDE;         // ends are stored from-ends first: warp-uniform
     const int f = V.f[e], t = V.t[e];
@@ -241,6 +245,11 @@ __device__ __forceinline__ void branch_end(const EvalParams& P, const SRec& R, c
     double* q = Q + EQ * e;
     q[Q_FP] = side ? pt : pf;
     q[Q_FQ] = side ? qt : qf;
+    if (need_f) {          // acopf.py:448-465 (_branch_flows_mw, before the MVA scaling)
+        double* fl = P.flows + R.fl_off + 2 * side * (long long)R.nbr + (V.code[e] >> 1);
+        fl[0] = side ? pt : pf;
+        fl[R.nbr] = side ? qt : qf;
+    }
     if (r >= 0 && need_c) P.cons[R.ineq_row + 2 * rs + side] = side ? pt * pt + qt * qt : pf * pf + qf * qf;
     if (!(need_j || need_h)) return;
     double gpf[4], gqf[4], gpt[4], gqt[4];
@@ -362,7 +371,8 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
         o.jineq = S.jineq_base;
         o.nb = P.topos[S.topo].nb;
         o.ng = P.topos[S.topo].ng;
-        o.pad = 0;
+        o.nbr = P.topos[S.topo].nbr;
+        o.fl_off = S.fl_off; o.inj_off = S.inj_off;
         recs[i] = o;
     }
     TileView V;
@@ -381,7 +391,7 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
     V.adm = reinterpret_cast<const double*>(smem + H->o_adm);
     // WHAT != 0: the mask is a compile-time constant (the all-callbacks path)
     const unsigned what = WHAT ? WHAT : P.what;
-    const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS;
+    const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS, need_f = what & W_FLOWS;
     const int qbus = EQ * H->nE;
     const int nbt = H->nB;
     if (threadIdx.x == 0) Q[qbus + BQ * nbt] = 1.0;
@@ -393,10 +403,10 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         // ---- A: branch ends ------------------------------------------------
-        if (need_j || need_h || need_c)
+        if (need_j || need_h || need_c || need_f)
             for (int e = threadIdx.x; e < H->nE; e += blockDim.x) {
-                if (e < H->nF) branch_end<0>(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c);
-                else branch_end<1>(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c);
+                if (e < H->nF) branch_end<0>(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c, need_f);
+                else branch_end<1>(P, R, V, Gv, RS[e], FO[e], e, Q, need_j, need_h, need_c, need_f);
             }
         // ---- A2: bus-level terms ---------------------------------------------------
         // bus bl belongs to thread blockDim-1-bl (the threads without a branch end
@@ -417,14 +427,14 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
                 P.grad[R.var_off + i] = R.w * 0.0;
                 P.grad[R.var_off + R.nb + i] = R.w * 0.0;
             }
-            if (need_c) { vm_c = vmi; pd_c = Gb[3 * nbt + bl]; qd_c = Gb[4 * nbt + bl]; }
+            if (need_c || need_f) { vm_c = vmi; pd_c = Gb[3 * nbt + bl]; qd_c = Gb[4 * nbt + bl]; }
         }
         __syncthreads();
         // the staging buffers are free again: gather the next stage's inputs
         // while this stage's balance rows and scatter sums are stored
         if (ri + 1 < it.count) issue_gathers(P, recs[ri + 1], V, Gv, Gb, RS, FO, need_h, need_c);
         // ---- B: balance rows, then the scatter-map sums -------------------------
-        if (need_c) {
+        if (need_c || need_f) {
             const double* pgv = P.x + R.var_off + 2 * R.nb;
             const double* qgv = pgv + R.ng;
             if (blc < nbt) {
@@ -439,15 +449,21 @@ __global__ void __launch_bounds__(BUS_BLOCK, ACOPF_BUS_MINB) acopf_bus_kernel(co
                 }
                 p = p + (V.gs[bl] * vmi) * vmi;
                 r = r - (V.bs[bl] * vmi) * vmi;
-                double cp = -(pd_c + p);
-                double cq = -(qd_c + r);
-                for (int gi = V.gptr[bl]; gi < V.gptr[bl + 1]; ++gi) {
-                    const int g = V.glist[gi];
-                    cp = cp + __ldg(pgv + g);
-                    cq = cq + __ldg(qgv + g);
+                if (need_f) {      // Engine.injections (acopf.py:252-264)
+                    P.inj[R.inj_off + i] = p;
+                    P.inj[R.inj_off + R.nb + i] = r;
                 }
-                P.cons[R.eq_row + i] = cp;
-                P.cons[R.eq_row + R.nb + i] = cq;
+                if (need_c) {
+                    double cp = -(pd_c + p);
+                    double cq = -(qd_c + r);
+                    for (int gi = V.gptr[bl]; gi < V.gptr[bl + 1]; ++gi) {
+                        const int g = V.glist[gi];
+                        cp = cp + __ldg(pgv + g);
+                        cq = cq + __ldg(qgv + g);
+                    }
+                    P.cons[R.eq_row + i] = cp;
+                    P.cons[R.eq_row + R.nb + i] = cq;
+                }
             }
         }
         const unsigned short* mterms = reinterpret_cast<const unsigned short*>(smem + H->o_mterms);

@@ -163,5 +163,56 @@ def main():
         print(name, p.n, p.m_eq + p.m_ineq, len(imap.coupling_rows))
 
 
+SOLUTION_STAGES = ["stage_ring9", "stage_feat30", "stage_feat200"]
+SOLUTION_FIELDS = ("vm", "va", "pg", "qg", "pf", "qf", "pt", "qt")
+
+
+def _dump_solution(out, prefix, sol, ok):
+    for f in SOLUTION_FIELDS:
+        out[prefix + f] = getattr(sol, f)
+    out[prefix + "objective"] = np.array([sol.objective])
+    dp, dq = ok.residuals_at(sol.case, sol)
+    out[prefix + "dp"], out[prefix + "dq"] = dp, dq
+
+
+def solutions():
+    """solution_*.npz: extract_solution / solution_from_case / residuals_at (acopf.py:413-546)."""
+    import refbridge as rb
+    ok = rb.opfkit()
+    if ok is None:
+        raise SystemExit("reference not mounted at /root/reference")
+    for name in SOLUTION_STAGES:
+        spec = STAGE_SPECS[name]
+        case = stage_case(spec)
+        rc = rb.to_ref_case(case)
+        p, lay = ok.build_acopf(rc)
+        kinds = syn.variable_kinds([(len(lay.va), len(lay.pg))])
+        x, _ = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 3000)
+        out = dict(spec=json.dumps(spec), case_digest=case_digest(case), x=x)
+        sol = ok.extract_solution(rc, lay, x)
+        _dump_solution(out, "ex_", sol, ok)
+        out["packed"] = ok.pack_solution(rc, lay, sol)
+        _dump_solution(out, "fc_", ok.solution_from_case(rc), ok)
+        np.savez_compressed(os.path.join(HERE, "solution_" + name + ".npz"), **out)
+        print("solution", name)
+    conv_map = dict(case=rb.to_ref_case, ctgs=rb.to_ref_ctgs, scens=rb.to_ref_scens, mode=rb.to_ref_mode)
+    for name in ("scopf_corrective", "general"):
+        spec = COMPOSITE_SPECS[name]
+        a, bases = composite_inputs(spec)
+        p, imap = compose(ok, spec["kind"], a, conv=lambda k, v: conv_map[k](v))
+        kinds = variable_kinds_from_layouts(imap.layouts)
+        x, _ = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 3001)
+        out = dict(spec=json.dumps(spec), case_digest=case_digest(bases[0]), x=x,
+                   n_stages=np.array([len(imap.stages)]))
+        for k, st in enumerate(imap.stages):
+            o, lay = imap.var_offset[k], imap.layouts[k]
+            _dump_solution(out, f"s{k}_", ok.extract_solution(st.case, lay, x[o:o + lay.n_vars]), ok)
+        np.savez_compressed(os.path.join(HERE, "solution_" + name + ".npz"), **out)
+        print("solution", name, len(imap.stages))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["solutions"]:
+        solutions()
+    else:
+        main()

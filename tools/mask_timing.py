@@ -21,3 +21,10 @@ for name, what in [("ALL", L.ALL), ("CONS", L.CONS), ("JAC", L.JAC), ("HESS", L.
     e1.record(s); torch.cuda.synchronize()
     res[name] = e0.elapsed_time(e1) / 10
 print(json.dumps(res))
+from paper_2203_10587_b200 import solution as SOL
+for _ in range(3): SOL.device_flows(ev, x, stream=s.cuda_stream)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize(); e0.record(s)
+for _ in range(10): SOL.device_flows(ev, x, stream=s.cuda_stream)
+e1.record(s); torch.cuda.synchronize()
+print(json.dumps({"FLOWS(+alloc)": e0.elapsed_time(e1) / 10}))
