@@ -22,6 +22,9 @@ from .lattice import (
     compose_general, compose_multiperiod, compose_multiperiod_scopf, compose_scopf,
     compose_sopf_flat, compose_sopf_full,
 )
+from .solution import (
+    SolvedCase, extract_solution, extract_solutions, pack_solution, residuals_at, solution_from_case,
+)
 from .stage import build_acopf
 from .types import (
     CONTINGENCY_BOX, CORRECTIVE, PREVENTIVE, PREVENTIVE_PIN, RAMP, SCENARIO_BOX,
@@ -35,8 +38,9 @@ __all__ = [
     "ContingencySet", "Coupling", "CouplingMode", "CouplingRow", "CORRECTIVE", "CONTINGENCY_BOX",
     "DeviceError", "DimensionMismatch", "Disconnected", "GenCost", "Generator", "LoadProfile",
     "NetworkCase", "NlpProblem", "Outage", "PREVENTIVE", "PREVENTIVE_PIN", "RAMP", "SCENARIO_BOX",
-    "Scenario", "ScenarioSet", "StagePlan", "StageSpec", "apply_contingency", "apply_load_step",
+    "Scenario", "ScenarioSet", "SolvedCase", "StagePlan", "StageSpec", "apply_contingency", "apply_load_step",
     "apply_scenario", "branch_admittance", "build_acopf", "check_connectivity", "compose_general",
     "compose_multiperiod", "compose_multiperiod_scopf", "compose_scopf", "compose_sopf_flat",
-    "compose_sopf_full", "declare_wind", "errors",
+    "compose_sopf_full", "declare_wind", "errors", "extract_solution", "extract_solutions",
+    "pack_solution", "residuals_at", "solution_from_case",
 ]

@@ -121,12 +121,27 @@ class NetworkCase:
     def bus_pos(self) -> dict:
         return {b.id: k for k, b in enumerate(self.buses)}
 
+    @cached_property
+    def _gens_by_bus(self) -> dict:
+        out = {}
+        for k, g in enumerate(self.gens):
+            out.setdefault(g.bus, []).append(k)
+        return out
+
+    @cached_property
+    def _branches_by_ends(self) -> dict:
+        out = {}
+        for k, br in enumerate(self.branches):
+            out.setdefault((br.fbus, br.tbus), []).append(k)
+        return out
+
     def gens_at(self, bus_id: int) -> list:
-        return [k for k, g in enumerate(self.gens) if g.bus == bus_id]
+        """Positions of the generators at a bus, case order (network.py:120-122)."""
+        return list(self._gens_by_bus.get(bus_id, ()))
 
     def branches_between(self, fbus: int, tbus: int) -> list:
-        return [k for k, br in enumerate(self.branches)
-                if br.fbus == fbus and br.tbus == tbus]
+        """Positions of the branches fbus -> tbus, case order (network.py:124-127)."""
+        return list(self._branches_by_ends.get((fbus, tbus), ()))
 
 
 @dataclass(frozen=True)
