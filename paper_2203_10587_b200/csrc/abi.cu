@@ -178,22 +178,26 @@ static void upload(acopf_batch* b) {
         d.obj_slot = b->obj_slot[s];
         d.w = st.w;
         d.fl_off = fl_off; d.inj_off = inj_off;
+        d.nb = b->topos[st.topo]->nb; d.ng = b->topos[st.topo]->ng; d.nbr = b->topos[st.topo]->nbr;
         fl_off += 4LL * b->topos[st.topo]->nbr;
         inj_off += 2LL * b->topos[st.topo]->nb;
     }
-    // bus work: for every tile, the stages sharing one table, in chunks of G
+    // tile work: for every tile, the stages sharing one table, in chunks of G
+    // stages; about 4 warps' worth of items per resident warp slot
     int64_t total_recs = 0;
     for (const StageInfo& st : b->stages) total_recs += (int64_t)st.table.size();
-    const int64_t target_items = 148 * 2 * 6;
-    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(32, total_recs / target_items));
+    const int64_t target_items = 148LL * (WARP_MINB / 2) * 4;
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(64, total_recs / target_items));
     std::vector<DBusItem> items;
-    std::vector<DBusRec> recs;
+    std::vector<DRec> recs;
     size_t max_smem = 0;
     std::map<int, std::vector<int>> by_table;     // table id -> stages (in order)
     std::vector<std::pair<int, int>> tiles;       // (topo, tile)
     for (size_t ti = 0; ti < b->topos.size(); ++ti)
         for (size_t t = 0; t < b->base_table[ti].size(); ++t) tiles.push_back({(int)ti, (int)t});
-    // stage-group-major order: CTAs running together share one group's x/mult in L2
+    std::vector<int> table_area(b->tables.size());
+    for (size_t i = 0; i < b->tables.size(); ++i) table_area[i] = b->tables[i].nArea;
+    // stage-group-major order: warps running together share one group's x/mult in L2
     for (int g0 = 0; g0 < S; g0 += G) {
         const int g1 = std::min(S, g0 + G);
         for (auto [topo, t] : tiles) {
@@ -208,17 +212,20 @@ static void upload(acopf_batch* b) {
                 it.count = (int)kv.second.size();
                 for (int s : kv.second) {
                     const StageInfo& st = b->stages[s];
-                    DBusRec r{};
+                    const DStage& d = ds[s];
+                    DRec r{};
+                    r.var_off = d.var_off; r.eq_row = d.eq_row; r.ineq_row = d.ineq_row; r.pd_off = d.pd_off;
+                    r.jineq = d.jineq_base;
+                    r.oP = d.jeq_base + st.tile_off[4 * t + 0]; r.oQ = d.jeq_base + st.tile_off[4 * t + 1];
+                    r.oA = d.h_base + st.tile_off[4 * t + 2]; r.oV = d.h_base + st.tile_off[4 * t + 3];
+                    r.fl_off = d.fl_off; r.inj_off = d.inj_off; r.rem_off = d.rem_off;
+                    r.w = d.w; r.nrem = d.nrem; r.nb = d.nb; r.ng = d.ng; r.nbr = d.nbr;
                     r.stage = s;
-                    r.jP = st.tile_off[4 * t + 0]; r.jQ = st.tile_off[4 * t + 1];
-                    r.hA = st.tile_off[4 * t + 2]; r.hV = st.tile_off[4 * t + 3];
                     recs.push_back(r);
                 }
                 items.push_back(it);
-                size_t q, gv, gb, rs, fo, rc;
                 const TileTable& tt = b->tables[kv.first];
-                max_smem = std::max(max_smem, bus_smem_layout(table_bytes[kv.first], tt.nQ(), (int)tt.ends.size(),
-                                                              tt.nB, it.count, &q, &gv, &gb, &rs, &fo, &rc));
+                max_smem = std::max(max_smem, tile_smem_bytes(table_bytes[kv.first], table_area[kv.first], tt.nB, tt.ngl));
             }
         }
     }
@@ -285,11 +292,11 @@ static void upload(acopf_batch* b) {
     P.obj_mode = b->obj_mode;
     P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
     P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
-    b->smem = (max_smem + 127) & ~size_t(127);
+    b->smem = (max_smem + 15) & ~size_t(15);
     b->aux_smem = sizeof(double) * max_leaf;
-    for (auto fn : {acopf_bus_kernel<0u>, acopf_bus_kernel<ACOPF_ALL>})
+    for (auto fn : {acopf_tile_kernel<0u>, acopf_tile_kernel<ACOPF_ALL>})
         cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(bus)");
+                                        (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(tile)");
     if (b->aux_smem > 48 * 1024)
         cuda_check(cudaFuncSetAttribute(acopf_aux_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)b->aux_smem), "cudaFuncSetAttribute(aux)");
@@ -509,9 +516,9 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
             b->launches++;
         }
         if (bus) {
-            if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P, 0);
-            else acopf_bus_kernel<0u><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P, 0);
-            cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
+            if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
+            else acopf_tile_kernel<0u><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
+            cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
             b->launches++;
         }
         if (fork) {
@@ -533,8 +540,8 @@ int acopf_batch_flows(acopf_batch* b, const double* x, double* flows, double* in
         P.flows = flows; P.inj = inj;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
         if (P.n_bus_items > 0) {
-            acopf_bus_kernel<0u><<<P.n_bus_items, BUS_BLOCK, b->smem, st>>>(P, 0);
-            cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
+            acopf_tile_kernel<0u><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
+            cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
             b->launches++;
         }
     });
@@ -594,9 +601,9 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
                     b->launches++;
                 }
                 if (pc.bus_count && (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD))) {
-                    if (what == ACOPF_ALL) acopf_bus_kernel<ACOPF_ALL><<<pc.bus_count, BUS_BLOCK, b->smem, cs>>>(P, pc.bus_first);
-                    else acopf_bus_kernel<0u><<<pc.bus_count, BUS_BLOCK, b->smem, cs>>>(P, pc.bus_first);
-                    cuda_check(cudaGetLastError(), "acopf_bus_kernel launch");
+                    if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<pc.bus_count, TILE_THREADS, b->smem, cs>>>(P, pc.bus_first);
+                    else acopf_tile_kernel<0u><<<pc.bus_count, TILE_THREADS, b->smem, cs>>>(P, pc.bus_first);
+                    cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
                     b->launches++;
                 }
                 if ((what & ACOPF_OBJ) && obj) cuda_check(cudaMemcpyAsync(obj + pc.s0, dobj + pc.s0, 8 * (pc.s1 - pc.s0), cudaMemcpyDeviceToHost, cs), "D2H obj");

@@ -33,35 +33,36 @@
 
 namespace acopf {
 
-// per-end quantity slots in the tile's shared-memory array
-constexpr int EQ = 17;          // doubles per branch end
+// Per-end quantities (what one branch end contributes to its own bus's rows).
+// Both ends of a branch compute the same flows and partials (acopf.py:230-250);
+// the quantities below are the end's share of the J/H rows of its own bus.
+constexpr int NQE = 15;         // quantities per branch end
 constexpr int Q_JP = 0;         // 0..3  -dP/d(VA_f, VA_t, VM_f, VM_t) of this end's P row
 constexpr int Q_JQ = 4;         // 4..7  same for the Q row
-constexpr int Q_H = 8;          // 8..14 Hessian values of the 7 positions this end owns
-constexpr int Q_FP = 15;        // P flow at this end (pf or pt)
-constexpr int Q_FQ = 16;        // Q flow at this end (qf or qt)
-constexpr int BQ = 3;           // doubles per bus: shunt J(P,VM), shunt J(Q,VM), shunt H(VM,VM)
+constexpr int Q_H = 8;          // 8..14 Hessian values of the 7 positions this end owns (HSLOT_*)
+constexpr int NQB = 3;          // per bus: shunt J(P,VM), shunt J(Q,VM), shunt H(VM,VM)
 
 // POSITIONS (acopf.py:48-49): (row-axis, col-axis) over (VA_f, VA_t, VM_f, VM_t)
 constexpr int POS_A[10] = {0, 0, 0, 0, 1, 1, 1, 2, 2, 3};
 constexpr int POS_B[10] = {0, 1, 2, 3, 1, 2, 3, 2, 3, 3};
-// which of the 7 Hessian slots of the from (F) / to (T) end holds position p (-1: none)
-constexpr int HSLOT_F[10] = {0, 1, 2, 3, -1, 4, -1, 5, 6, -1};
-constexpr int HSLOT_T[10] = {-1, 0, -1, 1, 2, 3, 4, -1, 5, 6};
-constexpr int POS_OF_SLOT_F[7] = {0, 1, 2, 3, 5, 7, 8};
-constexpr int POS_OF_SLOT_T[7] = {1, 3, 4, 5, 6, 8, 9};
+// Hessian slot of the from (F) / to (T) end that holds position p (-1: not owned).
+// Slots 0..4 are side-independent: slot 0 is position 0 for a from-end and
+// position 4 for a to-end (bitwise the same value: the (tf,tf) and (tt,tt)
+// expressions differ only by the signs of squared partials), slots 1..4 are
+// positions 1, 3, 5, 8 (owned by both ends).  Slot 5 is position 2 / 6 and
+// slot 6 position 7 / 9: the kernel forms them with operand selects, so a
+// warp holding both sides never diverges.
+constexpr int HSLOT_F[10] = {0, 1, 5, 2, -1, 3, -1, 6, 4, -1};
+constexpr int HSLOT_T[10] = {-1, 1, -1, 2, 0, 3, 5, -1, 4, 6};
 
 #ifndef ACOPF_TILE_ENDS
-#define ACOPF_TILE_ENDS 192
+#define ACOPF_TILE_ENDS 32
 #endif
 #ifndef ACOPF_TILE_BUSES
-#define ACOPF_TILE_BUSES 96
+#define ACOPF_TILE_BUSES 64
 #endif
-#if ACOPF_TILE_BUSES > 256
-#error "one bus per thread: ACOPF_TILE_BUSES must not exceed the bus kernel block"
-#endif
-constexpr int TILE_MAX_ENDS = ACOPF_TILE_ENDS;    // soft cap; a single high-degree bus may exceed it
-constexpr int TILE_MAX_BUSES = ACOPF_TILE_BUSES;  // <= bus kernel block size (one bus per thread)
+constexpr int TILE_MAX_ENDS = ACOPF_TILE_ENDS;    // per side; soft cap: a single high-degree bus may exceed it
+constexpr int TILE_MAX_BUSES = ACOPF_TILE_BUSES;
 constexpr int SMEM_LIMIT_BYTES = 220 * 1024;
 
 // symbolic term: what a COO entry's value is made of
@@ -160,16 +161,18 @@ inline void Topo::finalize() {
         foff[r] = acc;
         acc += rowsz[r];
     }
-    // tiles: greedy runs of consecutive buses
+    // tiles: greedy runs of consecutive buses with at most TILE_MAX_ENDS
+    // from-ends and TILE_MAX_ENDS to-ends (one warp per side)
     tile_b0.clear();
     int i = 0;
     while (i < nb) {
         tile_b0.push_back(i);
-        int ends = 0, nbus = 0;
+        int nf = 0, nt = 0, nbus = 0;
         while (i < nb) {
-            int d = (from_ptr[i + 1] - from_ptr[i]) + (to_ptr[i + 1] - to_ptr[i]);
-            if (nbus > 0 && (ends + d > TILE_MAX_ENDS || nbus >= TILE_MAX_BUSES)) break;
-            ends += d;
+            const int df = from_ptr[i + 1] - from_ptr[i], dt = to_ptr[i + 1] - to_ptr[i];
+            if (nbus > 0 && (nf + df > TILE_MAX_ENDS || nt + dt > TILE_MAX_ENDS || nbus >= TILE_MAX_BUSES)) break;
+            nf += df;
+            nt += dt;
             nbus++;
             i++;
         }
@@ -245,47 +248,63 @@ inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
 }
 
 // ---------------------------------------------------------------------------
-// Tile tables (serialised into one device blob)
+// Warp tiles (serialised into one device blob)
+//
+// A tile is a run of consecutive buses with at most TILE_MAX_ENDS branch ends;
+// one warp evaluates it for a list of stages.  Its table (header + sections,
+// 16-byte aligned) is bulk-copied into the warp's shared memory once; after it
+// comes the warp's working "area" of doubles:
+//
+//   [0, T)           staging of the tile's four output segments
+//                    (J rows P_i | J rows Q_i | H rows VA_i | H rows VM_i),
+//                    copied out to global memory contiguously
+//   sum runs         one contiguous run per multi-term output entry, holding
+//                    its terms in scipy's summation order
+//   balance runs     per bus: the P flows, then the Q flows of its ends in
+//                    np.add.at order
+//   trash slot
+//
+// Every term of every output entry is used exactly once (each end quantity
+// once, except the (tf,vf)/(tt,vt) Hessian position, which appears in both
+// the VA and the VM row of the end's bus), so every quantity is stored
+// straight to where its consumer reads it: the staging position of the
+// entry it alone makes up, or its place in a sum run.  Sums then read
+// contiguous slots with no index tables.
 
-struct TileHdr {            // 192 bytes; offsets in bytes from the header start
-    int32_t b0, nB, nE, nQ;           // first bus, buses, ends, shared doubles for quantities
-    int32_t LP, LQ, LHA, LHV;         // entries of the four row segments
-    int32_t ngl, bytes, nSJ, nSH;     // generator ids, serialised size, single-term J / H entries
-    int32_t nMJ, nMH, nMT, nF;        // multi-term J / H entries, their term count, from-ends
-    int32_t o_code, o_f, o_t, o_ridx;
-    int32_t o_foff, o_busptr, o_gptr, o_glist;
-    int32_t o_gs, o_bs, o_adm, o_sj_dst;
-    int32_t o_sj_term, o_sh_dst, o_sh_term, o_mj_dst;
-    int32_t o_mj_info, o_mh_dst, o_mh_info, o_mterms;
-    int32_t o_bend;
-    int32_t pad[11];
+constexpr int NST = 18;           // stores per end: 15 quantities, P flow, Q flow, second copy of quantity 13
+constexpr int ST_FP = 15, ST_FQ = 16, ST_X13 = 17;
+
+struct TileHdr {                      // 144 bytes; section offsets in bytes from the header start
+    int32_t b0, nB, nE, nF;           // first bus, buses, ends, from-ends (ends [0,nF) are from-ends)
+    int32_t L[4];                     // entries of the four row segments
+    int32_t nArea, nSumJ, nSumH, nConst;
+    int32_t bytes, tslot, ngl, pad1;  // serialised size; trash slot; generators of the tile's buses
+    int32_t o_adm, o_f, o_t, o_ridx;
+    int32_t o_foff, o_code, o_dst, o_gs;
+    int32_t o_bs, o_brun, o_gptr, o_glist;
+    int32_t o_bqd, o_sinfo, o_const, pad2;
+    int32_t pad3[4];
 };
-static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 144, "TileHdr layout");
 
-// A tile's complete working set, copied to shared memory in one bulk copy:
-// per-end topology (bus slots, rated index, flow-row offset, SoA admittances),
-// per-bus shunts and generator lists, and the scatter map split into classes:
-//   single-term entries  dst (bit 31: Q row / VM row segment, else P / VA)
-//                        + the one quantity slot;
-//   multi-term entries   dst + (first term << 10 | term count), sorted by
-//                        decreasing count: warps run uniform trip counts and
-//                        the longest sums start first.
 struct TileTable {
     int topo = 0;
     int b0 = 0, nB = 0;
     std::vector<int> ends;        // k*2+side: all from-ends (bus order), then all to-ends
-    int nF = 0;                   // from-ends
+    int nF = 0;
     std::vector<int> busptr;      // nB+1, into bend
-    std::vector<int> bend;        // per bus: its from-ends then to-ends (end indices)
+    std::vector<int> bend;        // per bus: its from-ends then to-ends (np.add.at order)
     int L[4] = {0, 0, 0, 0};      // entries in P, Q, VA, VM segments
     std::vector<int> cols;        // stage-local column per entry (pattern export)
     std::vector<int> rowlen;      // entries per row, 4 segments x nB rows
-    std::vector<uint32_t> sdst[2];      // [0] J, [1] H
-    std::vector<uint16_t> sterm[2];
-    std::vector<uint32_t> mdst[2];
-    std::vector<uint32_t> minfo[2];
-    std::vector<uint16_t> mterms;
-    int nQ() const { return EQ * (int)ends.size() + BQ * nB + 1; }
+    // locations
+    int nArea = 0, tslot = 0, ngl = 0;   // area doubles, trash slot, generators of the tile's buses
+    std::vector<uint16_t> dst;    // NST x nE (SoA): where each end store goes
+    std::vector<uint16_t> brun;   // 2 x nB: balance P-run start, degree (Q run follows the P run)
+    std::vector<uint16_t> bqd;    // NQB x nB (SoA): location of each bus quantity
+    std::vector<uint32_t> sinfo;  // per sum entry: (dst | count << 16, run start); J sums then H sums
+    int nSumJ = 0, nSumH = 0;
+    std::vector<uint16_t> cpos;   // slots holding the constant 1.0
     void serialise(const Topo& T, std::vector<uint8_t>& blob) const;
 };
 
@@ -293,7 +312,7 @@ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) const {
     const int nE = (int)ends.size();
-    std::vector<int> f(nE), t(nE), ridx(nE), foff(nE), gptr(1, 0), glist;
+    std::vector<int> f(nE), t(nE), ridx(nE), foff(nE), code(nE), glist;
     std::vector<double> adm(8 * (size_t)nE), gs(nB), bs(nB);
     for (int e = 0; e < nE; ++e) {
         int k = ends[e] >> 1;
@@ -301,73 +320,61 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
         t[e] = T.to[k];
         ridx[e] = T.ridx[k];
         foff[e] = T.ridx[k] >= 0 ? (int)T.foff[T.ridx[k]] : 0;
+        code[e] = ends[e];
         for (int q = 0; q < 8; ++q) adm[(size_t)q * nE + e] = T.adm[8 * (size_t)k + q];
     }
+    std::vector<uint16_t> gptr(1, 0);
     for (int bl = 0; bl < nB; ++bl) {
         int i = b0 + bl;
         gs[bl] = T.gs[i];
         bs[bl] = T.bs[i];
         for (int p = T.gen_ptr[i]; p < T.gen_ptr[i + 1]; ++p) glist.push_back(T.gen_list[p]);
-        gptr.push_back((int)glist.size());
+        gptr.push_back((uint16_t)glist.size());
     }
     TileHdr h{};
-    h.b0 = b0; h.nB = nB; h.nE = nE; h.nQ = nQ();
-    h.LP = L[0]; h.LQ = L[1]; h.LHA = L[2]; h.LHV = L[3];
+    h.b0 = b0; h.nB = nB; h.nE = nE; h.nF = nF;
+    for (int s = 0; s < 4; ++s) h.L[s] = L[s];
+    h.nArea = nArea; h.nSumJ = nSumJ; h.nSumH = nSumH; h.nConst = (int)cpos.size();
+    h.tslot = tslot;
     h.ngl = (int)glist.size();
-    h.nSJ = (int)sdst[0].size(); h.nSH = (int)sdst[1].size();
-    h.nMJ = (int)mdst[0].size(); h.nMH = (int)mdst[1].size();
-    h.nMT = (int)mterms.size();
-    h.nF = nF;
     size_t off = sizeof(TileHdr);
     auto take = [&](size_t n) { int o = (int)off; off = align16(off + n); return o; };
-    h.o_code = take(4 * (size_t)nE);
+    h.o_adm = take(8 * adm.size());
     h.o_f = take(4 * (size_t)nE);
     h.o_t = take(4 * (size_t)nE);
     h.o_ridx = take(4 * (size_t)nE);
     h.o_foff = take(4 * (size_t)nE);
-    h.o_busptr = take(4 * busptr.size());
-    h.o_bend = take(4 * bend.size());
-    h.o_gptr = take(4 * gptr.size());
-    h.o_glist = take(4 * glist.size());
+    h.o_code = take(4 * (size_t)nE);
+    h.o_dst = take(2 * dst.size());
     h.o_gs = take(8 * (size_t)nB);
     h.o_bs = take(8 * (size_t)nB);
-    h.o_adm = take(8 * adm.size());
-    h.o_sj_dst = take(4 * sdst[0].size());
-    h.o_sj_term = take(2 * sterm[0].size());
-    h.o_sh_dst = take(4 * sdst[1].size());
-    h.o_sh_term = take(2 * sterm[1].size());
-    h.o_mj_dst = take(4 * mdst[0].size());
-    h.o_mj_info = take(4 * minfo[0].size());
-    h.o_mh_dst = take(4 * mdst[1].size());
-    h.o_mh_info = take(4 * minfo[1].size());
-    h.o_mterms = take(2 * mterms.size());
+    h.o_brun = take(2 * brun.size());
+    h.o_gptr = take(2 * gptr.size());
+    h.o_glist = take(4 * glist.size());
+    h.o_bqd = take(2 * bqd.size());
+    h.o_sinfo = take(4 * sinfo.size());
+    h.o_const = take(2 * cpos.size());
     h.bytes = (int)off;
     size_t base = blob.size();
     blob.resize(base + off, 0);
     uint8_t* p = blob.data() + base;
     std::memcpy(p, &h, sizeof h);
     auto put = [&](int o, const void* src, size_t n) { if (n) std::memcpy(p + o, src, n); };
-    put(h.o_code, ends.data(), 4 * (size_t)nE);
+    put(h.o_adm, adm.data(), 8 * adm.size());
     put(h.o_f, f.data(), 4 * (size_t)nE);
     put(h.o_t, t.data(), 4 * (size_t)nE);
     put(h.o_ridx, ridx.data(), 4 * (size_t)nE);
     put(h.o_foff, foff.data(), 4 * (size_t)nE);
-    put(h.o_busptr, busptr.data(), 4 * busptr.size());
-    put(h.o_bend, bend.data(), 4 * bend.size());
-    put(h.o_gptr, gptr.data(), 4 * gptr.size());
-    put(h.o_glist, glist.data(), 4 * glist.size());
+    put(h.o_code, code.data(), 4 * (size_t)nE);
+    put(h.o_dst, dst.data(), 2 * dst.size());
     put(h.o_gs, gs.data(), 8 * (size_t)nB);
     put(h.o_bs, bs.data(), 8 * (size_t)nB);
-    put(h.o_adm, adm.data(), 8 * adm.size());
-    put(h.o_sj_dst, sdst[0].data(), 4 * sdst[0].size());
-    put(h.o_sj_term, sterm[0].data(), 2 * sterm[0].size());
-    put(h.o_sh_dst, sdst[1].data(), 4 * sdst[1].size());
-    put(h.o_sh_term, sterm[1].data(), 2 * sterm[1].size());
-    put(h.o_mj_dst, mdst[0].data(), 4 * mdst[0].size());
-    put(h.o_mj_info, minfo[0].data(), 4 * minfo[0].size());
-    put(h.o_mh_dst, mdst[1].data(), 4 * mdst[1].size());
-    put(h.o_mh_info, minfo[1].data(), 4 * minfo[1].size());
-    put(h.o_mterms, mterms.data(), 2 * mterms.size());
+    put(h.o_brun, brun.data(), 2 * brun.size());
+    put(h.o_gptr, gptr.data(), 2 * gptr.size());
+    put(h.o_glist, glist.data(), 4 * glist.size());
+    put(h.o_bqd, bqd.data(), 2 * bqd.size());
+    put(h.o_sinfo, sinfo.data(), 4 * sinfo.size());
+    put(h.o_const, cpos.data(), 2 * cpos.size());
 }
 
 inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
@@ -377,7 +384,7 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     tt.nB = b1 - b0;
     std::vector<Row> rows(4 * tt.nB);
     std::unordered_map<int, int> end_pos;
-    // ends: all from-ends of the tile first (so a warp sees one side), then all to-ends
+    // ends: all from-ends of the tile first, then all to-ends
     for (int i = b0; i < b1; ++i)
         for (int p = T.from_ptr[i]; p < T.from_ptr[i + 1]; ++p)
             if (live(T.from_list[p])) {
@@ -403,52 +410,82 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         for (int s = 0; s < 4; ++s) rows[s * tt.nB + (i - b0)] = std::move(r4[s]);
     }
     const int nE = (int)tt.ends.size();
-    // classify entries: single-term gather-stores and multi-term sums
-    struct Multi { uint32_t dst; std::vector<uint16_t> t; };
-    std::vector<Multi> multi[2];
-    for (int s = 0; s < 4; ++s) {
-        const int cls = s / 2;                    // 0: J (P, Q rows), 1: H (VA, VM rows)
-        const uint32_t segbit = (s & 1) ? 0x80000000u : 0u;
-        uint32_t local = 0;
-        for (int r = 0; r < tt.nB; ++r) {
-            const Row& row = rows[s * tt.nB + r];
+    const int nB = tt.nB;
+    for (int s = 0; s < 4; ++s)
+        for (int r = 0; r < nB; ++r) {
+            const Row& row = rows[s * nB + r];
             tt.rowlen.push_back((int)row.cols.size());
             tt.L[s] += (int)row.cols.size();
-            for (size_t e = 0; e < row.cols.size(); ++e, ++local) {
-                tt.cols.push_back(row.cols[e]);
-                std::vector<uint16_t> slots;
-                for (int t = row.tptr[e]; t < row.tptr[e + 1]; ++t) {
-                    const Sym& y = row.terms[t];
-                    int slot;
-                    if (y.kind == 0) slot = EQ * end_pos.at(y.a) + y.q;
-                    else if (y.kind == 1) slot = EQ * nE + BQ * (y.a - b0) + y.q;
-                    else slot = EQ * nE + BQ * tt.nB;
-                    slots.push_back((uint16_t)slot);
-                }
-                if (slots.size() == 1) {
-                    tt.sdst[cls].push_back(segbit | local);
-                    tt.sterm[cls].push_back(slots[0]);
-                } else {
-                    multi[cls].push_back(Multi{segbit | local, slots});
-                }
+            tt.cols.insert(tt.cols.end(), row.cols.begin(), row.cols.end());
+        }
+    // locations: each term use gets one slot; -1 = not yet placed
+    std::vector<int> loc_e((size_t)NST * nE, -1), loc_b((size_t)NQB * nB, -1);
+    std::vector<int> cpos;
+    auto place = [&](const Sym& y, int slot) {
+        if (y.kind == 2) { cpos.push_back(slot); return; }
+        if (y.kind == 1) {
+            int& l = loc_b[(size_t)y.q * nB + (y.a - b0)];
+            if (l >= 0) throw std::runtime_error("planner: bus quantity used twice");
+            l = slot;
+            return;
+        }
+        const int e = end_pos.at(y.a);
+        int& l = loc_e[(size_t)y.q * nE + e];
+        if (l < 0) { l = slot; return; }
+        int& l2 = loc_e[(size_t)ST_X13 * nE + e];
+        if (y.q != Q_H + 5 || l2 >= 0) throw std::runtime_error("planner: unexpected reuse of an end quantity");
+        l2 = slot;
+    };
+    struct Sum { int dst; int row, entry; };
+    std::vector<Sum> sums[2];
+    int pos = 0;
+    for (int s = 0; s < 4; ++s)
+        for (int r = 0; r < nB; ++r) {
+            const Row& row = rows[s * nB + r];
+            for (size_t e = 0; e < row.cols.size(); ++e, ++pos) {
+                const int n = row.tptr[e + 1] - row.tptr[e];
+                if (n == 1) place(row.terms[row.tptr[e]], pos);
+                else sums[s / 2].push_back(Sum{pos, s * nB + r, (int)e});
             }
         }
-    }
-    for (int cls = 0; cls < 2; ++cls) {
-        std::stable_sort(multi[cls].begin(), multi[cls].end(),
-                         [](const Multi& x, const Multi& y) { return x.t.size() > y.t.size(); });
-        for (const Multi& m : multi[cls]) {
-            if (m.t.size() >= 1024) throw std::runtime_error("entry with >= 1024 duplicate terms");
-            tt.mdst[cls].push_back(m.dst);
-            tt.minfo[cls].push_back(((uint32_t)tt.mterms.size() << 10) | (uint32_t)m.t.size());
-            tt.mterms.insert(tt.mterms.end(), m.t.begin(), m.t.end());
+    int next = pos;
+    for (int c = 0; c < 2; ++c) {
+        std::stable_sort(sums[c].begin(), sums[c].end(), [&](const Sum& x, const Sum& y) {
+            const Row& rx = rows[x.row];
+            const Row& ry = rows[y.row];
+            return rx.tptr[x.entry + 1] - rx.tptr[x.entry] > ry.tptr[y.entry + 1] - ry.tptr[y.entry];
+        });
+        for (const Sum& sm : sums[c]) {
+            const Row& row = rows[sm.row];
+            const int n = row.tptr[sm.entry + 1] - row.tptr[sm.entry];
+            tt.sinfo.push_back((uint32_t)sm.dst | ((uint32_t)n << 16));
+            tt.sinfo.push_back((uint32_t)next);
+            for (int t = row.tptr[sm.entry]; t < row.tptr[sm.entry + 1]; ++t) place(row.terms[t], next++);
         }
+        (c == 0 ? tt.nSumJ : tt.nSumH) = (int)sums[c].size();
     }
-    // shared memory = serialised table + quantity array (checked again at upload)
-    size_t approx = 192 + 84 * (size_t)nE + 24 * (size_t)tt.nB + 6 * tt.cols.size() + 2 * tt.mterms.size() +
-                    8 * (size_t)tt.nQ() + 512;
-    if (approx > (size_t)SMEM_LIMIT_BYTES)
-        throw std::runtime_error("bus degree too high for one tile's shared memory");
+    // balance runs: per bus its P flows then its Q flows, in np.add.at order
+    tt.brun.assign(2 * (size_t)nB, 0);
+    for (int bl = 0; bl < nB; ++bl) {
+        const int deg = tt.busptr[bl + 1] - tt.busptr[bl];
+        tt.brun[bl] = (uint16_t)next;
+        tt.brun[nB + bl] = (uint16_t)deg;
+        for (int j = 0; j < deg; ++j) {
+            const int e = tt.bend[tt.busptr[bl] + j];
+            loc_e[(size_t)ST_FP * nE + e] = next + j;
+            loc_e[(size_t)ST_FQ * nE + e] = next + deg + j;
+        }
+        next += 2 * deg;
+    }
+    for (int i = b0; i < b1; ++i) tt.ngl += T.gen_ptr[i + 1] - T.gen_ptr[i];
+    tt.tslot = next++;
+    tt.nArea = next;
+    if (tt.nArea > 65535) throw std::runtime_error("tile working area exceeds 16-bit slots");
+    for (int v : cpos) tt.cpos.push_back((uint16_t)v);
+    tt.dst.resize(loc_e.size());
+    for (size_t i = 0; i < loc_e.size(); ++i) tt.dst[i] = (uint16_t)(loc_e[i] < 0 ? tt.tslot : loc_e[i]);
+    tt.bqd.resize(loc_b.size());
+    for (size_t i = 0; i < loc_b.size(); ++i) tt.bqd[i] = (uint16_t)(loc_b[i] < 0 ? tt.tslot : loc_b[i]);
     return tt;
 }
 
