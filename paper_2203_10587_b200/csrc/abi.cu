@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <numeric>
@@ -225,7 +226,7 @@ static void upload(acopf_batch* b) {
                 }
                 items.push_back(it);
                 const TileTable& tt = b->tables[kv.first];
-                max_smem = std::max(max_smem, tile_smem_bytes(table_bytes[kv.first], table_area[kv.first], tt.nB, tt.ngl));
+                max_smem = std::max(max_smem, tile_smem_bytes(table_bytes[kv.first], table_area[kv.first]));
             }
         }
     }
@@ -360,6 +361,33 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
                 ids.push_back((int)B->tables.size() - 1);
             }
             B->base_table.push_back(ids);
+            if (getenv("ACOPF_DEBUG_PLAN")) {     // planner statistics (development aid)
+                size_t tb = 0, ar = 0, mx = 0, ends = 0, terms = 0, slots = 0;
+                for (int id : ids) {
+                    std::vector<uint8_t> blob;
+                    const TileTable& tt = B->tables[id];
+                    tt.serialise(T, blob);
+                    tb += blob.size();
+                    ar += 8 * (size_t)tt.nArea;
+                    mx = std::max(mx, tile_smem_bytes((int)blob.size(), tt.nArea));
+                    ends += tt.ends.size();
+                    for (size_t r = 0; r < tt.sround.size() / 2; ++r) slots += 32 * (size_t)tt.sround[2 * r + 1];
+                    terms += tt.nega.size();
+                }
+                std::vector<size_t> sm;
+                for (int id : ids) {
+                    std::vector<uint8_t> blob;
+                    B->tables[id].serialise(T, blob);
+                    sm.push_back(tile_smem_bytes((int)blob.size(), B->tables[id].nArea));
+                }
+                std::sort(sm.begin(), sm.end());
+                fprintf(stderr, "plan: smem p50 %zu p90 %zu p99 %zu max %zu\n", sm[sm.size() / 2], sm[sm.size() * 9 / 10],
+                        sm[sm.size() * 99 / 100], sm.back());
+                fprintf(stderr, "plan: topo %d: %zu tiles, %.1f ends/tile, table %.0f B, area %.0f B, max smem %zu, "
+                        "sum-round slots %.0f, -0.0 pads %.0f per tile\n", i, ids.size(), (double)ends / ids.size(),
+                        (double)tb / ids.size(), (double)ar / ids.size(), mx, (double)slots / ids.size(),
+                        (double)terms / ids.size());
+            }
         }
         B->pd.assign(pd, pd + n_load_values);
         B->qd.assign(qd, qd + n_load_values);

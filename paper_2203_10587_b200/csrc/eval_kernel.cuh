@@ -127,20 +127,18 @@ __device__ __forceinline__ double hval(double cpf, double cqf, double cpt, doubl
 }
 
 constexpr int TILE_THREADS = 64;   // warp 0: the tile's from-ends, warp 1: its to-ends
-constexpr int GB = 5;              // gathered doubles per bus: vm mu_P mu_Q pd qd; then Pg, Qg per generator
 
-// Dynamic shared memory of one tile CTA: table | area | 2 bus-gather buffers | 2 records.
+constexpr int GQ = 4;    // doubles per thread in the gather buffer: pd qd (bus representative), Pg Qg (generator)
+
+// Dynamic shared memory of one tile CTA: table | area | gather buffer | 2 stage records.
 __host__ __device__ __forceinline__ size_t tile_gather_off(int table_bytes, int n_area) {
     return (size_t)table_bytes + ((8 * (size_t)n_area + 15) & ~size_t(15));
 }
-__host__ __device__ __forceinline__ size_t tile_gather_stride(int nB, int ngl) {
-    return (8 * (size_t)(GB * nB + 2 * ngl) + 15) & ~size_t(15);
+__host__ __device__ __forceinline__ size_t tile_rec_off(int table_bytes, int n_area) {
+    return tile_gather_off(table_bytes, n_area) + 8 * (size_t)GQ * TILE_THREADS;
 }
-__host__ __device__ __forceinline__ size_t tile_rec_off(int table_bytes, int n_area, int nB, int ngl) {
-    return tile_gather_off(table_bytes, n_area) + 2 * tile_gather_stride(nB, ngl);
-}
-__host__ __device__ __forceinline__ size_t tile_smem_bytes(int table_bytes, int n_area, int nB, int ngl) {
-    return tile_rec_off(table_bytes, n_area, nB, ngl) + 2 * sizeof(DRec);
+__host__ __device__ __forceinline__ size_t tile_smem_bytes(int table_bytes, int n_area) {
+    return tile_rec_off(table_bytes, n_area) + 2 * sizeof(DRec);
 }
 
 __device__ __forceinline__ void cp_async8s(unsigned dst, const void* src) {
@@ -175,23 +173,42 @@ __device__ __forceinline__ void rated_shift(const EvalParams& P, const DRec& R, 
 struct TileView {
     const TileHdr* H;
     const double* adm;
-    const int *f, *t, *ridx, *foff, *code;
-    const unsigned short* dst;
+    const int *f, *t, *ridx, *foff, *code, *rep;
+    const unsigned* dst;      // per end: 9 words of two area byte offsets
+    const double *gs, *bs;
+    const unsigned short* bqd;
 };
 
-// One end's stage inputs (registers; prefetched during the previous stage).
+// One thread's stage inputs: its branch end's, its bus's loads when the end
+// represents the bus, and one generator's set-points.
 struct EndIn {
     double vaf, vat, vf, vt, mpf, mqf, mpt, mqt, sf, st;
     long long fo;
     int rs;
 };
 
-__device__ __forceinline__ void load_end(const EvalParams& P, const DRec& R, const TileView& V, int e, bool need_h,
-                                         EndIn& in) {
+// Prefetch one thread's stage inputs: its branch end's into registers (in),
+// its bus's loads and its generator's set-points with cp.async into its
+// column of the gather buffer (G[q * TILE_THREADS + tid]).
+__device__ __forceinline__ void prefetch(const EvalParams& P, const DRec& R, const TileView& V, int e, int gi,
+                                         unsigned sG, bool need_h, bool need_c, EndIn& in) {
     const int nE = V.H->nE;
-    if (e >= nE) return;
-    const int f = V.f[e], t = V.t[e], r = V.ridx[e];
     const double* x = opaque(P.x + R.var_off);
+    const unsigned st = 8u * TILE_THREADS;
+    if (need_c && gi < V.H->ngl) {
+        const int g = reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(V.H) + V.H->o_glist)[gi];
+        const double* pg = x + 2 * R.nb + g;
+        cp_async8s(sG + 2 * st, pg);
+        cp_async8s(sG + 3 * st, pg + R.ng);
+    }
+    if (e >= nE) return;
+    const int rb = V.rep[e];
+    if (need_c && rb >= 0) {
+        const int i = V.H->b0 + rb;
+        cp_async8s(sG, P.pd + R.pd_off + i);
+        cp_async8s(sG + st, P.qd + R.pd_off + i);
+    }
+    const int f = V.f[e], t = V.t[e], r = V.ridx[e];
     const double* xm = x + R.nb;
     in.vaf = __ldg(x + f);
     in.vat = __ldg(x + t);
@@ -217,58 +234,91 @@ __device__ __forceinline__ void load_end(const EvalParams& P, const DRec& R, con
     }
 }
 
-// Prefetch one stage's bus and generator inputs of the tile (LDGSTS).
-__device__ __forceinline__ void issue_bus_gathers(const EvalParams& P, const DRec& R, const TileHdr* H,
-                                                  const unsigned char* smem, double* Gb, int tid, bool need_h,
-                                                  bool need_c) {
-    const int nB = H->nB, b0 = H->b0;
-    const double* xm = opaque(P.x + R.var_off) + R.nb;
-    const double* mu = opaque(P.mult + R.eq_row);
-    const double* mq = mu + R.nb;
-    const double* pd = opaque(P.pd + R.pd_off);
-    const double* qd = opaque(P.qd + R.pd_off);
-    const unsigned sB = smem_u32(Gb);
-    const unsigned sb = 8u * (unsigned)nB;
-    for (int bl = tid; bl < nB; bl += TILE_THREADS) {
-        const int i = b0 + bl;
-        const unsigned d = sB + 8u * (unsigned)bl;
-        cp_async8s(d, xm + i);
-        if (need_h) {
-            cp_async8s(d + sb, mu + i);
-            cp_async8s(d + 2 * sb, mq + i);
-        }
-        if (need_c) {
-            cp_async8s(d + 3 * sb, pd + i);
-            cp_async8s(d + 4 * sb, qd + i);
+// Direct (unprefetched) inputs of end e: ends beyond the first 32 of a side.
+__device__ __forceinline__ void load_end(const EvalParams& P, const DRec& R, const TileView& V, int e, bool need_h,
+                                         bool need_c, EndIn& in) {
+    const int f = V.f[e], t = V.t[e], r = V.ridx[e];
+    const double* x = P.x + R.var_off;
+    const double* xm = x + R.nb;
+    in.vaf = __ldg(x + f);
+    in.vat = __ldg(x + t);
+    in.vf = __ldg(xm + f);
+    in.vt = __ldg(xm + t);
+    in.rs = -1;
+    in.fo = 0;
+    if (r >= 0) rated_shift(P, R, r, V.foff[e], in.rs, in.fo);
+    if (need_h) {
+        const double* mu = P.mult + R.eq_row;
+        const double* mq = mu + R.nb;
+        in.mpf = __ldg(mu + f);
+        in.mqf = __ldg(mq + f);
+        in.mpt = __ldg(mu + t);
+        in.mqt = __ldg(mq + t);
+        in.sf = 0.0;
+        in.st = 0.0;
+        if (r >= 0) {
+            const double* mi = P.mult + R.ineq_row + 2 * in.rs;
+            in.sf = __ldg(mi);
+            in.st = __ldg(mi + 1);
         }
     }
+}
+
+__device__ __forceinline__ void sts64(unsigned addr, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
+// A bus's own terms (acopf.py:262-263, 283, 296-297, 366): shunt Jacobian and
+// Hessian entries, the shunt terms of its balance rows, its loads, and its
+// zero gradient entries.  Computed by the bus's first branch end (or, for a
+// bus without branches, by the orphan loop).
+__device__ __forceinline__ void bus_terms(const EvalParams& P, const DRec& R, const TileView& V, int rb, double vm,
+                                          double mp, double mq, double pd, double qd, unsigned sA, bool need_j,
+                                          bool need_h, bool need_c, bool need_f, bool need_g) {
+    const int nB = V.H->nB;
+    const double gsb = V.gs[rb], bsb = V.bs[rb];
+    const unsigned short* q = V.bqd + rb;
+    if (need_j) {
+        sts64(sA + 8u * q[0], (-2.0 * gsb) * vm);
+        sts64(sA + 8u * q[nB], (2.0 * bsb) * vm);
+    }
+    if (need_h) sts64(sA + 8u * q[2 * nB], 2.0 * ((-mp) * gsb - (-mq) * bsb));
+    if (need_c || need_f) {
+        sts64(sA + 8u * q[3 * nB], (gsb * vm) * vm);
+        sts64(sA + 8u * q[4 * nB], -((bsb * vm) * vm));
+    }
     if (need_c) {
-        const int ngl = H->ngl;
-        const int* glist = reinterpret_cast<const int*>(smem + H->o_glist);
-        const unsigned sg = sB + GB * sb;
-        const double* pg = opaque(P.x + R.var_off) + 2 * R.nb;
-        const double* qg = pg + R.ng;
-        for (int gi = tid; gi < ngl; gi += TILE_THREADS) {
-            const int g = glist[gi];
-            cp_async8s(sg + 8u * (unsigned)gi, pg + g);
-            cp_async8s(sg + 8u * (unsigned)(ngl + gi), qg + g);
-        }
+        sts64(sA + 8u * q[5 * nB], pd);
+        sts64(sA + 8u * q[6 * nB], qd);
+    }
+    if (need_g) {
+        const int i = V.H->b0 + rb;
+        P.grad[R.var_off + i] = R.w * 0.0;
+        P.grad[R.var_off + R.nb + i] = R.w * 0.0;
     }
 }
 
 // Phase A for one branch end of side SIDE (0: from-end, 1: to-end):
 // acopf.py:230-250 (flows, partials), 290-311 (Jacobian), 313-369 (Hessian),
 // in the reference's association with no contraction.  Each of the end's 18
-// stores goes to the slot its consumer reads (planner.hpp).
+// stores goes to the area slot its consumer reads (planner.hpp).
+//
+// Hessian positions: with gpf1 = -gpf0, gqf1 = -gqf0, gpt1 = -gpt0 and
+// gqt1 = -gqt0 bitwise (acopf.py:244-247), and the position coefficients of
+// acopf.py:321-328, every product of positions 1, 5 and 6 is the exact
+// negation of the matching product of positions 0, 2 and 3; round-to-nearest
+// is symmetric under negation, so v1 = -v0, v5 = -v2, v6 = -v3 bitwise, and
+// v4 = v0 (the squared partials agree).  An end evaluates 5 positions.
 template <int SIDE>
 __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, const TileView& V, int e,
-                                         const EndIn& in, double* A, bool need_j, bool need_h, bool need_c,
-                                         bool need_f) {
+                                         const EndIn& in, const double* G, unsigned sA, bool need_j, bool need_h,
+                                         bool need_c, bool need_f, bool need_g) {
     const int nE = V.H->nE;
-    const double* adm = V.adm;
-    const double gff = adm[e], bff = adm[nE + e], gft = adm[2 * nE + e], bft = adm[3 * nE + e];
-    const double gtf = adm[4 * nE + e], btf = adm[5 * nE + e], gtt = adm[6 * nE + e], btt = adm[7 * nE + e];
-    const unsigned short* dq = V.dst + e;
+    const double* adm = V.adm + e;
+    const double gff = adm[0], bff = adm[nE], gft = adm[2 * nE], bft = adm[3 * nE];
+    const double gtf = adm[4 * nE], btf = adm[5 * nE], gtt = adm[6 * nE], btt = adm[7 * nE];
+    const double g2ff = adm[8 * nE], m2bff = adm[9 * nE], g2tt = adm[10 * nE], m2btt = adm[11 * nE];
+    const unsigned* dw = V.dst + 9 * e;
     const double vf = in.vf, vt = in.vt;
     const double th = in.vaf - in.vat;
     double sn, cs;
@@ -283,8 +333,9 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
     const double pt = (gtt * vt) * vt + vv * u2;
     const double qt = ((-btt) * vt) * vt + vv * w2;
     const double fp = SIDE ? pt : pf, fq = SIDE ? qt : qf;
-    A[dq[ST_FP * nE]] = fp;
-    A[dq[ST_FQ * nE]] = fq;
+    const unsigned d7 = dw[7], d8 = dw[8];
+    sts64(sA + (d7 >> 16), fp);              // store 15
+    sts64(sA + (d8 & 0xffffu), fq);          // store 16
     if (need_f) {          // acopf.py:448-465 (_branch_flows_mw, before the MVA scaling)
         double* flw = P.flows + R.fl_off + 2 * SIDE * (long long)R.nbr + (V.code[e] >> 1);
         flw[0] = fp;
@@ -292,27 +343,47 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
     }
     const bool rated = in.rs >= 0;
     if (rated && need_c) P.cons[R.ineq_row + 2 * in.rs + SIDE] = fp * fp + fq * fq;
+    const int rb = V.rep[e];
+    if (rb >= 0) {
+        double pdv = 0.0, qdv = 0.0;
+        if (need_c) {
+            if (G) { pdv = G[0]; qdv = G[TILE_THREADS]; }
+            else {
+                const int i = V.H->b0 + rb;
+                pdv = __ldg(P.pd + R.pd_off + i);
+                qdv = __ldg(P.qd + R.pd_off + i);
+            }
+        }
+        bus_terms(P, R, V, rb, SIDE ? vt : vf, SIDE ? in.mpt : in.mpf, SIDE ? in.mqt : in.mqf, pdv, qdv, sA,
+                  need_j, need_h, need_c, need_f, need_g);
+    }
     if (!(need_j || need_h)) return;
-    const double gpf0 = (-vv) * w, gpf1 = vv * w, gpf2 = (2.0 * gff) * vf + vt * u, gpf3 = vf * u;
-    const double gqf0 = vv * u, gqf1 = (-vv) * u, gqf2 = (-2.0 * bff) * vf + vt * w, gqf3 = vf * w;
-    const double gpt0 = vv * w2, gpt1 = (-vv) * w2, gpt2 = vt * u2, gpt3 = (2.0 * gtt) * vt + vf * u2;
-    const double gqt0 = (-vv) * u2, gqt1 = vv * u2, gqt2 = vt * w2, gqt3 = (-2.0 * btt) * vt + vf * w2;
+    const double gpf0 = (-vv) * w, gpf2 = g2ff * vf + vt * u, gpf3 = vf * u;
+    const double gqf0 = vv * u, gqf2 = m2bff * vf + vt * w, gqf3 = vf * w;
+    const double gpt0 = vv * w2, gpt2 = vt * u2, gpt3 = g2tt * vt + vf * u2;
+    const double gqt0 = (-vv) * u2, gqt2 = vt * w2, gqt3 = m2btt * vt + vf * w2;
     if (need_j) {
-        const double gp0 = SIDE ? gpt0 : gpf0, gp1 = SIDE ? gpt1 : gpf1;
-        const double gp2 = SIDE ? gpt2 : gpf2, gp3 = SIDE ? gpt3 : gpf3;
-        const double gq0 = SIDE ? gqt0 : gqf0, gq1 = SIDE ? gqt1 : gqf1;
-        const double gq2 = SIDE ? gqt2 : gqf2, gq3 = SIDE ? gqt3 : gqf3;
-        A[dq[0 * nE]] = -gp0; A[dq[1 * nE]] = -gp1; A[dq[2 * nE]] = -gp2; A[dq[3 * nE]] = -gp3;
-        A[dq[4 * nE]] = -gq0; A[dq[5 * nE]] = -gq1; A[dq[6 * nE]] = -gq2; A[dq[7 * nE]] = -gq3;
+        // own partials; index 1 is the exact negation of index 0
+        const double gp0 = SIDE ? gpt0 : gpf0, gp2 = SIDE ? gpt2 : gpf2, gp3 = SIDE ? gpt3 : gpf3;
+        const double gq0 = SIDE ? gqt0 : gqf0, gq2 = SIDE ? gqt2 : gqf2, gq3 = SIDE ? gqt3 : gqf3;
+        const unsigned d0 = dw[0], d1 = dw[1], d2 = dw[2], d3 = dw[3];
+        sts64(sA + (d0 & 0xffffu), -gp0);
+        sts64(sA + (d0 >> 16), gp0);
+        sts64(sA + (d1 & 0xffffu), -gp2);
+        sts64(sA + (d1 >> 16), -gp3);
+        sts64(sA + (d2 & 0xffffu), -gq0);
+        sts64(sA + (d2 >> 16), gq0);
+        sts64(sA + (d3 & 0xffffu), -gq2);
+        sts64(sA + (d3 >> 16), -gq3);
         if (rated) {
             const double tp = 2.0 * fp, tq = 2.0 * fq;
-            const double d0 = (0.0 + tp * gp0) + tq * gq0, d1 = (0.0 + tp * gp1) + tq * gq1;
-            const double d2 = (0.0 + tp * gp2) + tq * gq2, d3 = (0.0 + tp * gp3) + tq * gq3;
+            const double r0 = (0.0 + tp * gp0) + tq * gq0, r1 = (0.0 + tp * (-gp0)) + tq * (-gq0);
+            const double r2 = (0.0 + tp * gp2) + tq * gq2, r3 = (0.0 + tp * gp3) + tq * gq3;
             const int f = V.f[e], t = V.t[e];
             double* out = P.jval + R.jineq + in.fo + (f == t ? 2 : 4) * SIDE;
-            if (f < t) { out[0] = d0; out[1] = d1; out[2] = d2; out[3] = d3; }
-            else if (f > t) { out[0] = d1; out[1] = d0; out[2] = d3; out[3] = d2; }
-            else { out[0] = d0 + d1; out[1] = d2 + d3; }
+            if (f < t) { out[0] = r0; out[1] = r1; out[2] = r2; out[3] = r3; }
+            else if (f > t) { out[0] = r1; out[1] = r0; out[2] = r3; out[3] = r2; }
+            else { out[0] = r0 + r1; out[1] = r2 + r3; }
         }
     }
     if (need_h) {
@@ -321,52 +392,66 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
         const double cpt = (-in.mpt) + s2t * pt, cqt = (-in.mqt) + s2t * qt;
         const double vvu = vv * u, vvw = vv * w, vvu2 = vv * u2, vvw2 = vv * w2;
         const double z = 0.0;
-        // slot 0: position 0 (from) = position 4 (to), bitwise
-        A[dq[8 * nE]] = hval(cpf, cqf, cpt, cqt, s2f, s2t, -vvu, -vvw, -vvu2, -vvw2,
-                             gpf0, gpf0, gqf0, gqf0, gpt0, gpt0, gqt0, gqt0);
-        // slot 1: position 1 (tf, tt)
-        A[dq[9 * nE]] = hval(cpf, cqf, cpt, cqt, s2f, s2t, vvu, vvw, vvu2, vvw2,
-                             gpf0, gpf1, gqf0, gqf1, gpt0, gpt1, gqt0, gqt1);
-        // slot 2: position 3 (tf, vt)
-        A[dq[10 * nE]] = hval(cpf, cqf, cpt, cqt, s2f, s2t, (-vf) * w, vf * u, vf * w2, (-vf) * u2,
-                              gpf0, gpf3, gqf0, gqf3, gpt0, gpt3, gqt0, gqt3);
-        // slot 3: position 5 (tt, vf)
-        A[dq[11 * nE]] = hval(cpf, cqf, cpt, cqt, s2f, s2t, vt * w, (-vt) * u, (-vt) * w2, vt * u2,
-                              gpf1, gpf2, gqf1, gqf2, gpt1, gpt2, gqt1, gqt2);
-        // slot 4: position 8 (vf, vt)
-        A[dq[12 * nE]] = hval(cpf, cqf, cpt, cqt, s2f, s2t, u, w, u2, w2,
-                              gpf2, gpf3, gqf2, gqf3, gpt2, gpt3, gqt2, gqt3);
-        double v5, v6;
-        if constexpr (SIDE == 0) {
-            // slot 5: position 2 (tf, vf); slot 6: position 7 (vf, vf)
-            v5 = hval(cpf, cqf, cpt, cqt, s2f, s2t, (-vt) * w, vt * u, vt * w2, (-vt) * u2,
-                      gpf0, gpf2, gqf0, gqf2, gpt0, gpt2, gqt0, gqt2);
-            v6 = hval(cpf, cqf, cpt, cqt, s2f, s2t, 2.0 * gff, -(2.0 * bff), z, z,
-                      gpf2, gpf2, gqf2, gqf2, gpt2, gpt2, gqt2, gqt2);
-        } else {
-            // slot 5: position 6 (tt, vt); slot 6: position 9 (vt, vt)
-            v5 = hval(cpf, cqf, cpt, cqt, s2f, s2t, vf * w, (-vf) * u, (-vf) * w2, vf * u2,
-                      gpf1, gpf3, gqf1, gqf3, gpt1, gpt3, gqt1, gqt3);
-            v6 = hval(cpf, cqf, cpt, cqt, s2f, s2t, z, z, 2.0 * gtt, -(2.0 * btt),
-                      gpf3, gpf3, gqf3, gqf3, gpt3, gpt3, gqt3, gqt3);
-        }
-        // position 2 / 6 appears in both the VA and the VM row of the end's bus
-        A[dq[13 * nE]] = v5;
-        A[dq[ST_X13 * nE]] = v5;
-        A[dq[14 * nE]] = v6;
+        // position 0 (= position 4; position 1 is its negation)
+        const double v0 = hval(cpf, cqf, cpt, cqt, s2f, s2t, -vvu, -vvw, -vvu2, -vvw2,
+                               gpf0, gpf0, gqf0, gqf0, gpt0, gpt0, gqt0, gqt0);
+        // position 2 (tf, vf) (position 5 is its negation)
+        const double v2 = hval(cpf, cqf, cpt, cqt, s2f, s2t, (-vt) * w, vt * u, vt * w2, (-vt) * u2,
+                               gpf0, gpf2, gqf0, gqf2, gpt0, gpt2, gqt0, gqt2);
+        // position 3 (tf, vt) (position 6 is its negation)
+        const double v3 = hval(cpf, cqf, cpt, cqt, s2f, s2t, (-vf) * w, vf * u, vf * w2, (-vf) * u2,
+                               gpf0, gpf3, gqf0, gqf3, gpt0, gpt3, gqt0, gqt3);
+        // position 8 (vf, vt)
+        const double v8 = hval(cpf, cqf, cpt, cqt, s2f, s2t, u, w, u2, w2,
+                               gpf2, gpf3, gqf2, gqf3, gpt2, gpt3, gqt2, gqt3);
+        // position 7 (vf, vf) of a from-end, position 9 (vt, vt) of a to-end
+        const double v79 = SIDE ? hval(cpf, cqf, cpt, cqt, s2f, s2t, z, z, g2tt, m2btt,
+                                       gpf3, gpf3, gqf3, gqf3, gpt3, gpt3, gqt3, gqt3)
+                                : hval(cpf, cqf, cpt, cqt, s2f, s2t, g2ff, m2bff, z, z,
+                                       gpf2, gpf2, gqf2, gqf2, gpt2, gpt2, gqt2, gqt2);
+        const double v5s = SIDE ? -v3 : v2;      // slot 5: position 2 (from) / 6 (to)
+        const unsigned d4 = dw[4], d5 = dw[5], d6 = dw[6];
+        sts64(sA + (d4 & 0xffffu), v0);          // slot 0: position 0 / 4
+        sts64(sA + (d4 >> 16), -v0);             // slot 1: position 1
+        sts64(sA + (d5 & 0xffffu), v3);          // slot 2: position 3
+        sts64(sA + (d5 >> 16), -v2);             // slot 3: position 5
+        sts64(sA + (d6 & 0xffffu), v8);          // slot 4: position 8
+        sts64(sA + (d6 >> 16), v5s);             // slot 5
+        sts64(sA + (d7 & 0xffffu), v79);         // slot 6: position 7 / 9
+        sts64(sA + (d8 >> 16), v5s);             // slot 5, second use
     }
 }
 
 template <int SIDE>
 __device__ __forceinline__ void ends_phase(const EvalParams& P, const DRec& R, const TileView& V, int lane,
-                                           const EndIn& pre, double* A, bool need_j, bool need_h, bool need_c,
-                                           bool need_f) {
+                                           const EndIn& pre, const double* G, unsigned sA, bool need_j,
+                                           bool need_h, bool need_c, bool need_f, bool need_g) {
     const int e0 = SIDE ? V.H->nF : 0, e1 = SIDE ? V.H->nE : V.H->nF;
-    if (e0 + lane < e1) end_eval<SIDE>(P, R, V, e0 + lane, pre, A, need_j, need_h, need_c, need_f);
+    if (e0 + lane < e1) end_eval<SIDE>(P, R, V, e0 + lane, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
     for (int e = e0 + lane + 32; e < e1; e += 32) {     // sides with more than 32 ends: unprefetched
         EndIn in;
-        load_end(P, R, V, e, need_h, in);
-        end_eval<SIDE>(P, R, V, e, in, A, need_j, need_h, need_c, need_f);
+        load_end(P, R, V, e, need_h, need_c, in);
+        end_eval<SIDE>(P, R, V, e, in, nullptr, sA, need_j, need_h, need_c, need_f, need_g);
+    }
+}
+
+// Generator set-points into their balance-round slots (thread tid: generator
+// tid prefetched, further ones loaded here).
+__device__ __forceinline__ void gens_phase(const EvalParams& P, const DRec& R, const TileView& V, int tid,
+                                           const double* G, unsigned sA) {
+    const int ngl = V.H->ngl;
+    const unsigned char* base = reinterpret_cast<const unsigned char*>(V.H);
+    const unsigned short* gdst = reinterpret_cast<const unsigned short*>(base + V.H->o_gdst);
+    if (tid < ngl) {
+        sts64(sA + 8u * gdst[tid], G[2 * TILE_THREADS]);
+        sts64(sA + 8u * gdst[ngl + tid], G[3 * TILE_THREADS]);
+    }
+    const int* glist = reinterpret_cast<const int*>(base + V.H->o_glist);
+    const double* pg = P.x + R.var_off + 2 * R.nb;
+    for (int gi = tid + TILE_THREADS; gi < ngl; gi += TILE_THREADS) {
+        const int g = glist[gi];
+        sts64(sA + 8u * gdst[gi], __ldg(pg + g));
+        sts64(sA + 8u * gdst[ngl + gi], __ldg(pg + R.ng + g));
     }
 }
 
@@ -380,13 +465,23 @@ __device__ __forceinline__ void copy_seg16(double* g, const double* s, int L, in
     if (sub == 15 && ((L - peel) & 1)) g[L - 1] = s[L - 1];
     double2* g2 = reinterpret_cast<double2*>(g + peel) + sub;
     const double* s2 = s + peel + 2 * sub;
-    for (int k = sub; k < n2; k += 16) {
+    int k = sub;
+    for (; k + 16 < n2; k += 32) {
+        double2 v, v2;
+        v.x = s2[0];
+        v.y = s2[1];
+        v2.x = s2[32];
+        v2.y = s2[33];
+        g2[0] = v;
+        g2[16] = v2;
+        g2 += 32;
+        s2 += 64;
+    }
+    if (k < n2) {
         double2 v;
         v.x = s2[0];
         v.y = s2[1];
         *g2 = v;
-        g2 += 16;
-        s2 += 32;
     }
 }
 
@@ -394,16 +489,18 @@ __device__ __forceinline__ void copy_seg16(double* g, const double* s, int L, in
 // Tile kernel: one 64-thread CTA evaluates one tile for a run of stages.
 //
 //   0. one thread bulk-copies the tile table (cp.async.bulk + mbarrier) into
-//      shared memory; the constant 1.0 entries are written once;
-//   per stage (inputs and the next record were prefetched during the
-//   previous stage: end inputs into registers, bus inputs with cp.async):
+//      shared memory; the constant 1.0 entries and -0.0 paddings are written
+//      once;
+//   per stage (every thread's inputs were prefetched into registers during
+//   the previous stage, the next record with cp.async):
 //   A. warp 0 = the tile's from-ends, warp 1 = its to-ends, one per lane
-//      (side-uniform code: no divergence, no selects); thread = bus: shunt
-//      quantities (acopf.py:262-263, 296-297, 366).
-//   B. two threads per bus: P/Q balance rows in np.add.at order
-//      (acopf.py:252-288); the next stage's gathers are issued; thread = sum
-//      entry: left-to-right sum of its contiguous term run (scipy's
-//      duplicate order, planner.hpp).
+//      (side-uniform code: no divergence, no selects); the first end of each
+//      bus also stores the bus's shunt terms and loads; thread = generator:
+//      its set-points into the balance rounds.
+//   B. balance rounds: lane = (bus, P|Q), P/Q balance rows in np.add.at order
+//      (acopf.py:252-288); the next stage's gathers are issued; sum rounds:
+//      lane = multi-term entry, left-to-right sum in scipy's duplicate order
+//      (planner.hpp).  Rounds are warp-uniform loops over padded runs.
 //   C. the four staged segments are copied to their contiguous CSR runs.
 // Three CTA barriers per stage (two warps); CTAs never wait on each other.
 template <unsigned WHAT>
@@ -440,11 +537,12 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
         }
     }
     const TileHdr* H = reinterpret_cast<const TileHdr*>(smem);
-    const int nB = H->nB, b0 = H->b0, ngl = H->ngl;
+    const int b0 = H->b0;
     double* A = reinterpret_cast<double*>(smem + H->bytes);
-    double* Gbuf = reinterpret_cast<double*>(smem + tile_gather_off(H->bytes, H->nArea));
-    const size_t gstride = tile_gather_stride(nB, ngl) / 8;
-    DRec* ctx = reinterpret_cast<DRec*>(smem + tile_rec_off(H->bytes, H->nArea, nB, ngl));
+    const unsigned sA = smem_u32(A);
+    DRec* ctx = reinterpret_cast<DRec*>(smem + tile_rec_off(H->bytes, H->nArea));
+    const double* G = reinterpret_cast<const double*>(smem + tile_gather_off(H->bytes, H->nArea)) + tid;
+    const unsigned sG = smem_u32(G);
     TileView V;
     V.H = H;
     V.adm = reinterpret_cast<const double*>(smem + H->o_adm);
@@ -453,16 +551,23 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
     V.ridx = reinterpret_cast<const int*>(smem + H->o_ridx);
     V.foff = reinterpret_cast<const int*>(smem + H->o_foff);
     V.code = reinterpret_cast<const int*>(smem + H->o_code);
-    V.dst = reinterpret_cast<const unsigned short*>(smem + H->o_dst);
-    const double* Tgs = reinterpret_cast<const double*>(smem + H->o_gs);
-    const double* Tbs = reinterpret_cast<const double*>(smem + H->o_bs);
-    const unsigned short* brun = reinterpret_cast<const unsigned short*>(smem + H->o_brun);
-    const unsigned short* gptr = reinterpret_cast<const unsigned short*>(smem + H->o_gptr);
-    const unsigned short* bqd = reinterpret_cast<const unsigned short*>(smem + H->o_bqd);
-    const unsigned* sinfo = reinterpret_cast<const unsigned*>(smem + H->o_sinfo);
-    const unsigned short* cpos = reinterpret_cast<const unsigned short*>(smem + H->o_const);
-    for (int i = tid; i < H->nConst; i += TILE_THREADS) A[cpos[i]] = 1.0;
+    V.rep = reinterpret_cast<const int*>(smem + H->o_rep);
+    V.dst = reinterpret_cast<const unsigned*>(smem + H->o_dst);
+    V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
+    V.bs = reinterpret_cast<const double*>(smem + H->o_bs);
+    V.bqd = reinterpret_cast<const unsigned short*>(smem + H->o_bqd);
+    const unsigned short* sround = reinterpret_cast<const unsigned short*>(smem + H->o_sround);
+    const unsigned short* sdst = reinterpret_cast<const unsigned short*>(smem + H->o_sdst);
+    const unsigned short* bround = reinterpret_cast<const unsigned short*>(smem + H->o_bround);
+    const unsigned short* bitem = reinterpret_cast<const unsigned short*>(smem + H->o_bitem);
+    {
+        const unsigned short* cpos = reinterpret_cast<const unsigned short*>(smem + H->o_const);
+        const unsigned short* nega = reinterpret_cast<const unsigned short*>(smem + H->o_nega);
+        for (int i = tid; i < H->nConst; i += TILE_THREADS) A[cpos[i]] = 1.0;
+        for (int i = tid; i < H->nNegA; i += TILE_THREADS) A[nega[i]] = -0.0;
+    }
     const int my_e = (warp ? H->nF : 0) + lane;
+    const bool any_a = need_j || need_h || need_c || need_f || need_g;
 
     // first record and its inputs
     if (tid < 8) cp_async16(reinterpret_cast<unsigned char*>(ctx) + 16 * tid,
@@ -471,94 +576,74 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
     cp_wait<0>();
     __syncthreads();
     EndIn pre;
-    load_end(P, ctx[0], V, my_e, need_h, pre);
-    issue_bus_gathers(P, ctx[0], H, smem, Gbuf, tid, need_h, need_c);
+    prefetch(P, ctx[0], V, my_e, tid, sG, need_h, need_c, pre);
     cp_commit();
 
     for (int ri = 0; ri < it.count; ++ri) {
         const DRec& R = ctx[ri & 1];
-        const double* Gb = Gbuf + (ri & 1) * gstride;
-        cp_wait<0>();
+        cp_wait<0>();          // this stage's gathers
         __syncthreads();
         const bool more = ri + 1 < it.count;
         if (more && tid < 8)
             cp_async16(reinterpret_cast<unsigned char*>(ctx + ((ri + 1) & 1)) + 16 * tid,
                        reinterpret_cast<const unsigned char*>(P.bus_recs + it.first + ri + 1) + 16 * tid);
         cp_commit();
-        const long long var_off = R.var_off, eq_row = R.eq_row;
+        const long long eq_row = R.eq_row;
         const int nb = R.nb;
-        // ---- A: branch ends (one side per warp), bus quantities ---------------
-        if (need_j || need_h || need_c || need_f) {
-            if (warp == 0) ends_phase<0>(P, R, V, lane, pre, A, need_j, need_h, need_c, need_f);
-            else ends_phase<1>(P, R, V, lane, pre, A, need_j, need_h, need_c, need_f);
+        // ---- A: branch ends (one side per warp), generator set-points ----------
+        if (any_a) {
+            if (warp == 0) ends_phase<0>(P, R, V, lane, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
+            else ends_phase<1>(P, R, V, lane, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
         }
-        for (int bl = tid; bl < nB; bl += TILE_THREADS) {
-            const int i = b0 + bl;
-            const double vmi = Gb[bl], gsi = Tgs[bl], bsi = Tbs[bl];
-            if (need_j) {
-                A[bqd[bl]] = (-2.0 * gsi) * vmi;
-                A[bqd[nB + bl]] = (2.0 * bsi) * vmi;
+        if (need_c) gens_phase(P, R, V, tid, G, sA);
+        if (any_a)
+            for (int k = tid; k < H->nOrph; k += TILE_THREADS) {     // buses without branches
+                const int rb = reinterpret_cast<const unsigned short*>(smem + H->o_orph)[k], i = b0 + rb;
+                const double* x = P.x + R.var_off;
+                const double* mu = P.mult + R.eq_row;
+                bus_terms(P, R, V, rb, __ldg(x + nb + i), need_h ? __ldg(mu + i) : 0.0,
+                          need_h ? __ldg(mu + nb + i) : 0.0, need_c ? __ldg(P.pd + R.pd_off + i) : 0.0,
+                          need_c ? __ldg(P.qd + R.pd_off + i) : 0.0, sA, need_j, need_h, need_c, need_f, need_g);
             }
-            if (need_h) A[bqd[2 * nB + bl]] = 2.0 * ((-Gb[nB + bl]) * gsi - (-Gb[2 * nB + bl]) * bsi);
-            if (need_g) {
-                P.grad[var_off + i] = R.w * 0.0;
-                P.grad[var_off + nb + i] = R.w * 0.0;
-            }
-        }
         cp_wait<0>();          // the next record
         __syncthreads();
-        // ---- B: balance rows (two threads per bus), next gathers, sums ----------
+        // the gather buffer is free again: prefetch the next stage's inputs
+        if (more) prefetch(P, ctx[(ri + 1) & 1], V, my_e, tid, sG, need_h, need_c, pre);
+        cp_commit();
+        // ---- B: balance rounds, next gathers, sum rounds -------------------------
         if (need_c || need_f) {
-            const double* Gg = Gb + GB * nB;
-            for (int k0 = 0; k0 < 2 * nB; k0 += TILE_THREADS) {
-                const int k = k0 + tid;
-                const bool on = k < 2 * nB;
-                const int bl = on ? k >> 1 : 0;
-                const bool qc = k & 1;
-                const int deg = on ? brun[nB + bl] : 0;
-                const int dmax = __reduce_max_sync(0xffffffffu, deg);
-                const double* run = A + brun[bl] + (qc ? deg : 0);
+            for (int r = warp; r < H->nRB; r += 2) {
+                const unsigned short* rd = bround + 4 * r;
+                const int base = rd[0], dmax = rd[1], gbase = rd[2], gmax = rd[3];
+                const unsigned item = bitem[32 * r + lane];
+                const bool on = item != 0xffffu;
+                const int bl = on ? (int)(item & 0x7fffu) : 0;
+                const int qc = (item >> 15) & 1;
+                const double* run = A + base + lane;
                 double p = 0.0;
-                for (int j = 0; j < dmax; ++j)
-                    if (j < deg) p = p + run[j];
-                const double vmi = Gb[bl];
-                const double sh = ((qc ? Tbs[bl] : Tgs[bl]) * vmi) * vmi;
-                p = p + (qc ? -sh : sh);
+#pragma unroll 4
+                for (int j = 0; j < dmax; ++j) p = p + run[32 * j];
                 const int i = b0 + bl;
                 if (on && need_f) P.inj[R.inj_off + (qc ? nb : 0) + i] = p;     // Engine.injections (acopf.py:252-264)
                 if (need_c) {
-                    double c = -(Gb[(qc ? 4 : 3) * nB + bl] + p);
-                    const int g0 = gptr[bl], g1 = on ? gptr[bl + 1] : g0;
-                    const int gmax = __reduce_max_sync(0xffffffffu, g1 - g0);
-                    const double* gq = Gg + (qc ? ngl : 0) + g0;
-                    for (int j = 0; j < gmax; ++j)
-                        if (j < g1 - g0) c = c + gq[j];
+                    double c = -(A[V.bqd[(5 + qc) * H->nB + bl]] + p);
+                    const double* gq = A + gbase + lane;
+#pragma unroll 2
+                    for (int j = 0; j < gmax; ++j) c = c + gq[32 * j];
                     if (on) P.cons[eq_row + (qc ? nb : 0) + i] = c;
                 }
             }
         }
-        if (more) {
-            const DRec& Rn = ctx[(ri + 1) & 1];
-            load_end(P, Rn, V, my_e, need_h, pre);
-            issue_bus_gathers(P, Rn, H, smem, Gbuf + ((ri + 1) & 1) * gstride, tid, need_h, need_c);
-        }
-        cp_commit();
         {
-            // sum entries are sorted by decreasing term count (within J and H):
-            // each warp round runs its longest count, predicated per lane
-            const int s0 = need_j ? 0 : H->nSumJ;
-            const int s1 = need_h ? H->nSumJ + H->nSumH : H->nSumJ;
-            for (int k0 = s0; k0 < s1; k0 += TILE_THREADS) {
-                const int k = k0 + tid;
-                const bool on = k < s1;
-                const unsigned info = on ? sinfo[2 * k] : 0u;
-                const double* run = A + (on ? sinfo[2 * k + 1] : (unsigned)H->tslot);
-                const int c = (int)(info >> 16);
-                const int cmax = __reduce_max_sync(0xffffffffu, c);
+            const int r0 = need_j ? 0 : H->nRJ;
+            const int r1 = need_h ? H->nRJ + H->nRH : H->nRJ;
+            for (int r = r0 + warp; r < r1; r += 2) {
+                const int base = sround[2 * r], cmax = sround[2 * r + 1];
+                const double* run = A + base + lane;
                 double v = run[0];
-                for (int j = 1; j < cmax; ++j)
-                    if (j < c) v = v + run[j];
-                if (on) A[info & 0xffffu] = v;
+#pragma unroll 4
+                for (int j = 1; j < cmax; ++j) v = v + run[32 * j];
+                A[sdst[32 * r + lane]] = v;
             }
         }
         __syncthreads();

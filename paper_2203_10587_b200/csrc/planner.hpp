@@ -40,7 +40,7 @@ constexpr int NQE = 15;         // quantities per branch end
 constexpr int Q_JP = 0;         // 0..3  -dP/d(VA_f, VA_t, VM_f, VM_t) of this end's P row
 constexpr int Q_JQ = 4;         // 4..7  same for the Q row
 constexpr int Q_H = 8;          // 8..14 Hessian values of the 7 positions this end owns (HSLOT_*)
-constexpr int NQB = 3;          // per bus: shunt J(P,VM), shunt J(Q,VM), shunt H(VM,VM)
+constexpr int NQB = 7;          // per bus: shunt J(P,VM), shunt J(Q,VM), shunt H(VM,VM), balance shunt P, Q, pd, qd
 
 // POSITIONS (acopf.py:48-49): (row-axis, col-axis) over (VA_f, VA_t, VM_f, VM_t)
 constexpr int POS_A[10] = {0, 0, 0, 0, 1, 1, 1, 2, 2, 3};
@@ -248,44 +248,51 @@ inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
 }
 
 // ---------------------------------------------------------------------------
-// Warp tiles (serialised into one device blob)
+// Tiles (serialised into one device blob)
 //
-// A tile is a run of consecutive buses with at most TILE_MAX_ENDS branch ends;
-// one warp evaluates it for a list of stages.  Its table (header + sections,
-// 16-byte aligned) is bulk-copied into the warp's shared memory once; after it
-// comes the warp's working "area" of doubles:
+// A tile is a run of consecutive buses with at most TILE_MAX_ENDS from-ends
+// and TILE_MAX_ENDS to-ends; one 64-thread CTA (a warp per side) evaluates it
+// for a list of stages.  Its table (header + sections, 16-byte aligned) is
+// bulk-copied into shared memory once; after it comes the working "area":
 //
 //   [0, T)           staging of the tile's four output segments
 //                    (J rows P_i | J rows Q_i | H rows VA_i | H rows VM_i),
 //                    copied out to global memory contiguously
-//   sum runs         one contiguous run per multi-term output entry, holding
-//                    its terms in scipy's summation order
-//   balance runs     per bus: the P flows, then the Q flows of its ends in
-//                    np.add.at order
-//   trash slot
+//   sum rounds       multi-term output entries in rounds of 32 (one per
+//                    lane, sorted by decreasing term count); term j of the
+//                    entry on lane l sits at round_base + 32 j + l, short
+//                    entries are padded with -0.0 (x + -0.0 == x for every x)
+//   balance rounds   the same for the P / Q balance rows: (bus, P|Q) items
+//                    by decreasing degree, term j = the j-th flow in
+//                    np.add.at order, then the shunt term; then the bus's
+//                    generator set-points
+//   pd, qd of every bus; trash slot
 //
 // Every term of every output entry is used exactly once (each end quantity
 // once, except the (tf,vf)/(tt,vt) Hessian position, which appears in both
 // the VA and the VM row of the end's bus), so every quantity is stored
 // straight to where its consumer reads it: the staging position of the
-// entry it alone makes up, or its place in a sum run.  Sums then read
-// contiguous slots with no index tables.
+// entry it alone makes up, or its place in a round.  The first end of every
+// bus (its "representative") also computes and stores the bus's shunt terms
+// and its loads, so no bus-level gathers are needed.
 
 constexpr int NST = 18;           // stores per end: 15 quantities, P flow, Q flow, second copy of quantity 13
 constexpr int ST_FP = 15, ST_FQ = 16, ST_X13 = 17;
+constexpr int NADM = 12;          // per end: gff bff gft bft gtf btf gtt btt, 2 gff, -2 bff, 2 gtt, -2 btt
 
-struct TileHdr {                      // 144 bytes; section offsets in bytes from the header start
+struct TileHdr {                      // 160 bytes; section offsets in bytes from the header start
     int32_t b0, nB, nE, nF;           // first bus, buses, ends, from-ends (ends [0,nF) are from-ends)
     int32_t L[4];                     // entries of the four row segments
-    int32_t nArea, nSumJ, nSumH, nConst;
-    int32_t bytes, tslot, ngl, pad1;  // serialised size; trash slot; generators of the tile's buses
+    int32_t nArea, nRJ, nRH, nRB;     // area doubles; sum rounds (J, H); balance rounds
+    int32_t bytes, tslot, ngl, pad0;  // serialised size; trash slot; generators
+    int32_t nConst, nNegA, nOrph, o_orph;   // constants, -0.0 paddings, buses without branches
     int32_t o_adm, o_f, o_t, o_ridx;
     int32_t o_foff, o_code, o_dst, o_gs;
-    int32_t o_bs, o_brun, o_gptr, o_glist;
-    int32_t o_bqd, o_sinfo, o_const, pad2;
-    int32_t pad3[4];
+    int32_t o_bs, o_glist, o_gdst, o_bqd;
+    int32_t o_sround, o_sdst, o_bround, o_bitem;
+    int32_t o_const, o_nega, o_rep, pad3;
 };
-static_assert(sizeof(TileHdr) == 144, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 160, "TileHdr layout");
 
 struct TileTable {
     int topo = 0;
@@ -298,13 +305,19 @@ struct TileTable {
     std::vector<int> cols;        // stage-local column per entry (pattern export)
     std::vector<int> rowlen;      // entries per row, 4 segments x nB rows
     // locations
-    int nArea = 0, tslot = 0, ngl = 0;   // area doubles, trash slot, generators of the tile's buses
-    std::vector<uint16_t> dst;    // NST x nE (SoA): where each end store goes
-    std::vector<uint16_t> brun;   // 2 x nB: balance P-run start, degree (Q run follows the P run)
+    int nArea = 0, tslot = 0, ngl = 0;
+    std::vector<uint16_t> dst;    // NST x nE (SoA): where each end store goes (area slot)
     std::vector<uint16_t> bqd;    // NQB x nB (SoA): location of each bus quantity
-    std::vector<uint32_t> sinfo;  // per sum entry: (dst | count << 16, run start); J sums then H sums
-    int nSumJ = 0, nSumH = 0;
-    std::vector<uint16_t> cpos;   // slots holding the constant 1.0
+    std::vector<uint16_t> sround; // per sum round: base, term count; J rounds then H rounds
+    std::vector<uint16_t> sdst;   // per sum round: 32 staging destinations
+    int nRJ = 0, nRH = 0;
+    std::vector<uint16_t> bround; // per balance round: base, degree, gen base, gen count
+    std::vector<uint16_t> bitem;  // per balance round: 32 x (bus | Q << 15), 0xffff = none
+    std::vector<uint16_t> gdst;   // 2 x ngl: gen-round slot of each generator's Pg, Qg
+    std::vector<uint16_t> cpos;   // area slots holding the constant 1.0
+    std::vector<uint16_t> nega;   // area slots holding -0.0 (round padding)
+    std::vector<int> rep;         // per end: its bus (tile-local) if it is the bus's first end, else -1
+    std::vector<uint16_t> orph;   // buses without branch ends (tile-local)
     void serialise(const Topo& T, std::vector<uint8_t>& blob) const;
 };
 
@@ -313,7 +326,7 @@ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) const {
     const int nE = (int)ends.size();
     std::vector<int> f(nE), t(nE), ridx(nE), foff(nE), code(nE), glist;
-    std::vector<double> adm(8 * (size_t)nE), gs(nB), bs(nB);
+    std::vector<double> adm(NADM * (size_t)nE), gs(nB), bs(nB);
     for (int e = 0; e < nE; ++e) {
         int k = ends[e] >> 1;
         f[e] = T.fo[k];
@@ -321,22 +334,26 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
         ridx[e] = T.ridx[k];
         foff[e] = T.ridx[k] >= 0 ? (int)T.foff[T.ridx[k]] : 0;
         code[e] = ends[e];
-        for (int q = 0; q < 8; ++q) adm[(size_t)q * nE + e] = T.adm[8 * (size_t)k + q];
+        const double* a = &T.adm[8 * (size_t)k];
+        for (int q = 0; q < 8; ++q) adm[(size_t)q * nE + e] = a[q];
+        adm[(size_t)8 * nE + e] = 2.0 * a[0];      // exact scalings (acopf.py:243-246, 318-319)
+        adm[(size_t)9 * nE + e] = -2.0 * a[1];
+        adm[(size_t)10 * nE + e] = 2.0 * a[6];
+        adm[(size_t)11 * nE + e] = -2.0 * a[7];
     }
-    std::vector<uint16_t> gptr(1, 0);
     for (int bl = 0; bl < nB; ++bl) {
         int i = b0 + bl;
         gs[bl] = T.gs[i];
         bs[bl] = T.bs[i];
         for (int p = T.gen_ptr[i]; p < T.gen_ptr[i + 1]; ++p) glist.push_back(T.gen_list[p]);
-        gptr.push_back((uint16_t)glist.size());
     }
     TileHdr h{};
     h.b0 = b0; h.nB = nB; h.nE = nE; h.nF = nF;
     for (int s = 0; s < 4; ++s) h.L[s] = L[s];
-    h.nArea = nArea; h.nSumJ = nSumJ; h.nSumH = nSumH; h.nConst = (int)cpos.size();
+    h.nArea = nArea; h.nRJ = nRJ; h.nRH = nRH; h.nRB = (int)bround.size() / 4;
     h.tslot = tslot;
     h.ngl = (int)glist.size();
+    h.nConst = (int)cpos.size(); h.nNegA = (int)nega.size(); h.nOrph = (int)orph.size();
     size_t off = sizeof(TileHdr);
     auto take = [&](size_t n) { int o = (int)off; off = align16(off + n); return o; };
     h.o_adm = take(8 * adm.size());
@@ -345,15 +362,20 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     h.o_ridx = take(4 * (size_t)nE);
     h.o_foff = take(4 * (size_t)nE);
     h.o_code = take(4 * (size_t)nE);
-    h.o_dst = take(2 * dst.size());
+    h.o_dst = take(4 * 9 * (size_t)nE);
     h.o_gs = take(8 * (size_t)nB);
     h.o_bs = take(8 * (size_t)nB);
-    h.o_brun = take(2 * brun.size());
-    h.o_gptr = take(2 * gptr.size());
     h.o_glist = take(4 * glist.size());
+    h.o_gdst = take(2 * gdst.size());
     h.o_bqd = take(2 * bqd.size());
-    h.o_sinfo = take(4 * sinfo.size());
+    h.o_sround = take(2 * sround.size());
+    h.o_sdst = take(2 * sdst.size());
+    h.o_bround = take(2 * bround.size());
+    h.o_bitem = take(2 * bitem.size());
     h.o_const = take(2 * cpos.size());
+    h.o_nega = take(2 * nega.size());
+    h.o_rep = take(4 * rep.size());
+    h.o_orph = take(2 * orph.size());
     h.bytes = (int)off;
     size_t base = blob.size();
     blob.resize(base + off, 0);
@@ -366,15 +388,27 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     put(h.o_ridx, ridx.data(), 4 * (size_t)nE);
     put(h.o_foff, foff.data(), 4 * (size_t)nE);
     put(h.o_code, code.data(), 4 * (size_t)nE);
-    put(h.o_dst, dst.data(), 2 * dst.size());
+    {   // per end: 9 words of two byte offsets into the area (stores 2k, 2k+1)
+        std::vector<uint32_t> dw(9 * (size_t)nE);
+        for (int e = 0; e < nE; ++e)
+            for (int k = 0; k < 9; ++k)
+                dw[9 * (size_t)e + k] = (uint32_t)(8 * dst[(size_t)(2 * k) * nE + e]) |
+                                        ((uint32_t)(8 * dst[(size_t)(2 * k + 1) * nE + e]) << 16);
+        put(h.o_dst, dw.data(), 4 * dw.size());
+    }
     put(h.o_gs, gs.data(), 8 * (size_t)nB);
     put(h.o_bs, bs.data(), 8 * (size_t)nB);
-    put(h.o_brun, brun.data(), 2 * brun.size());
-    put(h.o_gptr, gptr.data(), 2 * gptr.size());
     put(h.o_glist, glist.data(), 4 * glist.size());
+    put(h.o_gdst, gdst.data(), 2 * gdst.size());
     put(h.o_bqd, bqd.data(), 2 * bqd.size());
-    put(h.o_sinfo, sinfo.data(), 4 * sinfo.size());
+    put(h.o_sround, sround.data(), 2 * sround.size());
+    put(h.o_sdst, sdst.data(), 2 * sdst.size());
+    put(h.o_bround, bround.data(), 2 * bround.size());
+    put(h.o_bitem, bitem.data(), 2 * bitem.size());
     put(h.o_const, cpos.data(), 2 * cpos.size());
+    put(h.o_nega, nega.data(), 2 * nega.size());
+    put(h.o_rep, rep.data(), 4 * rep.size());
+    put(h.o_orph, orph.data(), 2 * orph.size());
 }
 
 inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
@@ -420,7 +454,7 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         }
     // locations: each term use gets one slot; -1 = not yet placed
     std::vector<int> loc_e((size_t)NST * nE, -1), loc_b((size_t)NQB * nB, -1);
-    std::vector<int> cpos;
+    std::vector<int> cpos, nega;
     auto place = [&](const Sym& y, int slot) {
         if (y.kind == 2) { cpos.push_back(slot); return; }
         if (y.kind == 1) {
@@ -436,7 +470,7 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         if (y.q != Q_H + 5 || l2 >= 0) throw std::runtime_error("planner: unexpected reuse of an end quantity");
         l2 = slot;
     };
-    struct Sum { int dst; int row, entry; };
+    struct Sum { int dst; int row, entry, n; };
     std::vector<Sum> sums[2];
     int pos = 0;
     for (int s = 0; s < 4; ++s)
@@ -445,43 +479,103 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             for (size_t e = 0; e < row.cols.size(); ++e, ++pos) {
                 const int n = row.tptr[e + 1] - row.tptr[e];
                 if (n == 1) place(row.terms[row.tptr[e]], pos);
-                else sums[s / 2].push_back(Sum{pos, s * nB + r, (int)e});
+                else sums[s / 2].push_back(Sum{pos, s * nB + r, (int)e, n});
             }
         }
     int next = pos;
-    for (int c = 0; c < 2; ++c) {
-        std::stable_sort(sums[c].begin(), sums[c].end(), [&](const Sum& x, const Sum& y) {
-            const Row& rx = rows[x.row];
-            const Row& ry = rows[y.row];
-            return rx.tptr[x.entry + 1] - rx.tptr[x.entry] > ry.tptr[y.entry + 1] - ry.tptr[y.entry];
-        });
-        for (const Sum& sm : sums[c]) {
-            const Row& row = rows[sm.row];
-            const int n = row.tptr[sm.entry + 1] - row.tptr[sm.entry];
-            tt.sinfo.push_back((uint32_t)sm.dst | ((uint32_t)n << 16));
-            tt.sinfo.push_back((uint32_t)next);
-            for (int t = row.tptr[sm.entry]; t < row.tptr[sm.entry + 1]; ++t) place(row.terms[t], next++);
-        }
-        (c == 0 ? tt.nSumJ : tt.nSumH) = (int)sums[c].size();
-    }
-    // balance runs: per bus its P flows then its Q flows, in np.add.at order
-    tt.brun.assign(2 * (size_t)nB, 0);
-    for (int bl = 0; bl < nB; ++bl) {
-        const int deg = tt.busptr[bl + 1] - tt.busptr[bl];
-        tt.brun[bl] = (uint16_t)next;
-        tt.brun[nB + bl] = (uint16_t)deg;
-        for (int j = 0; j < deg; ++j) {
-            const int e = tt.bend[tt.busptr[bl] + j];
-            loc_e[(size_t)ST_FP * nE + e] = next + j;
-            loc_e[(size_t)ST_FQ * nE + e] = next + deg + j;
-        }
-        next += 2 * deg;
-    }
-    for (int i = b0; i < b1; ++i) tt.ngl += T.gen_ptr[i + 1] - T.gen_ptr[i];
     tt.tslot = next++;
+    for (int c = 0; c < 2; ++c) {
+        std::stable_sort(sums[c].begin(), sums[c].end(), [](const Sum& x, const Sum& y) { return x.n > y.n; });
+        const int nr = ((int)sums[c].size() + 31) / 32;
+        for (int r = 0; r < nr; ++r) {
+            int cmax = 0;
+            for (int l = 0; l < 32 && 32 * r + l < (int)sums[c].size(); ++l) cmax = std::max(cmax, sums[c][32 * r + l].n);
+            const int base = next;
+            next += 32 * cmax;
+            tt.sround.push_back((uint16_t)base);
+            tt.sround.push_back((uint16_t)cmax);
+            for (int l = 0; l < 32; ++l) {
+                const int k = 32 * r + l;
+                if (k >= (int)sums[c].size()) {
+                    tt.sdst.push_back((uint16_t)tt.tslot);
+                    for (int j = 0; j < cmax; ++j) nega.push_back(base + 32 * j + l);
+                    continue;
+                }
+                const Sum& sm = sums[c][k];
+                const Row& row = rows[sm.row];
+                tt.sdst.push_back((uint16_t)sm.dst);
+                for (int j = 0; j < cmax; ++j) {
+                    if (j < sm.n) place(row.terms[row.tptr[sm.entry] + j], base + 32 * j + l);
+                    else nega.push_back(base + 32 * j + l);
+                }
+            }
+        }
+        (c == 0 ? tt.nRJ : tt.nRH) = nr;
+    }
+    // balance rounds: (bus, P|Q) items by decreasing degree; a run holds the
+    // bus's flows in np.add.at order, then its shunt term; the generators'
+    // Pg (Qg) follow in the gen rounds
+    for (int i = b0; i < b1; ++i) tt.ngl += T.gen_ptr[i + 1] - T.gen_ptr[i];
+    std::vector<int> gfirst(nB + 1, 0);
+    for (int bl = 0; bl < nB; ++bl) gfirst[bl + 1] = gfirst[bl] + T.gen_ptr[b0 + bl + 1] - T.gen_ptr[b0 + bl];
+    std::vector<int> items;
+    for (int bl = 0; bl < nB; ++bl) { items.push_back(2 * bl); items.push_back(2 * bl + 1); }
+    auto deg = [&](int it) { return tt.busptr[(it >> 1) + 1] - tt.busptr[it >> 1]; };
+    std::stable_sort(items.begin(), items.end(), [&](int x, int y) { return deg(x) > deg(y); });
+    tt.gdst.assign(2 * (size_t)tt.ngl, 0);
+    for (int r = 0; r < ((int)items.size() + 31) / 32; ++r) {
+        int dmax = 0, gmax = 0;
+        for (int l = 0; l < 32 && 32 * r + l < (int)items.size(); ++l) {
+            const int it = items[32 * r + l];
+            dmax = std::max(dmax, deg(it) + 1);
+            gmax = std::max(gmax, gfirst[(it >> 1) + 1] - gfirst[it >> 1]);
+        }
+        const int base = next;
+        next += 32 * dmax;
+        const int gbase = next;
+        next += 32 * gmax;
+        tt.bround.push_back((uint16_t)base);
+        tt.bround.push_back((uint16_t)dmax);
+        tt.bround.push_back((uint16_t)gbase);
+        tt.bround.push_back((uint16_t)gmax);
+        for (int l = 0; l < 32; ++l) {
+            const int k = 32 * r + l;
+            if (k >= (int)items.size()) {
+                tt.bitem.push_back(0xffff);
+                for (int j = 0; j < dmax; ++j) nega.push_back(base + 32 * j + l);
+                for (int j = 0; j < gmax; ++j) nega.push_back(gbase + 32 * j + l);
+                continue;
+            }
+            const int it = items[k], bl = it >> 1, qc = it & 1;
+            tt.bitem.push_back((uint16_t)(bl | (qc << 15)));
+            const int d = deg(it);
+            for (int j = 0; j < dmax; ++j) {
+                if (j < d) loc_e[(size_t)(qc ? ST_FQ : ST_FP) * nE + tt.bend[tt.busptr[bl] + j]] = base + 32 * j + l;
+                else if (j == d) loc_b[(size_t)(3 + qc) * nB + bl] = base + 32 * j + l;
+                else nega.push_back(base + 32 * j + l);
+            }
+            const int ng = gfirst[bl + 1] - gfirst[bl];
+            for (int j = 0; j < gmax; ++j) {
+                if (j < ng) tt.gdst[(size_t)qc * tt.ngl + gfirst[bl] + j] = (uint16_t)(gbase + 32 * j + l);
+                else nega.push_back(gbase + 32 * j + l);
+            }
+        }
+    }
+    // pd, qd of every bus; the representative (first) end of every bus
+    for (int bl = 0; bl < nB; ++bl) {
+        loc_b[(size_t)5 * nB + bl] = next++;
+        loc_b[(size_t)6 * nB + bl] = next++;
+    }
+    tt.rep.assign(nE, -1);
+    for (int bl = 0; bl < nB; ++bl) {
+        if (tt.busptr[bl + 1] == tt.busptr[bl]) tt.orph.push_back((uint16_t)bl);
+        else tt.rep[tt.bend[tt.busptr[bl]]] = bl;
+    }
     tt.nArea = next;
-    if (tt.nArea > 65535) throw std::runtime_error("tile working area exceeds 16-bit slots");
+    if (tt.nArea >= 8192) throw std::runtime_error("tile working area exceeds 64 KB");
+    if (nB >= 0x8000) throw std::runtime_error("tile has too many buses");
     for (int v : cpos) tt.cpos.push_back((uint16_t)v);
+    for (int v : nega) tt.nega.push_back((uint16_t)v);
     tt.dst.resize(loc_e.size());
     for (size_t i = 0; i < loc_e.size(); ++i) tt.dst[i] = (uint16_t)(loc_e[i] < 0 ? tt.tslot : loc_e[i]);
     tt.bqd.resize(loc_b.size());

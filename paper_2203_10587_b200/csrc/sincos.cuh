@@ -144,14 +144,14 @@ SC_HD void acc_sincos(double x, double* sp, double* cp) {
 
 SC_HD void libm_sincos(double x, double* sp, double* cp) {
     const double ax = fabs(x);
-    if (!(ax < 0.85546875)) {            // outside the table scheme (and inf / nan)
-        acc_sincos(x, sp, cp);
-        return;
-    }
-    // table entry k = round(128 |x|) and remainder, exactly as big + |x| rounds
-    const double u = GL_BIG + ax;
+    const bool core = ax < 0.85546875;
+    // branch-free table scheme (an out-of-range or NaN argument evaluates it
+    // on 0.0 and takes the fallback below): table entry k = round(128 |x|)
+    // and remainder, exactly as big + |x| rounds
+    const double axs = core ? ax : 0.0;
+    const double u = GL_BIG + axs;
     const double xk = u - GL_BIG;
-    const double xr = ax - xk;
+    const double xr = axs - xk;
     const int k = (int)(xk * 128.0);
 #ifdef __CUDA_ARCH__
     const double* tab = sc_gl_table_dev + 4 * k;
@@ -162,25 +162,23 @@ SC_HD void libm_sincos(double x, double* sp, double* cp) {
     const double xx = xr * xr;
     const double ps = fma(xx, GL_SN5, GL_SN3);
     const double pc = xx * fma(xx, fma(xx, GL_CS6, GL_CS4), GL_CS2);
-    // cos
-    if (ax < 7.450580596923828e-09) {
-        *cp = 1.0;
-    } else {
-        const double s = fma(xr * xx, ps, xr);
-        const double cor = fma(-sn, s, fma(-cs, pc, fma(-s, ssn, ccs)));
-        *cp = cs + cor;
-    }
-    // sin
-    if (ax < 1.4901161193847656e-08) {
-        *sp = x;
-    } else if (ax < 0.126) {
-        const double a2 = x * x;
-        const double p = fma(fma(fma(fma(GL_S5, a2, GL_S4), a2, GL_S3), a2, GL_S2), a2, GL_S1);
-        *sp = x + (p * x) * a2;
-    } else {
-        const double s = xr + fma(xr * xx, ps, 0.0);
-        const double c = fma(xr, 0.0, pc);
-        const double cor = fma(cs, s, fma(-sn, c, fma(s, ccs, ssn)));
-        *sp = copysign(sn + cor, x);
+    // cos: 1 below 2^-27, else the table scheme
+    const double s1 = fma(xr * xx, ps, xr);
+    const double cor1 = fma(-sn, s1, fma(-cs, pc, fma(-s1, ssn, ccs)));
+    const double c = ax < 7.450580596923828e-09 ? 1.0 : cs + cor1;
+    // sin: x below 2^-26, the odd polynomial below 0.126, else the table scheme
+    const double a2 = x * x;
+    const double p = fma(fma(fma(fma(GL_S5, a2, GL_S4), a2, GL_S3), a2, GL_S2), a2, GL_S1);
+    const double s_small = x + (p * x) * a2;
+    const double s2 = xr + fma(xr * xx, ps, 0.0);
+    const double c2 = fma(xr, 0.0, pc);
+    const double cor2 = fma(cs, s2, fma(-sn, c2, fma(s2, ccs, ssn)));
+    const double s_tab = copysign(sn + cor2, x);
+    const double s = ax < 1.4901161193847656e-08 ? x : (ax < 0.126 ? s_small : s_tab);
+    if (core) {
+        *sp = s;
+        *cp = c;
+    } else {                           // outside the table scheme (and inf / nan)
+        acc_sincos(x, sp, cp);
     }
 }

@@ -1,2 +1,2 @@
-S = "[('hval','eval_kernel.cuh',117,140),('gath_end','eval_kernel.cuh',166,218),('gath_bus','eval_kernel.cuh',221,262),('A_end','eval_kernel.cuh',263,375),('copyfn','eval_kernel.cuh',376,408),('setup','eval_kernel.cuh',409,489),('A','eval_kernel.cuh',490,509),('B','eval_kernel.cuh',510,545),('sums','eval_kernel.cuh',546,564),('C','eval_kernel.cuh',565,582)]"
+S = "[('hval','eval_kernel.cuh',117,138),('prefetch','eval_kernel.cuh',159,266),('bus_terms','eval_kernel.cuh',267,311),('A_end','eval_kernel.cuh',312,439),('gens','eval_kernel.cuh',440,460),('copyfn','eval_kernel.cuh',461,505),('setup','eval_kernel.cuh',506,592),('A','eval_kernel.cuh',593,612),('B','eval_kernel.cuh',613,649),('C','eval_kernel.cuh',650,667)]"
 print(S)
