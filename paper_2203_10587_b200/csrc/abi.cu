@@ -531,7 +531,8 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         P.obj = obj; P.grad = grad; P.cons = cons; P.jval = jval; P.hval = hval;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
         const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD)) && P.n_bus_items > 0;
-        const bool aux = (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
+        static const bool no_aux = getenv("ACOPF_EXP_NO_AUX") != nullptr;   // development aid: tile kernel alone
+        const bool aux = !no_aux && (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
         // the generator/coupling kernel runs concurrently on a forked stream
         const bool fork = aux && bus;
         if (fork) {

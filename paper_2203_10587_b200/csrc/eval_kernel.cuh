@@ -556,6 +556,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
     V.gs = reinterpret_cast<const double*>(smem + H->o_gs);
     V.bs = reinterpret_cast<const double*>(smem + H->o_bs);
     V.bqd = reinterpret_cast<const unsigned short*>(smem + H->o_bqd);
+
     const unsigned short* sround = reinterpret_cast<const unsigned short*>(smem + H->o_sround);
     const unsigned short* sdst = reinterpret_cast<const unsigned short*>(smem + H->o_sdst);
     const unsigned short* bround = reinterpret_cast<const unsigned short*>(smem + H->o_bround);
@@ -635,15 +636,28 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
             }
         }
         {
+            // each warp takes rounds r and r + 2 together (two independent
+            // chains per lane)
             const int r0 = need_j ? 0 : H->nRJ;
             const int r1 = need_h ? H->nRJ + H->nRH : H->nRJ;
-            for (int r = r0 + warp; r < r1; r += 2) {
-                const int base = sround[2 * r], cmax = sround[2 * r + 1];
-                const double* run = A + base + lane;
-                double v = run[0];
-#pragma unroll 4
-                for (int j = 1; j < cmax; ++j) v = v + run[32 * j];
-                A[sdst[32 * r + lane]] = v;
+            for (int r = r0 + warp; r < r1; r += 4) {
+                const bool two = r + 2 < r1;
+                const int rb = two ? r + 2 : r;
+                const int ca = sround[2 * r + 1], cb = two ? sround[2 * rb + 1] : 0;
+                const double* ra = A + sround[2 * r] + lane;
+                const double* rbp = A + sround[2 * rb] + lane;
+                double va = ra[0], vb = rbp[0];
+                const int cm = ca < cb ? ca : cb;
+                int j = 1;
+#pragma unroll 2
+                for (; j < cm; ++j) {
+                    va = va + ra[32 * j];
+                    vb = vb + rbp[32 * j];
+                }
+                for (int k = j; k < ca; ++k) va = va + ra[32 * k];
+                for (int k = j; k < cb; ++k) vb = vb + rbp[32 * k];
+                A[sdst[32 * r + lane]] = va;
+                if (two) A[sdst[32 * rb + lane]] = vb;
             }
         }
         __syncthreads();

@@ -142,7 +142,9 @@ SC_HD void acc_sincos(double x, double* sp, double* cp) {
 #define GL_S5 (-0x1.addffc2fcdf59p-26)
 #define GL_BIG 52776558133248.0
 
-SC_HD void libm_sincos(double x, double* sp, double* cp) {
+// table: sc_gl_table_* (SC_GL_NK entries of sin hi, sin lo, cos hi, cos lo),
+// or a copy of it (the tile kernel keeps one in shared memory)
+SC_HD void libm_sincos_t(const double* table, double x, double* sp, double* cp) {
     const double ax = fabs(x);
     const bool core = ax < 0.85546875;
     // branch-free table scheme (an out-of-range or NaN argument evaluates it
@@ -153,11 +155,7 @@ SC_HD void libm_sincos(double x, double* sp, double* cp) {
     const double xk = u - GL_BIG;
     const double xr = axs - xk;
     const int k = (int)(xk * 128.0);
-#ifdef __CUDA_ARCH__
-    const double* tab = sc_gl_table_dev + 4 * k;
-#else
-    const double* tab = sc_gl_table_host + 4 * k;
-#endif
+    const double* tab = table + 4 * k;
     const double sn = tab[0], ssn = tab[1], cs = tab[2], ccs = tab[3];
     const double xx = xr * xr;
     const double ps = fma(xx, GL_SN5, GL_SN3);
@@ -181,4 +179,12 @@ SC_HD void libm_sincos(double x, double* sp, double* cp) {
     } else {                           // outside the table scheme (and inf / nan)
         acc_sincos(x, sp, cp);
     }
+}
+
+SC_HD void libm_sincos(double x, double* sp, double* cp) {
+#ifdef __CUDA_ARCH__
+    libm_sincos_t(sc_gl_table_dev, x, sp, cp);
+#else
+    libm_sincos_t(sc_gl_table_host, x, sp, cp);
+#endif
 }

@@ -12,7 +12,7 @@ x = torch.from_numpy(run.x_h).cuda(); m = torch.from_numpy(run.m_h).cuda()
 out = ev.alloc()
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
 res = {}
-for name, what in [("ALL", L.ALL), ("CONS", L.CONS), ("JAC", L.JAC), ("HESS", L.HESS), ("OBJ+GRAD", L.OBJ | L.GRAD),
+for name, what in [("ALL", L.ALL), ("CONS", L.CONS), ("JAC", L.JAC), ("HESS", L.HESS), ("OBJ+GRAD", L.OBJ | L.GRAD), ("OBJ", L.OBJ), ("GRAD", L.GRAD),
                    ("CONS+JAC", L.CONS | L.JAC)]:
     for _ in range(3): ev.eval_device(x, m, 1.0, what, out=out, stream=s.cuda_stream)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
