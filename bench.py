@@ -400,7 +400,9 @@ def main():
             "config": cfg,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "acopf_eval_kernel", "kernel_ms": kernel_ms},
+                         "kernel": "acopf_tile_kernel (one launch per step; the generator/objective kernel "
+                                   "runs concurrently on a forked stream and is included in kernel_ms)",
+                         "kernel_ms": kernel_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(gpu_launches),

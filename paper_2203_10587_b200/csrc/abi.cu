@@ -187,8 +187,17 @@ static void upload(acopf_batch* b) {
     // stages; about 4 warps' worth of items per resident warp slot
     int64_t total_recs = 0;
     for (const StageInfo& st : b->stages) total_recs += (int64_t)st.table.size();
+    // stages per item: enough items to fill the GPU a few times over, and few
+    // enough that the inputs (x, multipliers) of the stage groups in flight stay
+    // L2-resident (ACOPF_L2_INPUT_MB per group; gathers otherwise re-read HBM)
     const int64_t target_items = 148LL * (WARP_MINB / 2) * 4;
-    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(64, total_recs / target_items));
+    double in_bytes = 0.0;
+    for (const StageInfo& st : b->stages) in_bytes += 8.0 * (double)(st.n + st.m_eq + st.m_ineq);
+    const double per_stage = in_bytes / std::max(1, S);
+    const char* l2env = getenv("ACOPF_L2_INPUT_MB");
+    const double l2_budget = (l2env ? atof(l2env) : 8.0) * 1048576.0;
+    const int64_t g_l2 = std::max<int64_t>(1, (int64_t)(l2_budget / std::max(1.0, per_stage)));
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>({64, total_recs / target_items, g_l2}));
     std::vector<DBusItem> items;
     std::vector<DRec> recs;
     size_t max_smem = 0;
