@@ -49,6 +49,7 @@ _SIGNATURES = {
     "acopf_batch_pattern": (c_int32, [c_void_p, c_int32, c_int32, c_int64, _i64p, _i32p]),
     "acopf_batch_launches": (c_int64, [c_void_p]),
     "acopf_canonical_order": (c_int32, [c_int64, _i32p, _i32p]),
+    "acopf_batch_verify": (c_int32, [c_void_p, _i64p]),
 }
 
 

@@ -773,6 +773,30 @@ int acopf_batch_pattern(const acopf_batch* b, int32_t stage, int32_t which, int6
 
 int64_t acopf_batch_launches(const acopf_batch* b) { return b ? b->launches : 0; }
 
+int acopf_batch_verify(const acopf_batch* b, int64_t* stats) {
+    return guard([&] {
+        int64_t ntiles = 0, nends = 0, area = 0, pads = 0, smem = 0;
+        for (size_t ti = 0; ti < b->topos.size(); ++ti) {
+            ntiles += (int64_t)b->base_table[ti].size();
+            for (int id : b->base_table[ti]) nends += (int64_t)b->tables[id].ends.size();
+        }
+        for (size_t i = 0; i < b->tables.size(); ++i) {
+            const TileTable& tt = b->tables[i];
+            const std::string err = verify_tile(tt);
+            if (!err.empty()) throw std::runtime_error("table " + std::to_string(i) + ": " + err);
+            std::vector<uint8_t> blob;
+            tt.serialise(*b->topos[tt.topo], blob);
+            area += tt.nArea;
+            pads += (int64_t)tt.nega.size();
+            smem = std::max<int64_t>(smem, (int64_t)tile_smem_bytes((int)blob.size(), tt.nArea));
+        }
+        if (stats) {
+            stats[0] = (int64_t)b->tables.size(); stats[1] = ntiles; stats[2] = nends;
+            stats[3] = area; stats[4] = pads; stats[5] = smem;
+        }
+    });
+}
+
 int acopf_canonical_order(int64_t n, const int32_t* cols, int32_t* perm) {
     return guard([&] {
         std::vector<std::pair<int, Sym>> coo(n);

@@ -583,4 +583,72 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     return tt;
 }
 
+// Planner invariants of one tile table (host check, used by acopf_batch_verify):
+// every staging position and every round term slot has exactly one producer,
+// paddings are separate from producers, and all locations are in the area.
+inline std::string verify_tile(const TileTable& tt) {
+    const int nE = (int)tt.ends.size(), nB = tt.nB;
+    const int T = tt.L[0] + tt.L[1] + tt.L[2] + tt.L[3];
+    std::vector<int> prod(tt.nArea, 0), pad(tt.nArea, 0), read(tt.nArea, 0);
+    auto slot_ok = [&](int v) { return v >= 0 && v < tt.nArea; };
+    if ((int)tt.dst.size() != NST * nE || (int)tt.bqd.size() != NQB * nB) return "store tables have the wrong size";
+    for (int e = 0; e < nE; ++e)
+        for (int q = 0; q < NST; ++q) {
+            const int v = tt.dst[(size_t)q * nE + e];
+            if (!slot_ok(v)) return "end store outside the area";
+            if (v != tt.tslot) prod[v]++;
+        }
+    for (int v : tt.bqd) {
+        if (!slot_ok(v)) return "bus store outside the area";
+        if (v != tt.tslot) prod[v]++;
+    }
+    for (int v : tt.cpos) {
+        if (!slot_ok(v)) return "constant outside the area";
+        prod[v]++;
+    }
+    for (int v : tt.nega) {
+        if (!slot_ok(v)) return "padding outside the area";
+        pad[v]++;
+    }
+    for (int v : tt.gdst) {
+        if (!slot_ok(v)) return "generator store outside the area";
+        prod[v]++;
+    }
+    const int nR = tt.nRJ + tt.nRH;
+    if ((int)tt.sround.size() != 2 * nR || (int)tt.sdst.size() != 32 * nR) return "sum round tables have the wrong size";
+    for (int r = 0; r < nR; ++r) {
+        const int base = tt.sround[2 * r], c = tt.sround[2 * r + 1];
+        for (int l = 0; l < 32; ++l) {
+            const int d = tt.sdst[32 * r + l];
+            if (!slot_ok(d)) return "sum destination outside the area";
+            if (d != tt.tslot) {
+                if (d >= T) return "sum destination outside the staging segments";
+                prod[d]++;
+            }
+            for (int j = 0; j < c; ++j) {
+                const int v = base + 32 * j + l;
+                if (!slot_ok(v)) return "sum round outside the area";
+                read[v]++;
+            }
+        }
+    }
+    const int nRB = (int)tt.bround.size() / 4;
+    for (int r = 0; r < nRB; ++r) {
+        const int base = tt.bround[4 * r], d = tt.bround[4 * r + 1], gb = tt.bround[4 * r + 2], g = tt.bround[4 * r + 3];
+        for (int l = 0; l < 32; ++l) {
+            for (int j = 0; j < d; ++j) { if (!slot_ok(base + 32 * j + l)) return "balance round outside the area"; read[base + 32 * j + l]++; }
+            for (int j = 0; j < g; ++j) { if (!slot_ok(gb + 32 * j + l)) return "generator round outside the area"; read[gb + 32 * j + l]++; }
+        }
+    }
+    for (int v = 0; v < tt.nArea; ++v) {
+        if (v == tt.tslot) continue;
+        if (prod[v] > 1) return "area slot with more than one producer";
+        if (pad[v] && (prod[v] || pad[v] > 1)) return "padding slot also produced";
+        if (v < T && prod[v] + pad[v] != 1) return "staging position without exactly one producer";
+        if (read[v] > 1) return "round slot read twice";
+        if (read[v] && prod[v] + pad[v] != 1) return "round slot without exactly one producer or padding";
+    }
+    return "";
+}
+
 }  // namespace acopf

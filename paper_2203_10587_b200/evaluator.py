@@ -279,6 +279,13 @@ class BatchEvaluator:
     def launches(self) -> int:
         return int(L.lib().acopf_batch_launches(self._h))
 
+    def verify_plan(self) -> dict:
+        """Host check of the tile tables' invariants (acopf_batch_verify); no GPU needed."""
+        st = np.zeros(6, dtype=np.int64)
+        L.check(L.lib().acopf_batch_verify(self._h, L.ptr(st, ctypes.c_int64)))
+        keys = ("tables", "tiles", "ends", "area_doubles", "pad_slots", "max_smem_bytes")
+        return dict(zip(keys, (int(v) for v in st)))
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None:

@@ -154,3 +154,27 @@ def test_composite_structure_matches_golden(name):
     assert np.array_equal(ip, g["jindptr"]) and np.array_equal(ix, g["jindices"])
     ip, ix = p.evaluator.pattern("H")
     assert np.array_equal(ip, g["hindptr"]) and np.array_equal(ix, g["hindices"])
+
+
+@pytest.mark.parametrize("name", C.STAGE_FIXTURES + C.COMPOSITE_FIXTURES)
+def test_tile_tables_satisfy_planner_invariants(name):
+    """Every staging position and round slot has exactly one producer (no GPU)."""
+    if name in C.STAGE_FIXTURES:
+        p, _ = pkg.build_acopf(stage_case(STAGE_SPECS[name]))
+    else:
+        spec = COMPOSITE_SPECS[name]
+        a, _ = composite_inputs(spec)
+        p, _ = compose(pkg, spec["kind"], a)
+    st = p.evaluator.verify_plan()
+    assert st["tables"] >= st["tiles"] >= 1
+    assert st["max_smem_bytes"] <= 220 * 1024
+
+
+def test_tile_tables_config1_network():
+    """The 10k-bus network: invariants, tile fill and the CTA shared-memory budget."""
+    from paper_2203_10587_b200 import synthetic as syn
+    p, _ = pkg.build_acopf(syn.config_case(1))
+    st = p.evaluator.verify_plan()
+    assert st["ends"] == 2 * 12999
+    assert st["ends"] / st["tiles"] > 40          # tile fill (64 ends per 2-warp CTA)
+    assert st["max_smem_bytes"] <= 48 * 1024
