@@ -614,8 +614,8 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
         // ---- B: balance rounds, next gathers, sum rounds -------------------------
         if (need_c || need_f) {
             for (int r = warp; r < H->nRB; r += 2) {
-                const unsigned short* rd = bround + 4 * r;
-                const int base = rd[0], dmax = rd[1], gbase = rd[2], gmax = rd[3];
+                const unsigned short* rd = bround + 6 * r;
+                const int base = rd[0], dmax = rd[1], gbase = rd[2], gmax = rd[3], wd = rd[4];
                 const unsigned item = bitem[32 * r + lane];
                 const bool on = item != 0xffffu;
                 const int bl = on ? (int)(item & 0x7fffu) : 0;
@@ -623,14 +623,14 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
                 const double* run = A + base + lane;
                 double p = 0.0;
 #pragma unroll 4
-                for (int j = 0; j < dmax; ++j) p = p + run[32 * j];
+                for (int j = 0; j < dmax; ++j) p = p + run[wd * j];
                 const int i = b0 + bl;
                 if (on && need_f) P.inj[R.inj_off + (qc ? nb : 0) + i] = p;     // Engine.injections (acopf.py:252-264)
                 if (need_c) {
                     double c = -(A[V.bqd[(5 + qc) * H->nB + bl]] + p);
                     const double* gq = A + gbase + lane;
 #pragma unroll 2
-                    for (int j = 0; j < gmax; ++j) c = c + gq[32 * j];
+                    for (int j = 0; j < gmax; ++j) c = c + gq[wd * j];
                     if (on) P.cons[eq_row + (qc ? nb : 0) + i] = c;
                 }
             }
@@ -643,19 +643,20 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
             for (int r = r0 + warp; r < r1; r += 4) {
                 const bool two = r + 2 < r1;
                 const int rb = two ? r + 2 : r;
-                const int ca = sround[2 * r + 1], cb = two ? sround[2 * rb + 1] : 0;
-                const double* ra = A + sround[2 * r] + lane;
-                const double* rbp = A + sround[2 * rb] + lane;
+                const int ca = sround[4 * r + 1], cb = two ? sround[4 * rb + 1] : 0;
+                const int wa = sround[4 * r + 2], wb = sround[4 * rb + 2];
+                const double* ra = A + sround[4 * r] + lane;
+                const double* rbp = A + sround[4 * rb] + lane;
                 double va = ra[0], vb = rbp[0];
                 const int cm = ca < cb ? ca : cb;
                 int j = 1;
 #pragma unroll 2
                 for (; j < cm; ++j) {
-                    va = va + ra[32 * j];
-                    vb = vb + rbp[32 * j];
+                    va = va + ra[wa * j];
+                    vb = vb + rbp[wb * j];
                 }
-                for (int k = j; k < ca; ++k) va = va + ra[32 * k];
-                for (int k = j; k < cb; ++k) vb = vb + rbp[32 * k];
+                for (int k = j; k < ca; ++k) va = va + ra[wa * k];
+                for (int k = j; k < cb; ++k) vb = vb + rbp[wb * k];
                 A[sdst[32 * r + lane]] = va;
                 if (two) A[sdst[32 * rb + lane]] = vb;
             }

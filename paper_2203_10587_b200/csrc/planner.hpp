@@ -308,10 +308,10 @@ struct TileTable {
     int nArea = 0, tslot = 0, ngl = 0;
     std::vector<uint16_t> dst;    // NST x nE (SoA): where each end store goes (area slot)
     std::vector<uint16_t> bqd;    // NQB x nB (SoA): location of each bus quantity
-    std::vector<uint16_t> sround; // per sum round: base, term count; J rounds then H rounds
+    std::vector<uint16_t> sround; // per sum round: base, term count, width, 0; J rounds then H rounds
     std::vector<uint16_t> sdst;   // per sum round: 32 staging destinations
     int nRJ = 0, nRH = 0;
-    std::vector<uint16_t> bround; // per balance round: base, degree, gen base, gen count
+    std::vector<uint16_t> bround; // per balance round: base, run length, gen base, gen count, width, 0
     std::vector<uint16_t> bitem;  // per balance round: 32 x (bus | Q << 15), 0xffff = none
     std::vector<uint16_t> gdst;   // 2 x ngl: gen-round slot of each generator's Pg, Qg
     std::vector<uint16_t> cpos;   // area slots holding the constant 1.0
@@ -350,7 +350,7 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     TileHdr h{};
     h.b0 = b0; h.nB = nB; h.nE = nE; h.nF = nF;
     for (int s = 0; s < 4; ++s) h.L[s] = L[s];
-    h.nArea = nArea; h.nRJ = nRJ; h.nRH = nRH; h.nRB = (int)bround.size() / 4;
+    h.nArea = nArea; h.nRJ = nRJ; h.nRH = nRH; h.nRB = (int)bround.size() / 6;
     h.tslot = tslot;
     h.ngl = (int)glist.size();
     h.nConst = (int)cpos.size(); h.nNegA = (int)nega.size(); h.nOrph = (int)orph.size();
@@ -484,33 +484,47 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         }
     int next = pos;
     tt.tslot = next++;
+    // rounds: consecutive entries of a list sorted by decreasing length, up to 32
+    // per round and none shorter than half the round's longest (a long duplicate
+    // sum, e.g. a hub bus's diagonal, does not pad 31 short ones to its length);
+    // a round of width w keeps term j of lane l at base + w j + l
+    auto form_rounds = [](const std::vector<int>& len) {
+        std::vector<std::pair<int, int>> rr;       // (first, width)
+        size_t i = 0;
+        while (i < len.size()) {
+            const int cmax = len[i];
+            size_t k = i + 1;
+            while (k < len.size() && k - i < 32 && 2 * len[k] >= cmax) ++k;
+            rr.push_back({(int)i, (int)(k - i)});
+            i = k;
+        }
+        return rr;
+    };
     for (int c = 0; c < 2; ++c) {
         std::stable_sort(sums[c].begin(), sums[c].end(), [](const Sum& x, const Sum& y) { return x.n > y.n; });
-        const int nr = ((int)sums[c].size() + 31) / 32;
-        for (int r = 0; r < nr; ++r) {
-            int cmax = 0;
-            for (int l = 0; l < 32 && 32 * r + l < (int)sums[c].size(); ++l) cmax = std::max(cmax, sums[c][32 * r + l].n);
+        std::vector<int> len;
+        for (const Sum& sm : sums[c]) len.push_back(sm.n);
+        const auto rr = form_rounds(len);
+        for (auto [first, width] : rr) {
+            const int cmax = len[first];
             const int base = next;
-            next += 32 * cmax;
+            next += width * cmax;
             tt.sround.push_back((uint16_t)base);
             tt.sround.push_back((uint16_t)cmax);
+            tt.sround.push_back((uint16_t)width);
+            tt.sround.push_back(0);
             for (int l = 0; l < 32; ++l) {
-                const int k = 32 * r + l;
-                if (k >= (int)sums[c].size()) {
-                    tt.sdst.push_back((uint16_t)tt.tslot);
-                    for (int j = 0; j < cmax; ++j) nega.push_back(base + 32 * j + l);
-                    continue;
-                }
-                const Sum& sm = sums[c][k];
+                if (l >= width) { tt.sdst.push_back((uint16_t)tt.tslot); continue; }
+                const Sum& sm = sums[c][first + l];
                 const Row& row = rows[sm.row];
                 tt.sdst.push_back((uint16_t)sm.dst);
                 for (int j = 0; j < cmax; ++j) {
-                    if (j < sm.n) place(row.terms[row.tptr[sm.entry] + j], base + 32 * j + l);
-                    else nega.push_back(base + 32 * j + l);
+                    if (j < sm.n) place(row.terms[row.tptr[sm.entry] + j], base + width * j + l);
+                    else nega.push_back(base + width * j + l);
                 }
             }
         }
-        (c == 0 ? tt.nRJ : tt.nRH) = nr;
+        (c == 0 ? tt.nRJ : tt.nRH) = (int)rr.size();
     }
     // balance rounds: (bus, P|Q) items by decreasing degree; a run holds the
     // bus's flows in np.add.at order, then its shunt term; the generators'
@@ -523,44 +537,45 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     auto deg = [&](int it) { return tt.busptr[(it >> 1) + 1] - tt.busptr[it >> 1]; };
     std::stable_sort(items.begin(), items.end(), [&](int x, int y) { return deg(x) > deg(y); });
     tt.gdst.assign(2 * (size_t)tt.ngl, 0);
-    for (int r = 0; r < ((int)items.size() + 31) / 32; ++r) {
+    std::vector<int> blen;
+    for (int it : items) blen.push_back(deg(it) + 1);
+    for (auto [first, width] : form_rounds(blen)) {
         int dmax = 0, gmax = 0;
-        for (int l = 0; l < 32 && 32 * r + l < (int)items.size(); ++l) {
-            const int it = items[32 * r + l];
+        for (int l = 0; l < width; ++l) {
+            const int it = items[first + l];
             dmax = std::max(dmax, deg(it) + 1);
             gmax = std::max(gmax, gfirst[(it >> 1) + 1] - gfirst[it >> 1]);
         }
         const int base = next;
-        next += 32 * dmax;
+        next += width * dmax;
         const int gbase = next;
-        next += 32 * gmax;
+        next += width * gmax;
         tt.bround.push_back((uint16_t)base);
         tt.bround.push_back((uint16_t)dmax);
         tt.bround.push_back((uint16_t)gbase);
         tt.bround.push_back((uint16_t)gmax);
+        tt.bround.push_back((uint16_t)width);
+        tt.bround.push_back(0);
         for (int l = 0; l < 32; ++l) {
-            const int k = 32 * r + l;
-            if (k >= (int)items.size()) {
-                tt.bitem.push_back(0xffff);
-                for (int j = 0; j < dmax; ++j) nega.push_back(base + 32 * j + l);
-                for (int j = 0; j < gmax; ++j) nega.push_back(gbase + 32 * j + l);
-                continue;
-            }
-            const int it = items[k], bl = it >> 1, qc = it & 1;
+            if (l >= width) { tt.bitem.push_back(0xffff); continue; }
+            const int it = items[first + l], bl = it >> 1, qc = it & 1;
             tt.bitem.push_back((uint16_t)(bl | (qc << 15)));
             const int d = deg(it);
             for (int j = 0; j < dmax; ++j) {
-                if (j < d) loc_e[(size_t)(qc ? ST_FQ : ST_FP) * nE + tt.bend[tt.busptr[bl] + j]] = base + 32 * j + l;
-                else if (j == d) loc_b[(size_t)(3 + qc) * nB + bl] = base + 32 * j + l;
-                else nega.push_back(base + 32 * j + l);
+                const int v = base + width * j + l;
+                if (j < d) loc_e[(size_t)(qc ? ST_FQ : ST_FP) * nE + tt.bend[tt.busptr[bl] + j]] = v;
+                else if (j == d) loc_b[(size_t)(3 + qc) * nB + bl] = v;
+                else nega.push_back(v);
             }
             const int ng = gfirst[bl + 1] - gfirst[bl];
             for (int j = 0; j < gmax; ++j) {
-                if (j < ng) tt.gdst[(size_t)qc * tt.ngl + gfirst[bl] + j] = (uint16_t)(gbase + 32 * j + l);
-                else nega.push_back(gbase + 32 * j + l);
+                const int v = gbase + width * j + l;
+                if (j < ng) tt.gdst[(size_t)qc * tt.ngl + gfirst[bl] + j] = (uint16_t)v;
+                else nega.push_back(v);
             }
         }
     }
+    next += 32;        // margin: lanes beyond a round's width read (and discard) up to 31 slots past it
     // pd, qd of every bus; the representative (first) end of every bus
     for (int bl = 0; bl < nB; ++bl) {
         loc_b[(size_t)5 * nB + bl] = next++;
@@ -615,29 +630,34 @@ inline std::string verify_tile(const TileTable& tt) {
         prod[v]++;
     }
     const int nR = tt.nRJ + tt.nRH;
-    if ((int)tt.sround.size() != 2 * nR || (int)tt.sdst.size() != 32 * nR) return "sum round tables have the wrong size";
+    if ((int)tt.sround.size() != 4 * nR || (int)tt.sdst.size() != 32 * nR) return "sum round tables have the wrong size";
     for (int r = 0; r < nR; ++r) {
-        const int base = tt.sround[2 * r], c = tt.sround[2 * r + 1];
+        const int base = tt.sround[4 * r], c = tt.sround[4 * r + 1], w = tt.sround[4 * r + 2];
+        if (w < 1 || w > 32) return "sum round width out of range";
+        if (base + w * c + 31 >= tt.nArea + 1) return "sum round reads past the area";
         for (int l = 0; l < 32; ++l) {
             const int d = tt.sdst[32 * r + l];
             if (!slot_ok(d)) return "sum destination outside the area";
+            if (l >= w) {
+                if (d != tt.tslot) return "idle sum lane not sent to the trash slot";
+                continue;
+            }
             if (d != tt.tslot) {
                 if (d >= T) return "sum destination outside the staging segments";
                 prod[d]++;
             }
-            for (int j = 0; j < c; ++j) {
-                const int v = base + 32 * j + l;
-                if (!slot_ok(v)) return "sum round outside the area";
-                read[v]++;
-            }
+            for (int j = 0; j < c; ++j) read[base + w * j + l]++;
         }
     }
-    const int nRB = (int)tt.bround.size() / 4;
+    const int nRB = (int)tt.bround.size() / 6;
     for (int r = 0; r < nRB; ++r) {
-        const int base = tt.bround[4 * r], d = tt.bround[4 * r + 1], gb = tt.bround[4 * r + 2], g = tt.bround[4 * r + 3];
-        for (int l = 0; l < 32; ++l) {
-            for (int j = 0; j < d; ++j) { if (!slot_ok(base + 32 * j + l)) return "balance round outside the area"; read[base + 32 * j + l]++; }
-            for (int j = 0; j < g; ++j) { if (!slot_ok(gb + 32 * j + l)) return "generator round outside the area"; read[gb + 32 * j + l]++; }
+        const int base = tt.bround[6 * r], d = tt.bround[6 * r + 1], gb = tt.bround[6 * r + 2];
+        const int g = tt.bround[6 * r + 3], w = tt.bround[6 * r + 4];
+        if (w < 1 || w > 32) return "balance round width out of range";
+        if (base + w * d + 31 >= tt.nArea + 1 || gb + w * g + 31 >= tt.nArea + 1) return "balance round reads past the area";
+        for (int l = 0; l < w; ++l) {
+            for (int j = 0; j < d; ++j) read[base + w * j + l]++;
+            for (int j = 0; j < g; ++j) read[gb + w * j + l]++;
         }
     }
     for (int v = 0; v < tt.nArea; ++v) {
