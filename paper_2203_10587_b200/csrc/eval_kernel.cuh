@@ -317,7 +317,8 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
     const double* adm = V.adm + e;
     const double gff = adm[0], bff = adm[nE], gft = adm[2 * nE], bft = adm[3 * nE];
     const double gtf = adm[4 * nE], btf = adm[5 * nE], gtt = adm[6 * nE], btt = adm[7 * nE];
-    const double g2ff = adm[8 * nE], m2bff = adm[9 * nE], g2tt = adm[10 * nE], m2btt = adm[11 * nE];
+    // 2 gff, -2 bff, 2 gtt, -2 btt (acopf.py:243-246, 318-319): exact doublings
+    const double g2ff = gff + gff, m2bff = -(bff + bff), g2tt = gtt + gtt, m2btt = -(btt + btt);
     const unsigned* dw = V.dst + 9 * e;
     const double vf = in.vf, vt = in.vt;
     const double th = in.vaf - in.vat;

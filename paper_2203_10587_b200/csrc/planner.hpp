@@ -278,7 +278,7 @@ inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
 
 constexpr int NST = 18;           // stores per end: 15 quantities, P flow, Q flow, second copy of quantity 13
 constexpr int ST_FP = 15, ST_FQ = 16, ST_X13 = 17;
-constexpr int NADM = 12;          // per end: gff bff gft bft gtf btf gtt btt, 2 gff, -2 bff, 2 gtt, -2 btt
+constexpr int NADM = 8;           // per end: gff bff gft bft gtf btf gtt btt
 
 struct TileHdr {                      // 160 bytes; section offsets in bytes from the header start
     int32_t b0, nB, nE, nF;           // first bus, buses, ends, from-ends (ends [0,nF) are from-ends)
@@ -336,10 +336,6 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
         code[e] = ends[e];
         const double* a = &T.adm[8 * (size_t)k];
         for (int q = 0; q < 8; ++q) adm[(size_t)q * nE + e] = a[q];
-        adm[(size_t)8 * nE + e] = 2.0 * a[0];      // exact scalings (acopf.py:243-246, 318-319)
-        adm[(size_t)9 * nE + e] = -2.0 * a[1];
-        adm[(size_t)10 * nE + e] = 2.0 * a[6];
-        adm[(size_t)11 * nE + e] = -2.0 * a[7];
     }
     for (int bl = 0; bl < nB; ++bl) {
         int i = b0 + bl;
