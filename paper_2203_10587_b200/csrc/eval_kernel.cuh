@@ -142,7 +142,9 @@ __host__ __device__ __forceinline__ size_t tile_smem_bytes(int table_bytes, int 
 }
 
 __device__ __forceinline__ void cp_async8s(unsigned dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    // no "memory" clobber: completion is ordered by cp.async.wait_group (which
+    // has one) and the CTA barrier that follows it
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src));
 }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -264,8 +266,10 @@ __device__ __forceinline__ void load_end(const EvalParams& P, const DRec& R, con
     }
 }
 
-__device__ __forceinline__ void sts64(unsigned addr, double v) {
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+// A store into the working area (a typed shared-memory store the compiler can
+// order against the table and record loads it does not alias).
+__device__ __forceinline__ void sts64(unsigned char* addr, double v) {
+    *reinterpret_cast<double*>(addr) = v;
 }
 
 // A bus's own terms (acopf.py:262-263, 283, 296-297, 366): shunt Jacobian and
@@ -273,7 +277,7 @@ __device__ __forceinline__ void sts64(unsigned addr, double v) {
 // zero gradient entries.  Computed by the bus's first branch end (or, for a
 // bus without branches, by the orphan loop).
 __device__ __forceinline__ void bus_terms(const EvalParams& P, const DRec& R, const TileView& V, int rb, double vm,
-                                          double mp, double mq, double pd, double qd, unsigned sA, bool need_j,
+                                          double mp, double mq, double pd, double qd, unsigned char* sA, bool need_j,
                                           bool need_h, bool need_c, bool need_f, bool need_g) {
     const int nB = V.H->nB;
     const double gsb = V.gs[rb], bsb = V.bs[rb];
@@ -311,7 +315,7 @@ __device__ __forceinline__ void bus_terms(const EvalParams& P, const DRec& R, co
 // v4 = v0 (the squared partials agree).  An end evaluates 5 positions.
 template <int SIDE>
 __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, const TileView& V, int e,
-                                         const EndIn& in, const double* G, unsigned sA, bool need_j, bool need_h,
+                                         const EndIn& in, const double* G, unsigned char* sA, bool need_j, bool need_h,
                                          bool need_c, bool need_f, bool need_g) {
     const int nE = V.H->nE;
     const double* adm = V.adm + e;
@@ -425,7 +429,7 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
 
 template <int SIDE>
 __device__ __forceinline__ void ends_phase(const EvalParams& P, const DRec& R, const TileView& V, int lane,
-                                           const EndIn& pre, const double* G, unsigned sA, bool need_j,
+                                           const EndIn& pre, const double* G, unsigned char* sA, bool need_j,
                                            bool need_h, bool need_c, bool need_f, bool need_g) {
     const int e0 = SIDE ? V.H->nF : 0, e1 = SIDE ? V.H->nE : V.H->nF;
     if (e0 + lane < e1) end_eval<SIDE>(P, R, V, e0 + lane, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
@@ -439,7 +443,7 @@ __device__ __forceinline__ void ends_phase(const EvalParams& P, const DRec& R, c
 // Generator set-points into their balance-round slots (thread tid: generator
 // tid prefetched, further ones loaded here).
 __device__ __forceinline__ void gens_phase(const EvalParams& P, const DRec& R, const TileView& V, int tid,
-                                           const double* G, unsigned sA) {
+                                           const double* G, unsigned char* sA) {
     const int ngl = V.H->ngl;
     const unsigned char* base = reinterpret_cast<const unsigned char*>(V.H);
     const unsigned short* gdst = reinterpret_cast<const unsigned short*>(base + V.H->o_gdst);
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
     const TileHdr* H = reinterpret_cast<const TileHdr*>(smem);
     const int b0 = H->b0;
     double* A = reinterpret_cast<double*>(smem + H->bytes);
-    const unsigned sA = smem_u32(A);
+    unsigned char* const sA = reinterpret_cast<unsigned char*>(A);
     DRec* ctx = reinterpret_cast<DRec*>(smem + tile_rec_off(H->bytes, H->nArea));
     const double* G = reinterpret_cast<const double*>(smem + tile_gather_off(H->bytes, H->nArea)) + tid;
     const unsigned sG = smem_u32(G);
@@ -624,14 +628,15 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
                 const double* run = A + base + lane;
                 double p = 0.0;
 #pragma unroll 4
-                for (int j = 0; j < dmax; ++j) p = p + run[wd * j];
+#pragma unroll 4
+                for (int j = 0; j < dmax; ++j, run += wd) p = p + run[0];
                 const int i = b0 + bl;
                 if (on && need_f) P.inj[R.inj_off + (qc ? nb : 0) + i] = p;     // Engine.injections (acopf.py:252-264)
                 if (need_c) {
                     double c = -(A[V.bqd[(5 + qc) * H->nB + bl]] + p);
                     const double* gq = A + gbase + lane;
 #pragma unroll 2
-                    for (int j = 0; j < gmax; ++j) c = c + gq[wd * j];
+                    for (int j = 0; j < gmax; ++j, gq += wd) c = c + gq[0];
                     if (on) P.cons[eq_row + (qc ? nb : 0) + i] = c;
                 }
             }
@@ -651,13 +656,17 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
                 double va = ra[0], vb = rbp[0];
                 const int cm = ca < cb ? ca : cb;
                 int j = 1;
-#pragma unroll 2
-                for (; j < cm; ++j) {
-                    va = va + ra[wa * j];
-                    vb = vb + rbp[wb * j];
+                ra += wa;
+                rbp += wb;
+#pragma unroll 4
+                for (; j < cm; ++j, ra += wa, rbp += wb) {
+                    va = va + ra[0];
+                    vb = vb + rbp[0];
                 }
-                for (int k = j; k < ca; ++k) va = va + ra[wa * k];
-                for (int k = j; k < cb; ++k) vb = vb + rbp[wb * k];
+#pragma unroll 4
+                for (int k = j; k < ca; ++k, ra += wa) va = va + ra[0];
+#pragma unroll 4
+                for (int k = j; k < cb; ++k, rbp += wb) vb = vb + rbp[0];
                 A[sdst[32 * r + lane]] = va;
                 if (two) A[sdst[32 * rb + lane]] = vb;
             }
