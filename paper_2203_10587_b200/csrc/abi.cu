@@ -149,14 +149,38 @@ static void upload(acopf_batch* b) {
         max_leaf = std::max(max_leaf, T->leaf_start.size());
         dt.push_back(d);
     }
-    // blob of tile tables (each 16-byte aligned, sized for one bulk copy)
+    // blob of tile tables (each 16-byte aligned, sized for one bulk copy).  Each
+    // staging segment is shifted by a free slot when needed so that its 16-byte
+    // parity matches its output run's (first stage using the table; these
+    // layouts keep every stage's CSR bases even), so the copy-out is a TMA
+    // bulk store
     std::vector<uint8_t> blob;
     std::vector<int64_t> table_off(b->tables.size());
-    std::vector<int> table_bytes(b->tables.size());
+    std::vector<int> table_bytes(b->tables.size()), table_shift_n(b->tables.size(), 0);
+    std::vector<int> table_mask(b->tables.size(), -1);
+    for (int s = 0; s < S; ++s) {
+        const StageInfo& st = b->stages[s];
+        const int64_t* o = &b->off6[6 * s];
+        for (size_t t = 0; t < st.table.size(); ++t) {
+            int& m = table_mask[st.table[t]];
+            if (m >= 0) continue;
+            const TileTable& tt = b->tables[st.table[t]];
+            const int Sst[4] = {0, tt.L[0], tt.L[0] + tt.L[1], tt.L[0] + tt.L[1] + tt.L[2]};
+            m = 0;
+            for (int q = 0, c = 0; q < 4; ++q) {
+                const int64_t g = (q < 2 ? o[3] : o[5]) + st.tile_off[4 * t + q];
+                const int sh = (int)((g - Sst[q] - c) & 1);
+                m |= sh << q;
+                c += sh;
+            }
+        }
+    }
     for (size_t i = 0; i < b->tables.size(); ++i) {
         table_off[i] = (int64_t)blob.size();
-        b->tables[i].serialise(*b->topos[b->tables[i].topo], blob);
+        const unsigned m = table_mask[i] < 0 ? 0u : (unsigned)table_mask[i];
+        b->tables[i].serialise(*b->topos[b->tables[i].topo], blob, m);
         table_bytes[i] = (int)(blob.size() - table_off[i]);
+        table_shift_n[i] = __builtin_popcount(m);
     }
     // stages and removed lists
     std::vector<DStage> ds(S);
@@ -206,7 +230,7 @@ static void upload(acopf_batch* b) {
     for (size_t ti = 0; ti < b->topos.size(); ++ti)
         for (size_t t = 0; t < b->base_table[ti].size(); ++t) tiles.push_back({(int)ti, (int)t});
     std::vector<int> table_area(b->tables.size());
-    for (size_t i = 0; i < b->tables.size(); ++i) table_area[i] = b->tables[i].nArea;
+    for (size_t i = 0; i < b->tables.size(); ++i) table_area[i] = b->tables[i].nArea + table_shift_n[i];
     // stage-group-major order: warps running together share one group's x/mult in L2
     for (int g0 = 0; g0 < S; g0 += G) {
         const int g1 = std::min(S, g0 + G);

@@ -588,6 +588,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
     for (int ri = 0; ri < it.count; ++ri) {
         const DRec& R = ctx[ri & 1];
         cp_wait<0>();          // this stage's gathers
+        if ((tid & 15) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
         __syncthreads();
         const bool more = ri + 1 < it.count;
         if (more && tid < 8)
@@ -671,20 +672,42 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
                 if (two) A[sdst[32 * rb + lane]] = vb;
             }
         }
+        // staging writes (generic proxy) before the bulk stores read them (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
-        // ---- C: contiguous copy-out of the staged segments (16 threads each) ----
+        // ---- C: copy-out of the staged segments: a TMA bulk store per segment
+        // when its staging copy shares the output run's 16-byte parity (the
+        // planner aligns them), else 16 threads with 16-byte stores ----------
         {
             const int seg = tid >> 4, sub = tid & 15;
             const bool on = seg < 2 ? need_j : need_h;
             if (on) {
                 const long long go = (&R.oP)[seg];
                 double* g = (seg < 2 ? P.jval : P.hval) + go;
-                const int so = (seg > 0 ? H->L[0] : 0) + (seg > 1 ? H->L[1] : 0) + (seg > 2 ? H->L[2] : 0);
-                copy_seg16(g, A + so, H->L[seg], sub);
+                const int sw = seg < 2 ? H->so01 : H->so23;
+                const double* sp = A + ((seg & 1) ? (sw >> 16) : (sw & 0xffff));
+                const int L = H->L[seg];
+                if (((reinterpret_cast<uintptr_t>(g) ^ reinterpret_cast<uintptr_t>(sp)) & 15) == 0) {
+                    if (sub == 0 && L > 0) {
+                        const int peel = (reinterpret_cast<uintptr_t>(g) & 8) ? 1 : 0;
+                        const int n16 = (L - peel) >> 1;
+                        if (peel) g[0] = sp[0];
+                        if (n16 > 0) {
+                            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g + peel),
+                                         "r"(smem_u32(sp + peel)), "r"(16 * n16)
+                                         : "memory");
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                        if ((L - peel) & 1) g[L - 1] = sp[L - 1];
+                    }
+                } else {
+                    copy_seg16(g, sp, L, sub);
+                }
             }
         }
     }
     cp_wait<0>();
+    if ((tid & 15) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------

@@ -284,13 +284,13 @@ struct TileHdr {                      // 160 bytes; section offsets in bytes fro
     int32_t b0, nB, nE, nF;           // first bus, buses, ends, from-ends (ends [0,nF) are from-ends)
     int32_t L[4];                     // entries of the four row segments
     int32_t nArea, nRJ, nRH, nRB;     // area doubles; sum rounds (J, H); balance rounds
-    int32_t bytes, tslot, ngl, pad0;  // serialised size; trash slot; generators
+    int32_t bytes, tslot, ngl, so01;  // serialised size; trash slot; generators; segment starts 0|1 << 16
     int32_t nConst, nNegA, nOrph, o_orph;   // constants, -0.0 paddings, buses without branches
     int32_t o_adm, o_f, o_t, o_ridx;
     int32_t o_foff, o_code, o_dst, o_gs;
     int32_t o_bs, o_glist, o_gdst, o_bqd;
     int32_t o_sround, o_sdst, o_bround, o_bitem;
-    int32_t o_const, o_nega, o_rep, pad3;
+    int32_t o_const, o_nega, o_rep, so23;   // ...; segment starts 2|3 << 16
 };
 static_assert(sizeof(TileHdr) == 160, "TileHdr layout");
 
@@ -318,13 +318,34 @@ struct TileTable {
     std::vector<uint16_t> nega;   // area slots holding -0.0 (round padding)
     std::vector<int> rep;         // per end: its bus (tile-local) if it is the bus's first end, else -1
     std::vector<uint16_t> orph;   // buses without branch ends (tile-local)
-    void serialise(const Topo& T, std::vector<uint8_t>& blob) const;
+    // shift_mask bit s: one free slot before staging segment s (aligns the
+    // segment's 16-byte parity with its output run for TMA bulk stores)
+    void serialise(const Topo& T, std::vector<uint8_t>& blob, unsigned shift_mask = 0) const;
 };
 
 inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) const {
+inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob, unsigned shift_mask) const {
     const int nE = (int)ends.size();
+    // slot remap for the segment shifts
+    int S[5] = {0, L[0], L[0] + L[1], L[0] + L[1] + L[2], L[0] + L[1] + L[2] + L[3]};
+    int cum[4];
+    for (int q = 0, c = 0; q < 4; ++q) { c += (shift_mask >> q) & 1; cum[q] = c; }
+    auto remap = [&](int v) -> int {
+        if (v >= S[4]) return v + cum[3];
+        int q = 0;
+        while (v >= S[q + 1]) ++q;
+        return v + cum[q];
+    };
+    auto remap16 = [&](std::vector<uint16_t> v) { for (auto& x : v) x = (uint16_t)remap(x); return v; };
+    const std::vector<uint16_t> dstR = remap16(dst), bqdR = remap16(bqd), cposR = remap16(cpos),
+                                negaR = remap16(nega), gdstR = remap16(gdst), sdstR = remap16(sdst);
+    std::vector<uint16_t> sroundR = sround, broundR = bround;
+    for (size_t r = 0; r < sroundR.size() / 4; ++r) sroundR[4 * r] = (uint16_t)remap(sroundR[4 * r]);
+    for (size_t r = 0; r < broundR.size() / 6; ++r) {
+        broundR[6 * r] = (uint16_t)remap(broundR[6 * r]);
+        broundR[6 * r + 2] = (uint16_t)remap(broundR[6 * r + 2]);
+    }
     std::vector<int> f(nE), t(nE), ridx(nE), foff(nE), code(nE), glist;
     std::vector<double> adm(NADM * (size_t)nE), gs(nB), bs(nB);
     for (int e = 0; e < nE; ++e) {
@@ -346,8 +367,10 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
     TileHdr h{};
     h.b0 = b0; h.nB = nB; h.nE = nE; h.nF = nF;
     for (int s = 0; s < 4; ++s) h.L[s] = L[s];
-    h.nArea = nArea; h.nRJ = nRJ; h.nRH = nRH; h.nRB = (int)bround.size() / 6;
-    h.tslot = tslot;
+    h.nArea = nArea + cum[3]; h.nRJ = nRJ; h.nRH = nRH; h.nRB = (int)bround.size() / 6;
+    h.tslot = remap(tslot);
+    h.so01 = (S[0] + cum[0]) | ((S[1] + cum[1]) << 16);
+    h.so23 = (S[2] + cum[2]) | ((S[3] + cum[3]) << 16);
     h.ngl = (int)glist.size();
     h.nConst = (int)cpos.size(); h.nNegA = (int)nega.size(); h.nOrph = (int)orph.size();
     size_t off = sizeof(TileHdr);
@@ -388,21 +411,21 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob) cons
         std::vector<uint32_t> dw(9 * (size_t)nE);
         for (int e = 0; e < nE; ++e)
             for (int k = 0; k < 9; ++k)
-                dw[9 * (size_t)e + k] = (uint32_t)(8 * dst[(size_t)(2 * k) * nE + e]) |
-                                        ((uint32_t)(8 * dst[(size_t)(2 * k + 1) * nE + e]) << 16);
+                dw[9 * (size_t)e + k] = (uint32_t)(8 * dstR[(size_t)(2 * k) * nE + e]) |
+                                        ((uint32_t)(8 * dstR[(size_t)(2 * k + 1) * nE + e]) << 16);
         put(h.o_dst, dw.data(), 4 * dw.size());
     }
     put(h.o_gs, gs.data(), 8 * (size_t)nB);
     put(h.o_bs, bs.data(), 8 * (size_t)nB);
     put(h.o_glist, glist.data(), 4 * glist.size());
-    put(h.o_gdst, gdst.data(), 2 * gdst.size());
-    put(h.o_bqd, bqd.data(), 2 * bqd.size());
-    put(h.o_sround, sround.data(), 2 * sround.size());
-    put(h.o_sdst, sdst.data(), 2 * sdst.size());
-    put(h.o_bround, bround.data(), 2 * bround.size());
+    put(h.o_gdst, gdstR.data(), 2 * gdst.size());
+    put(h.o_bqd, bqdR.data(), 2 * bqd.size());
+    put(h.o_sround, sroundR.data(), 2 * sround.size());
+    put(h.o_sdst, sdstR.data(), 2 * sdst.size());
+    put(h.o_bround, broundR.data(), 2 * bround.size());
     put(h.o_bitem, bitem.data(), 2 * bitem.size());
-    put(h.o_const, cpos.data(), 2 * cpos.size());
-    put(h.o_nega, nega.data(), 2 * nega.size());
+    put(h.o_const, cposR.data(), 2 * cpos.size());
+    put(h.o_nega, negaR.data(), 2 * nega.size());
     put(h.o_rep, rep.data(), 4 * rep.size());
     put(h.o_orph, orph.data(), 2 * orph.size());
 }
