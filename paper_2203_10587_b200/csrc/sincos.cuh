@@ -142,6 +142,39 @@ SC_HD void acc_sincos(double x, double* sp, double* cp) {
 #define GL_S5 (-0x1.addffc2fcdf59p-26)
 #define GL_BIG 52776558133248.0
 
+// On the device the coefficients live in constant memory, so the fp64
+// instructions take them as constant-bank operands instead of materialising
+// each 64-bit immediate with register moves.
+#ifdef __CUDACC__
+__constant__ double sc_gl_k[11] = {GL_SN3, GL_SN5, GL_CS2, GL_CS4, GL_CS6, GL_S1,
+                                          GL_S2,  GL_S3,  GL_S4,  GL_S5,  GL_BIG};
+#endif
+#ifdef __CUDA_ARCH__
+#define GLK_SN3 sc_gl_k[0]
+#define GLK_SN5 sc_gl_k[1]
+#define GLK_CS2 sc_gl_k[2]
+#define GLK_CS4 sc_gl_k[3]
+#define GLK_CS6 sc_gl_k[4]
+#define GLK_S1 sc_gl_k[5]
+#define GLK_S2 sc_gl_k[6]
+#define GLK_S3 sc_gl_k[7]
+#define GLK_S4 sc_gl_k[8]
+#define GLK_S5 sc_gl_k[9]
+#define GLK_BIG sc_gl_k[10]
+#else
+#define GLK_SN3 GL_SN3
+#define GLK_SN5 GL_SN5
+#define GLK_CS2 GL_CS2
+#define GLK_CS4 GL_CS4
+#define GLK_CS6 GL_CS6
+#define GLK_S1 GL_S1
+#define GLK_S2 GL_S2
+#define GLK_S3 GL_S3
+#define GLK_S4 GL_S4
+#define GLK_S5 GL_S5
+#define GLK_BIG GL_BIG
+#endif
+
 // table: sc_gl_table_* (SC_GL_NK entries of sin hi, sin lo, cos hi, cos lo),
 // or a copy of it (the tile kernel keeps one in shared memory)
 SC_HD void libm_sincos_t(const double* table, double x, double* sp, double* cp) {
@@ -151,22 +184,22 @@ SC_HD void libm_sincos_t(const double* table, double x, double* sp, double* cp) 
     // on 0.0 and takes the fallback below): table entry k = round(128 |x|)
     // and remainder, exactly as big + |x| rounds
     const double axs = core ? ax : 0.0;
-    const double u = GL_BIG + axs;
-    const double xk = u - GL_BIG;
+    const double u = GLK_BIG + axs;
+    const double xk = u - GLK_BIG;
     const double xr = axs - xk;
     const int k = (int)(xk * 128.0);
     const double* tab = table + 4 * k;
     const double sn = tab[0], ssn = tab[1], cs = tab[2], ccs = tab[3];
     const double xx = xr * xr;
-    const double ps = fma(xx, GL_SN5, GL_SN3);
-    const double pc = xx * fma(xx, fma(xx, GL_CS6, GL_CS4), GL_CS2);
+    const double ps = fma(xx, GLK_SN5, GLK_SN3);
+    const double pc = xx * fma(xx, fma(xx, GLK_CS6, GLK_CS4), GLK_CS2);
     // cos: 1 below 2^-27, else the table scheme
     const double s1 = fma(xr * xx, ps, xr);
     const double cor1 = fma(-sn, s1, fma(-cs, pc, fma(-s1, ssn, ccs)));
     const double c = ax < 7.450580596923828e-09 ? 1.0 : cs + cor1;
     // sin: x below 2^-26, the odd polynomial below 0.126, else the table scheme
     const double a2 = x * x;
-    const double p = fma(fma(fma(fma(GL_S5, a2, GL_S4), a2, GL_S3), a2, GL_S2), a2, GL_S1);
+    const double p = fma(fma(fma(fma(GLK_S5, a2, GLK_S4), a2, GLK_S3), a2, GLK_S2), a2, GLK_S1);
     const double s_small = x + (p * x) * a2;
     const double s2 = xr + fma(xr * xx, ps, 0.0);
     const double c2 = fma(xr, 0.0, pc);
