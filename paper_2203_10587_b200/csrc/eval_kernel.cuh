@@ -645,8 +645,8 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
         {
             // each warp takes rounds r and r + 2 together (two independent
             // chains per lane)
-            const int r0 = need_j ? 0 : H->nRJ;
-            const int r1 = need_h ? H->nRJ + H->nRH : H->nRJ;
+            const int r0 = 0;
+            const int r1 = (need_j || need_h) ? H->nRJ + H->nRH : 0;
             for (int r = r0 + warp; r < r1; r += 4) {
                 const bool two = r + 2 < r1;
                 const int rb = two ? r + 2 : r;

@@ -519,6 +519,10 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         }
         return rr;
     };
+    // J and H sums share one list (fuller rounds); a what-mask without J or H only
+    // computes sums into staging segments that are not copied out
+    sums[0].insert(sums[0].end(), sums[1].begin(), sums[1].end());
+    sums[1].clear();
     for (int c = 0; c < 2; ++c) {
         std::stable_sort(sums[c].begin(), sums[c].end(), [](const Sum& x, const Sum& y) { return x.n > y.n; });
         std::vector<int> len;
