@@ -126,7 +126,7 @@ __device__ __forceinline__ double hval(double cpf, double cqf, double cpt, doubl
     return v;
 }
 
-constexpr int TILE_THREADS = 64;   // warp 0: the tile's from-ends, warp 1: its to-ends
+constexpr int TILE_THREADS = 64;   // one branch end per thread
 
 constexpr int GQ = 4;    // doubles per thread in the gather buffer: pd qd (bus representative), Pg Qg (generator)
 
@@ -302,7 +302,8 @@ __device__ __forceinline__ void bus_terms(const EvalParams& P, const DRec& R, co
     }
 }
 
-// Phase A for one branch end of side SIDE (0: from-end, 1: to-end):
+// Phase A for one branch end; SIDE 0 / 1: the end is a from- / to-end (known at
+// compile time), 2: either (the kernel's case; side-dependent values selected):
 // acopf.py:230-250 (flows, partials), 290-311 (Jacobian), 313-369 (Hessian),
 // in the reference's association with no contraction.  Each of the end's 18
 // stores goes to the area slot its consumer reads (planner.hpp).
@@ -318,6 +319,8 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
                                          const EndIn& in, const double* G, unsigned char* sA, bool need_j, bool need_h,
                                          bool need_c, bool need_f, bool need_g) {
     const int nE = V.H->nE;
+    // SIDE 0 / 1: a warp of from- / to-ends (compile-time); 2: either (selects)
+    const bool sd = SIDE == 2 ? (e >= V.H->nF) : (SIDE == 1);
     const double* adm = V.adm + e;
     const double gff = adm[0], bff = adm[nE], gft = adm[2 * nE], bft = adm[3 * nE];
     const double gtf = adm[4 * nE], btf = adm[5 * nE], gtt = adm[6 * nE], btt = adm[7 * nE];
@@ -337,17 +340,17 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
     const double qf = ((-bff) * vf) * vf + vv * w;
     const double pt = (gtt * vt) * vt + vv * u2;
     const double qt = ((-btt) * vt) * vt + vv * w2;
-    const double fp = SIDE ? pt : pf, fq = SIDE ? qt : qf;
+    const double fp = sd ? pt : pf, fq = sd ? qt : qf;
     const unsigned d7 = dw[7], d8 = dw[8];
     sts64(sA + (d7 >> 16), fp);              // store 15
     sts64(sA + (d8 & 0xffffu), fq);          // store 16
     if (need_f) {          // acopf.py:448-465 (_branch_flows_mw, before the MVA scaling)
-        double* flw = P.flows + R.fl_off + 2 * SIDE * (long long)R.nbr + (V.code[e] >> 1);
+        double* flw = P.flows + R.fl_off + 2 * (int)sd * (long long)R.nbr + (V.code[e] >> 1);
         flw[0] = fp;
         flw[R.nbr] = fq;
     }
     const bool rated = in.rs >= 0;
-    if (rated && need_c) P.cons[R.ineq_row + 2 * in.rs + SIDE] = fp * fp + fq * fq;
+    if (rated && need_c) P.cons[R.ineq_row + 2 * in.rs + (int)sd] = fp * fp + fq * fq;
     const int rb = V.rep[e];
     if (rb >= 0) {
         double pdv = 0.0, qdv = 0.0;
@@ -359,7 +362,7 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
                 qdv = __ldg(P.qd + R.pd_off + i);
             }
         }
-        bus_terms(P, R, V, rb, SIDE ? vt : vf, SIDE ? in.mpt : in.mpf, SIDE ? in.mqt : in.mqf, pdv, qdv, sA,
+        bus_terms(P, R, V, rb, sd ? vt : vf, sd ? in.mpt : in.mpf, sd ? in.mqt : in.mqf, pdv, qdv, sA,
                   need_j, need_h, need_c, need_f, need_g);
     }
     if (!(need_j || need_h)) return;
@@ -369,8 +372,8 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
     const double gqt0 = (-vv) * u2, gqt2 = vt * w2, gqt3 = m2btt * vt + vf * w2;
     if (need_j) {
         // own partials; index 1 is the exact negation of index 0
-        const double gp0 = SIDE ? gpt0 : gpf0, gp2 = SIDE ? gpt2 : gpf2, gp3 = SIDE ? gpt3 : gpf3;
-        const double gq0 = SIDE ? gqt0 : gqf0, gq2 = SIDE ? gqt2 : gqf2, gq3 = SIDE ? gqt3 : gqf3;
+        const double gp0 = sd ? gpt0 : gpf0, gp2 = sd ? gpt2 : gpf2, gp3 = sd ? gpt3 : gpf3;
+        const double gq0 = sd ? gqt0 : gqf0, gq2 = sd ? gqt2 : gqf2, gq3 = sd ? gqt3 : gqf3;
         const unsigned d0 = dw[0], d1 = dw[1], d2 = dw[2], d3 = dw[3];
         sts64(sA + (d0 & 0xffffu), -gp0);
         sts64(sA + (d0 >> 16), gp0);
@@ -385,7 +388,7 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
             const double r0 = (0.0 + tp * gp0) + tq * gq0, r1 = (0.0 + tp * (-gp0)) + tq * (-gq0);
             const double r2 = (0.0 + tp * gp2) + tq * gq2, r3 = (0.0 + tp * gp3) + tq * gq3;
             const int f = V.f[e], t = V.t[e];
-            double* out = P.jval + R.jineq + in.fo + (f == t ? 2 : 4) * SIDE;
+            double* out = P.jval + R.jineq + in.fo + (f == t ? 2 : 4) * (int)sd;
             if (f < t) { out[0] = r0; out[1] = r1; out[2] = r2; out[3] = r3; }
             else if (f > t) { out[0] = r1; out[1] = r0; out[2] = r3; out[3] = r2; }
             else { out[0] = r0 + r1; out[1] = r2 + r3; }
@@ -410,11 +413,18 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
         const double v8 = hval(cpf, cqf, cpt, cqt, s2f, s2t, u, w, u2, w2,
                                gpf2, gpf3, gqf2, gqf3, gpt2, gpt3, gqt2, gqt3);
         // position 7 (vf, vf) of a from-end, position 9 (vt, vt) of a to-end
-        const double v79 = SIDE ? hval(cpf, cqf, cpt, cqt, s2f, s2t, z, z, g2tt, m2btt,
-                                       gpf3, gpf3, gqf3, gqf3, gpt3, gpt3, gqt3, gqt3)
-                                : hval(cpf, cqf, cpt, cqt, s2f, s2t, g2ff, m2bff, z, z,
-                                       gpf2, gpf2, gqf2, gqf2, gpt2, gpt2, gqt2, gqt2);
-        const double v5s = SIDE ? -v3 : v2;      // slot 5: position 2 (from) / 6 (to)
+        double v79;
+        if constexpr (SIDE == 2) {     // operand selects: one position evaluation
+            const double a0 = sd ? gpf3 : gpf2, a1 = sd ? gqf3 : gqf2, a2 = sd ? gpt3 : gpt2, a3 = sd ? gqt3 : gqt2;
+            v79 = hval(cpf, cqf, cpt, cqt, s2f, s2t, sd ? z : g2ff, sd ? z : m2bff, sd ? g2tt : z, sd ? m2btt : z,
+                       a0, a0, a1, a1, a2, a2, a3, a3);
+        } else {
+            v79 = SIDE ? hval(cpf, cqf, cpt, cqt, s2f, s2t, z, z, g2tt, m2btt,
+                              gpf3, gpf3, gqf3, gqf3, gpt3, gpt3, gqt3, gqt3)
+                       : hval(cpf, cqf, cpt, cqt, s2f, s2t, g2ff, m2bff, z, z,
+                              gpf2, gpf2, gqf2, gqf2, gpt2, gpt2, gqt2, gqt2);
+        }
+        const double v5s = sd ? -v3 : v2;      // slot 5: position 2 (from) / 6 (to)
         const unsigned d4 = dw[4], d5 = dw[5], d6 = dw[6];
         sts64(sA + (d4 & 0xffffu), v0);          // slot 0: position 0 / 4
         sts64(sA + (d4 >> 16), -v0);             // slot 1: position 1
@@ -431,9 +441,10 @@ template <int SIDE>
 __device__ __forceinline__ void ends_phase(const EvalParams& P, const DRec& R, const TileView& V, int lane,
                                            const EndIn& pre, const double* G, unsigned char* sA, bool need_j,
                                            bool need_h, bool need_c, bool need_f, bool need_g) {
-    const int e0 = SIDE ? V.H->nF : 0, e1 = SIDE ? V.H->nE : V.H->nF;
+    const int e0 = SIDE == 2 ? 0 : (SIDE ? V.H->nF : 0), e1 = SIDE == 2 ? V.H->nE : (SIDE ? V.H->nE : V.H->nF);
+    const int stride = SIDE == 2 ? TILE_THREADS : 32;
     if (e0 + lane < e1) end_eval<SIDE>(P, R, V, e0 + lane, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
-    for (int e = e0 + lane + 32; e < e1; e += 32) {     // sides with more than 32 ends: unprefetched
+    for (int e = e0 + lane + stride; e < e1; e += stride) {     // beyond one end per thread: unprefetched
         EndIn in;
         load_end(P, R, V, e, need_h, need_c, in);
         end_eval<SIDE>(P, R, V, e, in, nullptr, sA, need_j, need_h, need_c, need_f, need_g);
@@ -498,10 +509,10 @@ __device__ __forceinline__ void copy_seg16(double* g, const double* s, int L, in
 //      once;
 //   per stage (every thread's inputs were prefetched into registers during
 //   the previous stage, the next record with cp.async):
-//   A. warp 0 = the tile's from-ends, warp 1 = its to-ends, one per lane
-//      (side-uniform code: no divergence, no selects); the first end of each
-//      bus also stores the bus's shunt terms and loads; thread = generator:
-//      its set-points into the balance rounds.
+//   A. thread = branch end (ends sorted from-ends first; side-dependent
+//      values are selected, so a warp holding both sides does not diverge);
+//      the first end of each bus also stores the bus's shunt terms and loads;
+//      thread = generator: its set-points into the balance rounds.
 //   B. balance rounds: lane = (bus, P|Q), P/Q balance rows in np.add.at order
 //      (acopf.py:252-288); the next stage's gathers are issued; sum rounds:
 //      lane = multi-term entry, left-to-right sum in scipy's duplicate order
@@ -572,7 +583,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
         for (int i = tid; i < H->nConst; i += TILE_THREADS) A[cpos[i]] = 1.0;
         for (int i = tid; i < H->nNegA; i += TILE_THREADS) A[nega[i]] = -0.0;
     }
-    const int my_e = (warp ? H->nF : 0) + lane;
+    const int my_e = tid;
     const bool any_a = need_j || need_h || need_c || need_f || need_g;
 
     // first record and its inputs
@@ -599,8 +610,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
         const int nb = R.nb;
         // ---- A: branch ends (one side per warp), generator set-points ----------
         if (any_a) {
-            if (warp == 0) ends_phase<0>(P, R, V, lane, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
-            else ends_phase<1>(P, R, V, lane, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
+            ends_phase<2>(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
         }
         if (need_c) gens_phase(P, R, V, tid, G, sA);
         if (any_a)

@@ -56,12 +56,12 @@ constexpr int HSLOT_F[10] = {0, 1, 5, 2, -1, 3, -1, 6, 4, -1};
 constexpr int HSLOT_T[10] = {-1, 1, -1, 2, 0, 3, 5, -1, 4, 6};
 
 #ifndef ACOPF_TILE_ENDS
-#define ACOPF_TILE_ENDS 32
+#define ACOPF_TILE_ENDS 64
 #endif
 #ifndef ACOPF_TILE_BUSES
 #define ACOPF_TILE_BUSES 64
 #endif
-constexpr int TILE_MAX_ENDS = ACOPF_TILE_ENDS;    // per side; soft cap: a single high-degree bus may exceed it
+constexpr int TILE_MAX_ENDS = ACOPF_TILE_ENDS;    // soft cap: a single high-degree bus may exceed it
 constexpr int TILE_MAX_BUSES = ACOPF_TILE_BUSES;
 constexpr int SMEM_LIMIT_BYTES = 220 * 1024;
 
@@ -162,7 +162,7 @@ inline void Topo::finalize() {
         acc += rowsz[r];
     }
     // tiles: greedy runs of consecutive buses with at most TILE_MAX_ENDS
-    // from-ends and TILE_MAX_ENDS to-ends (one warp per side)
+    // branch ends (one per thread of the tile CTA)
     tile_b0.clear();
     int i = 0;
     while (i < nb) {
@@ -170,7 +170,7 @@ inline void Topo::finalize() {
         int nf = 0, nt = 0, nbus = 0;
         while (i < nb) {
             const int df = from_ptr[i + 1] - from_ptr[i], dt = to_ptr[i + 1] - to_ptr[i];
-            if (nbus > 0 && (nf + df > TILE_MAX_ENDS || nt + dt > TILE_MAX_ENDS || nbus >= TILE_MAX_BUSES)) break;
+            if (nbus > 0 && (nf + df + nt + dt > TILE_MAX_ENDS || nbus >= TILE_MAX_BUSES)) break;
             nf += df;
             nt += dt;
             nbus++;
@@ -250,9 +250,9 @@ inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
 // ---------------------------------------------------------------------------
 // Tiles (serialised into one device blob)
 //
-// A tile is a run of consecutive buses with at most TILE_MAX_ENDS from-ends
-// and TILE_MAX_ENDS to-ends; one 64-thread CTA (a warp per side) evaluates it
-// for a list of stages.  Its table (header + sections, 16-byte aligned) is
+// A tile is a run of consecutive buses with at most TILE_MAX_ENDS branch
+// ends; one 64-thread CTA (an end per thread) evaluates it for a list of
+// stages.  Its table (header + sections, 16-byte aligned) is
 // bulk-copied into shared memory once; after it comes the working "area":
 //
 //   [0, T)           staging of the tile's four output segments
