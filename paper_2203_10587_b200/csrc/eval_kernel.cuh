@@ -126,7 +126,11 @@ __device__ __forceinline__ double hval(double cpf, double cqf, double cpt, doubl
     return v;
 }
 
-constexpr int TILE_THREADS = 64;   // one branch end per thread
+#ifndef ACOPF_TILE_WARPS
+#define ACOPF_TILE_WARPS 2
+#endif
+constexpr int TILE_WARPS = ACOPF_TILE_WARPS;
+constexpr int TILE_THREADS = 32 * TILE_WARPS;   // one branch end per thread
 
 constexpr int GQ = 4;    // doubles per thread in the gather buffer: pd qd (bus representative), Pg Qg (generator)
 
@@ -520,7 +524,7 @@ __device__ __forceinline__ void copy_seg16(double* g, const double* s, int L, in
 //   C. the four staged segments are copied to their contiguous CSR runs.
 // Three CTA barriers per stage (two warps); CTAs never wait on each other.
 template <unsigned WHAT>
-__global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel(const EvalParams P, int item0) {
+__global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_tile_kernel(const EvalParams P, int item0) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
         cp_commit();
         // ---- B: balance rounds, next gathers, sum rounds -------------------------
         if (need_c || need_f) {
-            for (int r = warp; r < H->nRB; r += 2) {
+            for (int r = warp; r < H->nRB; r += TILE_WARPS) {
                 const unsigned short* rd = bround + 6 * r;
                 const int base = rd[0], dmax = rd[1], gbase = rd[2], gmax = rd[3], wd = rd[4];
                 const unsigned item = bitem[32 * r + lane];
@@ -657,9 +661,9 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
             // chains per lane)
             const int r0 = 0;
             const int r1 = (need_j || need_h) ? H->nRJ + H->nRH : 0;
-            for (int r = r0 + warp; r < r1; r += 4) {
-                const bool two = r + 2 < r1;
-                const int rb = two ? r + 2 : r;
+            for (int r = r0 + warp; r < r1; r += 2 * TILE_WARPS) {
+                const bool two = r + TILE_WARPS < r1;
+                const int rb = two ? r + TILE_WARPS : r;
                 const int ca = sround[4 * r + 1], cb = two ? sround[4 * rb + 1] : 0;
                 const int wa = sround[4 * r + 2], wb = sround[4 * rb + 2];
                 const double* ra = A + sround[4 * r] + lane;
@@ -690,7 +694,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / 2) acopf_tile_kernel
         // planner aligns them), else 16 threads with 16-byte stores ----------
         {
             const int seg = tid >> 4, sub = tid & 15;
-            const bool on = seg < 2 ? need_j : need_h;
+            const bool on = seg < 2 ? need_j : (seg < 4 && need_h);
             if (on) {
                 const long long go = (&R.oP)[seg];
                 double* g = (seg < 2 ? P.jval : P.hval) + go;

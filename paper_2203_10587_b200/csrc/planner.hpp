@@ -56,7 +56,11 @@ constexpr int HSLOT_F[10] = {0, 1, 5, 2, -1, 3, -1, 6, 4, -1};
 constexpr int HSLOT_T[10] = {-1, 1, -1, 2, 0, 3, 5, -1, 4, 6};
 
 #ifndef ACOPF_TILE_ENDS
+#ifdef ACOPF_TILE_WARPS
+#define ACOPF_TILE_ENDS (32 * ACOPF_TILE_WARPS)
+#else
 #define ACOPF_TILE_ENDS 64
+#endif
 #endif
 #ifndef ACOPF_TILE_BUSES
 #define ACOPF_TILE_BUSES 64
