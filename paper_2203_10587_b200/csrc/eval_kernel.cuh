@@ -306,8 +306,8 @@ __device__ __forceinline__ void bus_terms(const EvalParams& P, const DRec& R, co
     }
 }
 
-// Phase A for one branch end; SIDE 0 / 1: the end is a from- / to-end (known at
-// compile time), 2: either (the kernel's case; side-dependent values selected):
+// Phase A for one branch end, from- or to-end (side-dependent values are
+// selected, so a warp holding both sides does not diverge):
 // acopf.py:230-250 (flows, partials), 290-311 (Jacobian), 313-369 (Hessian),
 // in the reference's association with no contraction.  Each of the end's 18
 // stores goes to the area slot its consumer reads (planner.hpp).
@@ -318,13 +318,11 @@ __device__ __forceinline__ void bus_terms(const EvalParams& P, const DRec& R, co
 // negation of the matching product of positions 0, 2 and 3; round-to-nearest
 // is symmetric under negation, so v1 = -v0, v5 = -v2, v6 = -v3 bitwise, and
 // v4 = v0 (the squared partials agree).  An end evaluates 5 positions.
-template <int SIDE>
 __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, const TileView& V, int e,
                                          const EndIn& in, const double* G, unsigned char* sA, bool need_j, bool need_h,
                                          bool need_c, bool need_f, bool need_g) {
     const int nE = V.H->nE;
-    // SIDE 0 / 1: a warp of from- / to-ends (compile-time); 2: either (selects)
-    const bool sd = SIDE == 2 ? (e >= V.H->nF) : (SIDE == 1);
+    const bool sd = e >= V.H->nF;            // ends are sorted from-ends first
     const double* adm = V.adm + e;
     const double gff = adm[0], bff = adm[nE], gft = adm[2 * nE], bft = adm[3 * nE];
     const double gtf = adm[4 * nE], btf = adm[5 * nE], gtt = adm[6 * nE], btt = adm[7 * nE];
@@ -417,17 +415,10 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
         const double v8 = hval(cpf, cqf, cpt, cqt, s2f, s2t, u, w, u2, w2,
                                gpf2, gpf3, gqf2, gqf3, gpt2, gpt3, gqt2, gqt3);
         // position 7 (vf, vf) of a from-end, position 9 (vt, vt) of a to-end
-        double v79;
-        if constexpr (SIDE == 2) {     // operand selects: one position evaluation
-            const double a0 = sd ? gpf3 : gpf2, a1 = sd ? gqf3 : gqf2, a2 = sd ? gpt3 : gpt2, a3 = sd ? gqt3 : gqt2;
-            v79 = hval(cpf, cqf, cpt, cqt, s2f, s2t, sd ? z : g2ff, sd ? z : m2bff, sd ? g2tt : z, sd ? m2btt : z,
-                       a0, a0, a1, a1, a2, a2, a3, a3);
-        } else {
-            v79 = SIDE ? hval(cpf, cqf, cpt, cqt, s2f, s2t, z, z, g2tt, m2btt,
-                              gpf3, gpf3, gqf3, gqf3, gpt3, gpt3, gqt3, gqt3)
-                       : hval(cpf, cqf, cpt, cqt, s2f, s2t, g2ff, m2bff, z, z,
-                              gpf2, gpf2, gqf2, gqf2, gpt2, gpt2, gqt2, gqt2);
-        }
+        // position 7 (from-end) / 9 (to-end): one evaluation with selected operands
+        const double a0 = sd ? gpf3 : gpf2, a1 = sd ? gqf3 : gqf2, a2 = sd ? gpt3 : gpt2, a3 = sd ? gqt3 : gqt2;
+        const double v79 = hval(cpf, cqf, cpt, cqt, s2f, s2t, sd ? z : g2ff, sd ? z : m2bff, sd ? g2tt : z,
+                                sd ? m2btt : z, a0, a0, a1, a1, a2, a2, a3, a3);
         const double v5s = sd ? -v3 : v2;      // slot 5: position 2 (from) / 6 (to)
         const unsigned d4 = dw[4], d5 = dw[5], d6 = dw[6];
         sts64(sA + (d4 & 0xffffu), v0);          // slot 0: position 0 / 4
@@ -441,17 +432,15 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
     }
 }
 
-template <int SIDE>
-__device__ __forceinline__ void ends_phase(const EvalParams& P, const DRec& R, const TileView& V, int lane,
+__device__ __forceinline__ void ends_phase(const EvalParams& P, const DRec& R, const TileView& V, int tid,
                                            const EndIn& pre, const double* G, unsigned char* sA, bool need_j,
                                            bool need_h, bool need_c, bool need_f, bool need_g) {
-    const int e0 = SIDE == 2 ? 0 : (SIDE ? V.H->nF : 0), e1 = SIDE == 2 ? V.H->nE : (SIDE ? V.H->nE : V.H->nF);
-    const int stride = SIDE == 2 ? TILE_THREADS : 32;
-    if (e0 + lane < e1) end_eval<SIDE>(P, R, V, e0 + lane, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
-    for (int e = e0 + lane + stride; e < e1; e += stride) {     // beyond one end per thread: unprefetched
+    const int nE = V.H->nE;
+    if (tid < nE) end_eval(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
+    for (int e = tid + TILE_THREADS; e < nE; e += TILE_THREADS) {     // beyond one end per thread: unprefetched
         EndIn in;
         load_end(P, R, V, e, need_h, need_c, in);
-        end_eval<SIDE>(P, R, V, e, in, nullptr, sA, need_j, need_h, need_c, need_f, need_g);
+        end_eval(P, R, V, e, in, nullptr, sA, need_j, need_h, need_c, need_f, need_g);
     }
 }
 
@@ -614,7 +603,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         const int nb = R.nb;
         // ---- A: branch ends (one side per warp), generator set-points ----------
         if (any_a) {
-            ends_phase<2>(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
+            ends_phase(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
         }
         if (need_c) gens_phase(P, R, V, tid, G, sA);
         if (any_a)
