@@ -506,11 +506,11 @@ __device__ __forceinline__ void copy_seg16(double* g, const double* s, int L, in
 //      values are selected, so a warp holding both sides does not diverge);
 //      the first end of each bus also stores the bus's shunt terms and loads;
 //      thread = generator: its set-points into the balance rounds.
-//   B. balance rounds: lane = (bus, P|Q), P/Q balance rows in np.add.at order
-//      (acopf.py:252-288); the next stage's gathers are issued; sum rounds:
-//      lane = multi-term entry, left-to-right sum in scipy's duplicate order
-//      (planner.hpp).  Rounds are warp-uniform loops over padded runs.
-//   C. the four staged segments are copied to their contiguous CSR runs.
+//   B. the next stage's gathers are issued; sum rounds: lane = multi-term
+//      entry (J/H duplicate sums in scipy's order, balance sums in np.add.at
+//      order), left-to-right over its contiguous -0.0-padded run.
+//   C. the four staged segments leave by TMA bulk stores; the balance
+//      epilogue finishes the P/Q balance rows (loads and generators).
 // Three CTA barriers per stage (two warps); CTAs never wait on each other.
 template <unsigned WHAT>
 __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_tile_kernel(const EvalParams P, int item0) {
@@ -568,13 +568,13 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
 
     const unsigned short* sround = reinterpret_cast<const unsigned short*>(smem + H->o_sround);
     const unsigned short* sdst = reinterpret_cast<const unsigned short*>(smem + H->o_sdst);
-    const unsigned short* bround = reinterpret_cast<const unsigned short*>(smem + H->o_bround);
-    const unsigned short* bitem = reinterpret_cast<const unsigned short*>(smem + H->o_bitem);
     {
         const unsigned short* cpos = reinterpret_cast<const unsigned short*>(smem + H->o_const);
         const unsigned short* nega = reinterpret_cast<const unsigned short*>(smem + H->o_nega);
         for (int i = tid; i < H->nConst; i += TILE_THREADS) A[cpos[i]] = 1.0;
         for (int i = tid; i < H->nNegA; i += TILE_THREADS) A[nega[i]] = -0.0;
+        const unsigned short* zpos = reinterpret_cast<const unsigned short*>(smem + H->o_zero);
+        for (int i = tid; i < H->nZero; i += TILE_THREADS) A[zpos[i]] = 0.0;
     }
     const int my_e = tid;
     const bool any_a = need_j || need_h || need_c || need_f || need_g;
@@ -621,35 +621,11 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         if (more) prefetch(P, ctx[(ri + 1) & 1], V, my_e, tid, sG, need_h, need_c, pre);
         cp_commit();
         // ---- B: balance rounds, next gathers, sum rounds -------------------------
-        if (need_c || need_f) {
-            for (int r = warp; r < H->nRB; r += TILE_WARPS) {
-                const unsigned short* rd = bround + 6 * r;
-                const int base = rd[0], dmax = rd[1], gbase = rd[2], gmax = rd[3], wd = rd[4];
-                const unsigned item = bitem[32 * r + lane];
-                const bool on = item != 0xffffu;
-                const int bl = on ? (int)(item & 0x7fffu) : 0;
-                const int qc = (item >> 15) & 1;
-                const double* run = A + base + lane;
-                double p = 0.0;
-#pragma unroll 4
-#pragma unroll 4
-                for (int j = 0; j < dmax; ++j, run += wd) p = p + run[0];
-                const int i = b0 + bl;
-                if (on && need_f) P.inj[R.inj_off + (qc ? nb : 0) + i] = p;     // Engine.injections (acopf.py:252-264)
-                if (need_c) {
-                    double c = -(A[V.bqd[(5 + qc) * H->nB + bl]] + p);
-                    const double* gq = A + gbase + lane;
-#pragma unroll 2
-                    for (int j = 0; j < gmax; ++j, gq += wd) c = c + gq[0];
-                    if (on) P.cons[eq_row + (qc ? nb : 0) + i] = c;
-                }
-            }
-        }
         {
             // each warp takes rounds r and r + 2 together (two independent
             // chains per lane)
             const int r0 = 0;
-            const int r1 = (need_j || need_h) ? H->nRJ + H->nRH : 0;
+            const int r1 = (need_j || need_h || need_c || need_f) ? H->nRJ + H->nRH : 0;
             for (int r = r0 + warp; r < r1; r += 2 * TILE_WARPS) {
                 const bool two = r + TILE_WARPS < r1;
                 const int rb = two ? r + TILE_WARPS : r;
@@ -705,6 +681,23 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
                     }
                 } else {
                     copy_seg16(g, sp, L, sub);
+                }
+            }
+        }
+        // ---- balance epilogue: P/Q balance rows -(pd + p) + generators in order
+        // (acopf.py:277-283) and the injections p (W_FLOWS, acopf.py:252-264) ----
+        if (need_c || need_f) {
+            const int nB = H->nB, ngl = H->ngl;
+            const unsigned short* gptr = reinterpret_cast<const unsigned short*>(smem + H->o_gptr);
+            for (int k = tid; k < 2 * nB; k += TILE_THREADS) {
+                const int bl = k >> 1, qc = k & 1, i = b0 + bl;
+                const double p = A[H->pbase + k];
+                if (need_f) P.inj[R.inj_off + (qc ? nb : 0) + i] = p;
+                if (need_c) {
+                    double c = -(A[V.bqd[(5 + qc) * nB + bl]] + p);
+                    const double* gv = A + H->gbase + (qc ? ngl : 0);
+                    for (int g = gptr[bl]; g < gptr[bl + 1]; ++g) c = c + gv[g];
+                    P.cons[eq_row + (qc ? nb : 0) + i] = c;
                 }
             }
         }

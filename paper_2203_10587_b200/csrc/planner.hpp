@@ -284,7 +284,7 @@ constexpr int NST = 18;           // stores per end: 15 quantities, P flow, Q fl
 constexpr int ST_FP = 15, ST_FQ = 16, ST_X13 = 17;
 constexpr int NADM = 8;           // per end: gff bff gft bft gtf btf gtt btt
 
-struct TileHdr {                      // 160 bytes; section offsets in bytes from the header start
+struct TileHdr {                      // 192 bytes; section offsets in bytes from the header start
     int32_t b0, nB, nE, nF;           // first bus, buses, ends, from-ends (ends [0,nF) are from-ends)
     int32_t L[4];                     // entries of the four row segments
     int32_t nArea, nRJ, nRH, nRB;     // area doubles; sum rounds (J, H); balance rounds
@@ -295,8 +295,10 @@ struct TileHdr {                      // 160 bytes; section offsets in bytes fro
     int32_t o_bs, o_glist, o_gdst, o_bqd;
     int32_t o_sround, o_sdst, o_bround, o_bitem;
     int32_t o_const, o_nega, o_rep, so23;   // ...; segment starts 2|3 << 16
+    int32_t pbase, gbase, nZero, o_zero;    // balance results, generator slots, +0.0 slots
+    int32_t o_gptr, pad5, pad6, pad7;
 };
-static_assert(sizeof(TileHdr) == 160, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 192, "TileHdr layout");
 
 struct TileTable {
     int topo = 0;
@@ -320,6 +322,9 @@ struct TileTable {
     std::vector<uint16_t> gdst;   // 2 x ngl: gen-round slot of each generator's Pg, Qg
     std::vector<uint16_t> cpos;   // area slots holding the constant 1.0
     std::vector<uint16_t> nega;   // area slots holding -0.0 (round padding)
+    std::vector<uint16_t> zpos;   // area slots holding +0.0 (the first term of every balance sum)
+    std::vector<uint16_t> gptr;   // nB+1: each bus's generators in tile order
+    int pbase = 0, gbase = 0;     // balance sums' results; generator set-points
     std::vector<int> rep;         // per end: its bus (tile-local) if it is the bus's first end, else -1
     std::vector<uint16_t> orph;   // buses without branch ends (tile-local)
     // shift_mask bit s: one free slot before staging segment s (aligns the
@@ -343,7 +348,8 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob, unsi
     };
     auto remap16 = [&](std::vector<uint16_t> v) { for (auto& x : v) x = (uint16_t)remap(x); return v; };
     const std::vector<uint16_t> dstR = remap16(dst), bqdR = remap16(bqd), cposR = remap16(cpos),
-                                negaR = remap16(nega), gdstR = remap16(gdst), sdstR = remap16(sdst);
+                                negaR = remap16(nega), gdstR = remap16(gdst), sdstR = remap16(sdst),
+                                zposR = remap16(zpos);
     std::vector<uint16_t> sroundR = sround, broundR = bround;
     for (size_t r = 0; r < sroundR.size() / 4; ++r) sroundR[4 * r] = (uint16_t)remap(sroundR[4 * r]);
     for (size_t r = 0; r < broundR.size() / 6; ++r) {
@@ -375,6 +381,9 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob, unsi
     h.tslot = remap(tslot);
     h.so01 = (S[0] + cum[0]) | ((S[1] + cum[1]) << 16);
     h.so23 = (S[2] + cum[2]) | ((S[3] + cum[3]) << 16);
+    h.pbase = remap(pbase);
+    h.gbase = remap(gbase);
+    h.nZero = (int)zpos.size();
     h.ngl = (int)glist.size();
     h.nConst = (int)cpos.size(); h.nNegA = (int)nega.size(); h.nOrph = (int)orph.size();
     size_t off = sizeof(TileHdr);
@@ -399,6 +408,8 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob, unsi
     h.o_nega = take(2 * nega.size());
     h.o_rep = take(4 * rep.size());
     h.o_orph = take(2 * orph.size());
+    h.o_zero = take(2 * zpos.size());
+    h.o_gptr = take(2 * gptr.size());
     h.bytes = (int)off;
     size_t base = blob.size();
     blob.resize(base + off, 0);
@@ -432,6 +443,8 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob, unsi
     put(h.o_nega, negaR.data(), 2 * nega.size());
     put(h.o_rep, rep.data(), 4 * rep.size());
     put(h.o_orph, orph.data(), 2 * orph.size());
+    put(h.o_zero, zposR.data(), 2 * zposR.size());
+    put(h.o_gptr, gptr.data(), 2 * gptr.size());
 }
 
 inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
@@ -477,9 +490,10 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         }
     // locations: each term use gets one slot; -1 = not yet placed
     std::vector<int> loc_e((size_t)NST * nE, -1), loc_b((size_t)NQB * nB, -1);
-    std::vector<int> cpos, nega;
+    std::vector<int> cpos, nega, zpos;
     auto place = [&](const Sym& y, int slot) {
         if (y.kind == 2) { cpos.push_back(slot); return; }
+        if (y.kind == 3) { zpos.push_back(slot); return; }
         if (y.kind == 1) {
             int& l = loc_b[(size_t)y.q * nB + (y.a - b0)];
             if (l >= 0) throw std::runtime_error("planner: bus quantity used twice");
@@ -493,47 +507,55 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         if (y.q != Q_H + 5 || l2 >= 0) throw std::runtime_error("planner: unexpected reuse of an end quantity");
         l2 = slot;
     };
-    struct Sum { int dst; int row, entry, n; };
-    std::vector<Sum> sums[2];
+    struct Sum { int dst; std::vector<Sym> t; };
+    std::vector<Sum> sums;
     int pos = 0;
     for (int s = 0; s < 4; ++s)
         for (int r = 0; r < nB; ++r) {
             const Row& row = rows[s * nB + r];
             for (size_t e = 0; e < row.cols.size(); ++e, ++pos) {
                 const int n = row.tptr[e + 1] - row.tptr[e];
-                if (n == 1) place(row.terms[row.tptr[e]], pos);
-                else sums[s / 2].push_back(Sum{pos, s * nB + r, (int)e, n});
+                if (n == 1) { place(row.terms[row.tptr[e]], pos); continue; }
+                Sum sm{pos, {}};
+                for (int t = row.tptr[e]; t < row.tptr[e + 1]; ++t) sm.t.push_back(row.terms[t]);
+                sums.push_back(std::move(sm));
             }
         }
     int next = pos;
     tt.tslot = next++;
+    // balance sums (acopf.py:252-264): per (bus, P|Q), np.add.at's accumulation
+    // 0.0 + the bus's flows in np.add.at order (from-ends, then to-ends), then
+    // its shunt term; the result p goes to slot pbase + 2 bus + P|Q, finished by
+    // the balance epilogue (-(pd + p) + generators, acopf.py:277-283)
+    tt.pbase = next;
+    next += 2 * nB;
+    for (int bl = 0; bl < nB; ++bl)
+        for (int qc = 0; qc < 2; ++qc) {
+            Sum sm{tt.pbase + 2 * bl + qc, {Sym{3, 0, 0}}};
+            for (int j = tt.busptr[bl]; j < tt.busptr[bl + 1]; ++j)
+                sm.t.push_back(Sym{0, tt.ends[tt.bend[j]], qc ? ST_FQ : ST_FP});
+            sm.t.push_back(Sym{1, b0 + bl, 3 + qc});
+            sums.push_back(std::move(sm));
+        }
     // rounds: consecutive entries of a list sorted by decreasing length, up to 32
     // per round and none shorter than half the round's longest (a long duplicate
     // sum, e.g. a hub bus's diagonal, does not pad 31 short ones to its length);
-    // a round of width w keeps term j of lane l at base + w j + l
-    auto form_rounds = [](const std::vector<int>& len) {
+    // a round of width w keeps term j of lane l at base + w j + l.  J, H and
+    // balance sums share one list (fuller rounds); a what-mask that needs only
+    // some of them computes the others from stale terms into slots nobody reads
+    {
+        std::stable_sort(sums.begin(), sums.end(), [](const Sum& x, const Sum& y) { return x.t.size() > y.t.size(); });
         std::vector<std::pair<int, int>> rr;       // (first, width)
         size_t i = 0;
-        while (i < len.size()) {
-            const int cmax = len[i];
+        while (i < sums.size()) {
+            const size_t cmax = sums[i].t.size();
             size_t k = i + 1;
-            while (k < len.size() && k - i < 32 && 2 * len[k] >= cmax) ++k;
+            while (k < sums.size() && k - i < 32 && 2 * sums[k].t.size() >= cmax) ++k;
             rr.push_back({(int)i, (int)(k - i)});
             i = k;
         }
-        return rr;
-    };
-    // J and H sums share one list (fuller rounds); a what-mask without J or H only
-    // computes sums into staging segments that are not copied out
-    sums[0].insert(sums[0].end(), sums[1].begin(), sums[1].end());
-    sums[1].clear();
-    for (int c = 0; c < 2; ++c) {
-        std::stable_sort(sums[c].begin(), sums[c].end(), [](const Sum& x, const Sum& y) { return x.n > y.n; });
-        std::vector<int> len;
-        for (const Sum& sm : sums[c]) len.push_back(sm.n);
-        const auto rr = form_rounds(len);
         for (auto [first, width] : rr) {
-            const int cmax = len[first];
+            const int cmax = (int)sums[first].t.size();
             const int base = next;
             next += width * cmax;
             tt.sround.push_back((uint16_t)base);
@@ -542,66 +564,26 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             tt.sround.push_back(0);
             for (int l = 0; l < 32; ++l) {
                 if (l >= width) { tt.sdst.push_back((uint16_t)tt.tslot); continue; }
-                const Sum& sm = sums[c][first + l];
-                const Row& row = rows[sm.row];
+                const Sum& sm = sums[first + l];
                 tt.sdst.push_back((uint16_t)sm.dst);
                 for (int j = 0; j < cmax; ++j) {
-                    if (j < sm.n) place(row.terms[row.tptr[sm.entry] + j], base + width * j + l);
+                    if (j < (int)sm.t.size()) place(sm.t[j], base + width * j + l);
                     else nega.push_back(base + width * j + l);
                 }
             }
         }
-        (c == 0 ? tt.nRJ : tt.nRH) = (int)rr.size();
+        tt.nRJ = (int)rr.size();
+        tt.nRH = 0;
     }
-    // balance rounds: (bus, P|Q) items by decreasing degree; a run holds the
-    // bus's flows in np.add.at order, then its shunt term; the generators'
-    // Pg (Qg) follow in the gen rounds
+    // generator set-points: Pg at gbase + g, Qg at gbase + ngl + g (tile order)
     for (int i = b0; i < b1; ++i) tt.ngl += T.gen_ptr[i + 1] - T.gen_ptr[i];
-    std::vector<int> gfirst(nB + 1, 0);
-    for (int bl = 0; bl < nB; ++bl) gfirst[bl + 1] = gfirst[bl] + T.gen_ptr[b0 + bl + 1] - T.gen_ptr[b0 + bl];
-    std::vector<int> items;
-    for (int bl = 0; bl < nB; ++bl) { items.push_back(2 * bl); items.push_back(2 * bl + 1); }
-    auto deg = [&](int it) { return tt.busptr[(it >> 1) + 1] - tt.busptr[it >> 1]; };
-    std::stable_sort(items.begin(), items.end(), [&](int x, int y) { return deg(x) > deg(y); });
-    tt.gdst.assign(2 * (size_t)tt.ngl, 0);
-    std::vector<int> blen;
-    for (int it : items) blen.push_back(deg(it) + 1);
-    for (auto [first, width] : form_rounds(blen)) {
-        int dmax = 0, gmax = 0;
-        for (int l = 0; l < width; ++l) {
-            const int it = items[first + l];
-            dmax = std::max(dmax, deg(it) + 1);
-            gmax = std::max(gmax, gfirst[(it >> 1) + 1] - gfirst[it >> 1]);
-        }
-        const int base = next;
-        next += width * dmax;
-        const int gbase = next;
-        next += width * gmax;
-        tt.bround.push_back((uint16_t)base);
-        tt.bround.push_back((uint16_t)dmax);
-        tt.bround.push_back((uint16_t)gbase);
-        tt.bround.push_back((uint16_t)gmax);
-        tt.bround.push_back((uint16_t)width);
-        tt.bround.push_back(0);
-        for (int l = 0; l < 32; ++l) {
-            if (l >= width) { tt.bitem.push_back(0xffff); continue; }
-            const int it = items[first + l], bl = it >> 1, qc = it & 1;
-            tt.bitem.push_back((uint16_t)(bl | (qc << 15)));
-            const int d = deg(it);
-            for (int j = 0; j < dmax; ++j) {
-                const int v = base + width * j + l;
-                if (j < d) loc_e[(size_t)(qc ? ST_FQ : ST_FP) * nE + tt.bend[tt.busptr[bl] + j]] = v;
-                else if (j == d) loc_b[(size_t)(3 + qc) * nB + bl] = v;
-                else nega.push_back(v);
-            }
-            const int ng = gfirst[bl + 1] - gfirst[bl];
-            for (int j = 0; j < gmax; ++j) {
-                const int v = gbase + width * j + l;
-                if (j < ng) tt.gdst[(size_t)qc * tt.ngl + gfirst[bl] + j] = (uint16_t)v;
-                else nega.push_back(v);
-            }
-        }
-    }
+    tt.gbase = next;
+    next += 2 * tt.ngl;
+    tt.gdst.resize(2 * (size_t)tt.ngl);
+    for (int g = 0; g < 2 * tt.ngl; ++g) tt.gdst[g] = (uint16_t)(tt.gbase + g);
+    tt.gptr.assign(1, 0);
+    for (int bl = 0; bl < nB; ++bl)
+        tt.gptr.push_back((uint16_t)(tt.gptr.back() + T.gen_ptr[b0 + bl + 1] - T.gen_ptr[b0 + bl]));
     next += 32;        // margin: lanes beyond a round's width read (and discard) up to 31 slots past it
     // pd, qd of every bus; the representative (first) end of every bus
     for (int bl = 0; bl < nB; ++bl) {
@@ -618,6 +600,7 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     if (nB >= 0x8000) throw std::runtime_error("tile has too many buses");
     for (int v : cpos) tt.cpos.push_back((uint16_t)v);
     for (int v : nega) tt.nega.push_back((uint16_t)v);
+    for (int v : zpos) tt.zpos.push_back((uint16_t)v);
     tt.dst.resize(loc_e.size());
     for (size_t i = 0; i < loc_e.size(); ++i) tt.dst[i] = (uint16_t)(loc_e[i] < 0 ? tt.tslot : loc_e[i]);
     tt.bqd.resize(loc_b.size());
@@ -648,6 +631,10 @@ inline std::string verify_tile(const TileTable& tt) {
         if (!slot_ok(v)) return "constant outside the area";
         prod[v]++;
     }
+    for (int v : tt.zpos) {
+        if (!slot_ok(v)) return "zero constant outside the area";
+        prod[v]++;
+    }
     for (int v : tt.nega) {
         if (!slot_ok(v)) return "padding outside the area";
         pad[v]++;
@@ -669,10 +656,7 @@ inline std::string verify_tile(const TileTable& tt) {
                 if (d != tt.tslot) return "idle sum lane not sent to the trash slot";
                 continue;
             }
-            if (d != tt.tslot) {
-                if (d >= T) return "sum destination outside the staging segments";
-                prod[d]++;
-            }
+            if (d != tt.tslot) prod[d]++;
             for (int j = 0; j < c; ++j) read[base + w * j + l]++;
         }
     }
@@ -687,6 +671,8 @@ inline std::string verify_tile(const TileTable& tt) {
             for (int j = 0; j < g; ++j) read[gb + w * j + l]++;
         }
     }
+    for (int k = 0; k < 2 * nB; ++k)
+        if (prod[tt.pbase + k] != 1) return "balance result without exactly one producer";
     for (int v = 0; v < tt.nArea; ++v) {
         if (v == tt.tslot) continue;
         if (prod[v] > 1) return "area slot with more than one producer";
