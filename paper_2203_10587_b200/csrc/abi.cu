@@ -328,6 +328,8 @@ static void upload(acopf_batch* b) {
     P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
     P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
     b->smem = (max_smem + 15) & ~size_t(15);
+    // development aid: extra shared memory per CTA (lowers the resident CTAs per SM)
+    if (const char* e = getenv("ACOPF_SMEM_PAD_KB")) b->smem += 1024 * (size_t)atoi(e);
     b->aux_smem = sizeof(double) * max_leaf;
     for (auto fn : {acopf_tile_kernel<0u>, acopf_tile_kernel<ACOPF_ALL>})
         cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -564,7 +566,7 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         P.x = x; P.mult = mult; P.obj_factor = obj_factor; P.what = what;
         P.obj = obj; P.grad = grad; P.cons = cons; P.jval = jval; P.hval = hval;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
-        const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD)) && P.n_bus_items > 0;
+        const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) && P.n_bus_items > 0;
         static const bool no_aux = getenv("ACOPF_EXP_NO_AUX") != nullptr;   // development aid: tile kernel alone
         const bool aux = !no_aux && (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
         // the generator/coupling kernel runs concurrently on a forked stream
@@ -663,7 +665,7 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
                     cuda_check(cudaGetLastError(), "acopf_aux_kernel launch");
                     b->launches++;
                 }
-                if (pc.bus_count && (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS | ACOPF_GRAD))) {
+                if (pc.bus_count && (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS))) {
                     if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<pc.bus_count, TILE_THREADS, b->smem, cs>>>(P, pc.bus_first);
                     else acopf_tile_kernel<0u><<<pc.bus_count, TILE_THREADS, b->smem, cs>>>(P, pc.bus_first);
                     cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
@@ -800,7 +802,7 @@ int64_t acopf_batch_launches(const acopf_batch* b) { return b ? b->launches : 0;
 
 int acopf_batch_verify(const acopf_batch* b, int64_t* stats) {
     return guard([&] {
-        int64_t ntiles = 0, nends = 0, area = 0, pads = 0, smem = 0;
+        int64_t ntiles = 0, nends = 0, area = 0, pads = 0, smem = 0, rounds = 0, lane_terms = 0, chain = 0;
         for (size_t ti = 0; ti < b->topos.size(); ++ti) {
             ntiles += (int64_t)b->base_table[ti].size();
             for (int id : b->base_table[ti]) nends += (int64_t)b->tables[id].ends.size();
@@ -813,11 +815,17 @@ int acopf_batch_verify(const acopf_batch* b, int64_t* stats) {
             tt.serialise(*b->topos[tt.topo], blob);
             area += tt.nArea;
             pads += (int64_t)tt.nega.size();
+            for (size_t r = 0; r < tt.sround.size() / 4; ++r) {
+                ++rounds;
+                lane_terms += (int64_t)tt.sround[4 * r + 1] * tt.sround[4 * r + 2];
+                chain += tt.sround[4 * r + 1];
+            }
             smem = std::max<int64_t>(smem, (int64_t)tile_smem_bytes((int)blob.size(), tt.nArea));
         }
         if (stats) {
             stats[0] = (int64_t)b->tables.size(); stats[1] = ntiles; stats[2] = nends;
             stats[3] = area; stats[4] = pads; stats[5] = smem;
+            stats[6] = rounds; stats[7] = lane_terms; stats[8] = chain;
         }
     });
 }

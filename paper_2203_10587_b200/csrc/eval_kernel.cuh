@@ -2,12 +2,12 @@
 // atomics, built with -fmad=false so every expression rounds exactly like the
 // reference's numpy evaluation).
 //
-// acopf_tile_kernel -- one warp (one 32-thread CTA) = one tile of consecutive
-// buses (<= 32 branch ends) evaluated for a run of stages that share the
-// tile's table.  Warps are independent (no CTA-wide barriers): lanes are
-// branch ends in phase A, buses / sum entries in phase B, and copy the
-// tile's staged CSR segments out contiguously in phase C.  Details at the
-// kernel.
+// acopf_tile_kernel -- one 64-thread CTA = one tile of consecutive buses
+// (<= 64 branch ends) evaluated for a run of stages that share the tile's
+// table.  Per stage, threads are branch ends in phase A, sum-round lanes in
+// phase B, and issue the bulk copy-out of the staged CSR segments and the
+// balance epilogue in phase C; three CTA barriers per stage, CTAs never wait
+// on each other.  Details at the kernel.
 //
 // acopf_aux_kernel -- generator chunks (gradient, PG Hessian diagonal, the
 // stage objective by numpy's pairwise sum, the weighted composite sum in
@@ -234,8 +234,14 @@ __device__ __forceinline__ void prefetch(const EvalParams& P, const DRec& R, con
         in.st = 0.0;
         if (r >= 0) {
             const double* mi = P.mult + R.ineq_row + 2 * in.rs;
-            in.sf = __ldg(mi);
-            in.st = __ldg(mi + 1);
+            if ((reinterpret_cast<uintptr_t>(P.mult + R.ineq_row) & 15) == 0) {   // stage-uniform
+                const double2 m2 = __ldg(reinterpret_cast<const double2*>(mi));
+                in.sf = m2.x;
+                in.st = m2.y;
+            } else {
+                in.sf = __ldg(mi);
+                in.st = __ldg(mi + 1);
+            }
         }
     }
 }
@@ -277,12 +283,12 @@ __device__ __forceinline__ void sts64(unsigned char* addr, double v) {
 }
 
 // A bus's own terms (acopf.py:262-263, 283, 296-297, 366): shunt Jacobian and
-// Hessian entries, the shunt terms of its balance rows, its loads, and its
-// zero gradient entries.  Computed by the bus's first branch end (or, for a
-// bus without branches, by the orphan loop).
+// Hessian entries, the shunt terms of its balance rows and its loads.
+// Computed by the bus's first branch end (or, for a bus without branches, by
+// the orphan loop).
 __device__ __forceinline__ void bus_terms(const EvalParams& P, const DRec& R, const TileView& V, int rb, double vm,
                                           double mp, double mq, double pd, double qd, unsigned char* sA, bool need_j,
-                                          bool need_h, bool need_c, bool need_f, bool need_g) {
+                                          bool need_h, bool need_c, bool need_f) {
     const int nB = V.H->nB;
     const double gsb = V.gs[rb], bsb = V.bs[rb];
     const unsigned short* q = V.bqd + rb;
@@ -298,11 +304,6 @@ __device__ __forceinline__ void bus_terms(const EvalParams& P, const DRec& R, co
     if (need_c) {
         sts64(sA + 8u * q[5 * nB], pd);
         sts64(sA + 8u * q[6 * nB], qd);
-    }
-    if (need_g) {
-        const int i = V.H->b0 + rb;
-        P.grad[R.var_off + i] = R.w * 0.0;
-        P.grad[R.var_off + R.nb + i] = R.w * 0.0;
     }
 }
 
@@ -320,7 +321,7 @@ __device__ __forceinline__ void bus_terms(const EvalParams& P, const DRec& R, co
 // v4 = v0 (the squared partials agree).  An end evaluates 5 positions.
 __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, const TileView& V, int e,
                                          const EndIn& in, const double* G, unsigned char* sA, bool need_j, bool need_h,
-                                         bool need_c, bool need_f, bool need_g) {
+                                         bool need_c, bool need_f) {
     const int nE = V.H->nE;
     const bool sd = e >= V.H->nF;            // ends are sorted from-ends first
     const double* adm = V.adm + e;
@@ -332,7 +333,11 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
     const double vf = in.vf, vt = in.vt;
     const double th = in.vaf - in.vat;
     double sn, cs;
+#ifdef ACOPF_DIAG_NO_SINCOS
+    sn = th; cs = th * th;
+#else
     libm_sincos(th, &sn, &cs);
+#endif
     const double u = gft * cs + bft * sn;
     const double w = gft * sn - bft * cs;
     const double u2 = gtf * cs - btf * sn;
@@ -365,7 +370,7 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
             }
         }
         bus_terms(P, R, V, rb, sd ? vt : vf, sd ? in.mpt : in.mpf, sd ? in.mqt : in.mqf, pdv, qdv, sA,
-                  need_j, need_h, need_c, need_f, need_g);
+                  need_j, need_h, need_c, need_f);
     }
     if (!(need_j || need_h)) return;
     const double gpf0 = (-vv) * w, gpf2 = g2ff * vf + vt * u, gpf3 = vf * u;
@@ -391,9 +396,19 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
             const double r2 = (0.0 + tp * gp2) + tq * gq2, r3 = (0.0 + tp * gp3) + tq * gq3;
             const int f = V.f[e], t = V.t[e];
             double* out = P.jval + R.jineq + in.fo + (f == t ? 2 : 4) * (int)sd;
-            if (f < t) { out[0] = r0; out[1] = r1; out[2] = r2; out[3] = r3; }
-            else if (f > t) { out[0] = r1; out[1] = r0; out[2] = r3; out[3] = r2; }
-            else { out[0] = r0 + r1; out[1] = r2 + r3; }
+            // rows have even lengths: 16-byte alignment is the stage's block's
+            const bool v2 = (reinterpret_cast<uintptr_t>(P.jval + R.jineq) & 15) == 0;
+            if (f != t) {
+                const double a0 = f < t ? r0 : r1, a1 = f < t ? r1 : r0, a2 = f < t ? r2 : r3, a3 = f < t ? r3 : r2;
+                if (v2) {
+                    reinterpret_cast<double2*>(out)[0] = make_double2(a0, a1);
+                    reinterpret_cast<double2*>(out)[1] = make_double2(a2, a3);
+                } else { out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3; }
+            } else {
+                const double a0 = r0 + r1, a1 = r2 + r3;
+                if (v2) reinterpret_cast<double2*>(out)[0] = make_double2(a0, a1);
+                else { out[0] = a0; out[1] = a1; }
+            }
         }
     }
     if (need_h) {
@@ -434,13 +449,13 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
 
 __device__ __forceinline__ void ends_phase(const EvalParams& P, const DRec& R, const TileView& V, int tid,
                                            const EndIn& pre, const double* G, unsigned char* sA, bool need_j,
-                                           bool need_h, bool need_c, bool need_f, bool need_g) {
+                                           bool need_h, bool need_c, bool need_f) {
     const int nE = V.H->nE;
-    if (tid < nE) end_eval(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
+    if (tid < nE) end_eval(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f);
     for (int e = tid + TILE_THREADS; e < nE; e += TILE_THREADS) {     // beyond one end per thread: unprefetched
         EndIn in;
         load_end(P, R, V, e, need_h, need_c, in);
-        end_eval(P, R, V, e, in, nullptr, sA, need_j, need_h, need_c, need_f, need_g);
+        end_eval(P, R, V, e, in, nullptr, sA, need_j, need_h, need_c, need_f);
     }
 }
 
@@ -532,7 +547,6 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
     // WHAT != 0: the mask is a compile-time constant (the all-callbacks path)
     const unsigned what = WHAT ? WHAT : P.what;
     const bool need_j = what & W_JAC, need_h = what & W_HESS, need_c = what & W_CONS, need_f = what & W_FLOWS;
-    const bool need_g = what & W_GRAD;
     __syncthreads();
     {
         const unsigned b = smem_u32(&bar);
@@ -577,7 +591,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         for (int i = tid; i < H->nZero; i += TILE_THREADS) A[zpos[i]] = 0.0;
     }
     const int my_e = tid;
-    const bool any_a = need_j || need_h || need_c || need_f || need_g;
+    const bool any_a = need_j || need_h || need_c || need_f;
 
     // first record and its inputs
     if (tid < 8) cp_async16(reinterpret_cast<unsigned char*>(ctx) + 16 * tid,
@@ -602,9 +616,11 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         const long long eq_row = R.eq_row;
         const int nb = R.nb;
         // ---- A: branch ends (one side per warp), generator set-points ----------
+#ifndef ACOPF_DIAG_NO_A
         if (any_a) {
-            ends_phase(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f, need_g);
+            ends_phase(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f);
         }
+#endif
         if (need_c) gens_phase(P, R, V, tid, G, sA);
         if (any_a)
             for (int k = tid; k < H->nOrph; k += TILE_THREADS) {     // buses without branches
@@ -613,42 +629,45 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
                 const double* mu = P.mult + R.eq_row;
                 bus_terms(P, R, V, rb, __ldg(x + nb + i), need_h ? __ldg(mu + i) : 0.0,
                           need_h ? __ldg(mu + nb + i) : 0.0, need_c ? __ldg(P.pd + R.pd_off + i) : 0.0,
-                          need_c ? __ldg(P.qd + R.pd_off + i) : 0.0, sA, need_j, need_h, need_c, need_f, need_g);
+                          need_c ? __ldg(P.qd + R.pd_off + i) : 0.0, sA, need_j, need_h, need_c, need_f);
             }
         cp_wait<0>();          // the next record
         __syncthreads();
         // the gather buffer is free again: prefetch the next stage's inputs
+#ifndef ACOPF_DIAG_NO_PF
         if (more) prefetch(P, ctx[(ri + 1) & 1], V, my_e, tid, sG, need_h, need_c, pre);
+#endif
         cp_commit();
         // ---- B: balance rounds, next gathers, sum rounds -------------------------
         {
             // each warp takes rounds r and r + 2 together (two independent
             // chains per lane)
             const int r0 = 0;
+#ifdef ACOPF_DIAG_NO_B
+            const int r1 = 0;
+#else
             const int r1 = (need_j || need_h || need_c || need_f) ? H->nRJ + H->nRH : 0;
+#endif
             for (int r = r0 + warp; r < r1; r += 2 * TILE_WARPS) {
                 const bool two = r + TILE_WARPS < r1;
                 const int rb = two ? r + TILE_WARPS : r;
-                const int ca = sround[4 * r + 1], cb = two ? sround[4 * rb + 1] : 0;
-                const int wa = sround[4 * r + 2], wb = sround[4 * rb + 2];
-                const double* ra = A + sround[4 * r] + lane;
-                const double* rbp = A + sround[4 * rb] + lane;
+                // descriptors (base | count << 16, width) and destinations first
+                const uint2 da = *reinterpret_cast<const uint2*>(sround + 4 * r);
+                const uint2 db = *reinterpret_cast<const uint2*>(sround + 4 * rb);
+                const unsigned oa = sdst[32 * r + lane], ob = sdst[32 * rb + lane];
+                const int ca = da.x >> 16, cb = two ? (int)(db.x >> 16) : 0;
+                const double* ra = A + (da.x & 0xffffu) + lane;
+                const double* rbp = A + (db.x & 0xffffu) + lane;
+                const int wa = da.y, wb = db.y;
                 double va = ra[0], vb = rbp[0];
-                const int cm = ca < cb ? ca : cb;
-                int j = 1;
-                ra += wa;
-                rbp += wb;
+                const int n = ca > cb ? ca : cb;
 #pragma unroll 4
-                for (; j < cm; ++j, ra += wa, rbp += wb) {
-                    va = va + ra[0];
-                    vb = vb + rbp[0];
+                for (int j = 1; j < n; ++j) {
+                    if (j < ca) va = va + ra[j * wa];
+                    if (j < cb) vb = vb + rbp[j * wb];
                 }
-#pragma unroll 4
-                for (int k = j; k < ca; ++k, ra += wa) va = va + ra[0];
-#pragma unroll 4
-                for (int k = j; k < cb; ++k, rbp += wb) vb = vb + rbp[0];
-                A[sdst[32 * r + lane]] = va;
-                if (two) A[sdst[32 * rb + lane]] = vb;
+                A[oa] = va;
+                if (two) A[ob] = vb;
             }
         }
         // staging writes (generic proxy) before the bulk stores read them (async proxy)
@@ -657,6 +676,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         // ---- C: copy-out of the staged segments: a TMA bulk store per segment
         // when its staging copy shares the output run's 16-byte parity (the
         // planner aligns them), else 16 threads with 16-byte stores ----------
+#ifndef ACOPF_DIAG_NO_C
         {
             const int seg = tid >> 4, sub = tid & 15;
             const bool on = seg < 2 ? need_j : (seg < 4 && need_h);
@@ -684,9 +704,14 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
                 }
             }
         }
+#endif
         // ---- balance epilogue: P/Q balance rows -(pd + p) + generators in order
         // (acopf.py:277-283) and the injections p (W_FLOWS, acopf.py:252-264) ----
+#ifdef ACOPF_DIAG_NO_C
+        if (false) {
+#else
         if (need_c || need_f) {
+#endif
             const int nB = H->nB, ngl = H->ngl;
             const unsigned short* gptr = reinterpret_cast<const unsigned short*>(smem + H->o_gptr);
             for (int k = tid; k < 2 * nB; k += TILE_THREADS) {
@@ -696,7 +721,11 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
                 if (need_c) {
                     double c = -(A[V.bqd[(5 + qc) * nB + bl]] + p);
                     const double* gv = A + H->gbase + (qc ? ngl : 0);
-                    for (int g = gptr[bl]; g < gptr[bl + 1]; ++g) c = c + gv[g];
+                    // warp-uniform trip count, predicated adds (no divergent loop)
+                    const int g0 = gptr[bl], n = gptr[bl + 1] - g0;
+                    const int nmax = __reduce_max_sync(__activemask(), (unsigned)n);
+                    for (int j = 0; j < nmax; ++j)
+                        if (j < n) c = c + gv[g0 + j];
                     P.cons[eq_row + (qc ? nb : 0) + i] = c;
                 }
             }
@@ -729,6 +758,13 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
     const int nb = T.nb, ng = T.ng;
     const double* pg = P.x + S.var_off + 2 * nb;
     const int g = chunk * GEN_CHUNK + threadIdx.x;
+    if (P.what & W_GRAD) {
+        // the angle and magnitude entries (acopf.py:271-275: w * 0.0), spread
+        // over the stage's generator chunks
+        const int nch = ng > GEN_CHUNK ? (ng + GEN_CHUNK - 1) / GEN_CHUNK : 1;
+        const int span = (2 * nb + nch - 1) / nch, v1 = min(2 * nb, (chunk + 1) * span);
+        for (int v = chunk * span + threadIdx.x; v < v1; v += blockDim.x) P.grad[S.var_off + v] = S.w * 0.0;
+    }
     if (g < ng) {
         if (P.what & W_GRAD) {
             const double ca = P.ca[S.cost_off + g], cb = P.cb[S.cost_off + g];

@@ -22,7 +22,7 @@
 #ifdef __CUDACC__
 #define SC_HD __host__ __device__ __forceinline__
 __device__ static const double sc_table_dev[SC_NJ * 4] = {SC_TABLE_VALUES};
-__device__ static const double sc_gl_table_dev[SC_GL_NK * 4] = {SC_GL_TABLE_VALUES};
+__device__ static const double __align__(16) sc_gl_table_dev[SC_GL_NK * 4] = {SC_GL_TABLE_VALUES};
 #else
 #define SC_HD static inline
 #endif
@@ -189,7 +189,13 @@ SC_HD void libm_sincos_t(const double* table, double x, double* sp, double* cp) 
     const double xr = axs - xk;
     const int k = (int)(xk * 128.0);
     const double* tab = table + 4 * k;
+#ifdef __CUDA_ARCH__
+    // an entry is 32 bytes (16-byte aligned table): two 128-bit loads
+    const double2 e01 = *reinterpret_cast<const double2*>(tab), e23 = *reinterpret_cast<const double2*>(tab + 2);
+    const double sn = e01.x, ssn = e01.y, cs = e23.x, ccs = e23.y;
+#else
     const double sn = tab[0], ssn = tab[1], cs = tab[2], ccs = tab[3];
+#endif
     const double xx = xr * xr;
     const double ps = fma(xx, GLK_SN5, GLK_SN3);
     const double pc = xx * fma(xx, fma(xx, GLK_CS6, GLK_CS4), GLK_CS2);
