@@ -139,11 +139,13 @@ int64_t acopf_batch_launches(const acopf_batch* b);
 /* Host check of every tile table of the batch (planner invariants, no GPU):
  * each staging position and each round term slot has exactly one producer
  * (an end or bus store, a constant, or a sum), padding slots hold -0.0, and
- * all locations lie inside the tile's area.  stats (may be NULL) receives 9
+ * all locations lie inside the tile's area.  stats (may be NULL) receives 12
  * values: tables, tiles of the base topologies, branch ends in base tiles,
  * area doubles (sum over tables), -0.0 padding slots (sum), largest tile CTA
- * shared memory in bytes, sum rounds, round lane-terms (sum of terms x width)
- * and round chain terms (sum of terms per round).  Returns nonzero with acopf_last_error() on the
+ * shared memory in bytes, sum rounds, round lane-terms (sum of terms x width),
+ * round chain terms (sum of terms per round), and the modeled shared-memory
+ * wavefronts of one stage's area stores over all tables (half-warp model,
+ * whole-warp model, conflict-free ideal).  Returns nonzero with acopf_last_error() on the
  * first violation. */
 int acopf_batch_verify(const acopf_batch* b, int64_t* stats);
 

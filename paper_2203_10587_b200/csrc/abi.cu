@@ -803,6 +803,7 @@ int64_t acopf_batch_launches(const acopf_batch* b) { return b ? b->launches : 0;
 int acopf_batch_verify(const acopf_batch* b, int64_t* stats) {
     return guard([&] {
         int64_t ntiles = 0, nends = 0, area = 0, pads = 0, smem = 0, rounds = 0, lane_terms = 0, chain = 0;
+        int64_t cost[3] = {0, 0, 0};
         for (size_t ti = 0; ti < b->topos.size(); ++ti) {
             ntiles += (int64_t)b->base_table[ti].size();
             for (int id : b->base_table[ti]) nends += (int64_t)b->tables[id].ends.size();
@@ -815,9 +816,10 @@ int acopf_batch_verify(const acopf_batch* b, int64_t* stats) {
             tt.serialise(*b->topos[tt.topo], blob);
             area += tt.nArea;
             pads += (int64_t)tt.nega.size();
+            tile_store_cost(tt, cost);
             for (size_t r = 0; r < tt.sround.size() / 4; ++r) {
                 ++rounds;
-                lane_terms += (int64_t)tt.sround[4 * r + 1] * tt.sround[4 * r + 2];
+                lane_terms += (int64_t)tt.sround[4 * r + 1] * tt.sround[4 * r + 3];
                 chain += tt.sround[4 * r + 1];
             }
             smem = std::max<int64_t>(smem, (int64_t)tile_smem_bytes((int)blob.size(), tt.nArea));
@@ -826,6 +828,7 @@ int acopf_batch_verify(const acopf_batch* b, int64_t* stats) {
             stats[0] = (int64_t)b->tables.size(); stats[1] = ntiles; stats[2] = nends;
             stats[3] = area; stats[4] = pads; stats[5] = smem;
             stats[6] = rounds; stats[7] = lane_terms; stats[8] = chain;
+            stats[9] = cost[0]; stats[10] = cost[1]; stats[11] = cost[2];
         }
     });
 }

@@ -651,14 +651,14 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
             for (int r = r0 + warp; r < r1; r += 2 * TILE_WARPS) {
                 const bool two = r + TILE_WARPS < r1;
                 const int rb = two ? r + TILE_WARPS : r;
-                // descriptors (base | count << 16, width) and destinations first
+                // descriptors (base | count << 16, stride | width << 16) and destinations first
                 const uint2 da = *reinterpret_cast<const uint2*>(sround + 4 * r);
                 const uint2 db = *reinterpret_cast<const uint2*>(sround + 4 * rb);
                 const unsigned oa = sdst[32 * r + lane], ob = sdst[32 * rb + lane];
                 const int ca = da.x >> 16, cb = two ? (int)(db.x >> 16) : 0;
                 const double* ra = A + (da.x & 0xffffu) + lane;
                 const double* rbp = A + (db.x & 0xffffu) + lane;
-                const int wa = da.y, wb = db.y;
+                const int wa = da.y & 0xffffu, wb = db.y & 0xffffu;
                 double va = ra[0], vb = rbp[0];
                 const int n = ca > cb ? ca : cb;
 #pragma unroll 4

@@ -30,6 +30,7 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+#include <array>
 
 namespace acopf {
 
@@ -447,6 +448,42 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob, unsi
     put(h.o_gptr, gptr.data(), 2 * gptr.size());
 }
 
+// Half-warp shared-memory store model used to lay out the sum rounds (see
+// tile_store_cost): per store instruction (end store kind or bus-term kind of
+// a 32-end warp, or a round's result store) and half-warp, the number of slots
+// on each 8-byte bank pair; the instruction costs the largest count.
+struct StoreModel {
+    struct Grp { int16_t cnt[16]; int16_t mx; };
+    std::vector<Grp> g;
+    int nW = 0;
+    struct Undo { int gi, bank, mx; };
+    std::vector<Undo> journal;
+    void init(int nE, int nRounds) {
+        nW = (nE + 31) / 32;
+        g.assign((size_t)nW * (NST + 7) * 2 + 2 * (size_t)std::max(nRounds, 1), Grp{});
+    }
+    int end_grp(int e, int q) const { return ((e >> 5) * NST + q) * 2 + ((e >> 4) & 1); }
+    int bus_grp(int e, int q) const { return nW * NST * 2 + ((e >> 5) * 7 + q) * 2 + ((e >> 4) & 1); }
+    int res_grp(int r, int l) const { return nW * (NST + 7) * 2 + 2 * r + (l >> 4); }
+    // add slot v to group gi; returns the instruction's cost increase
+    int add(int gi, int v, bool record) {
+        Grp& x = g[gi];
+        const int b = v & 15;
+        if (record) journal.push_back({gi, b, x.mx});
+        const int c = ++x.cnt[b];
+        if (c > x.mx) { x.mx = (int16_t)c; return 1; }
+        return 0;
+    }
+    void rollback() {
+        for (size_t i = journal.size(); i-- > 0;) {
+            Grp& x = g[journal[i].gi];
+            --x.cnt[journal[i].bank];
+            x.mx = (int16_t)journal[i].mx;
+        }
+        journal.clear();
+    }
+};
+
 inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     TileTable tt;
     const int b0 = T.tile_b0[tile], b1 = T.tile_b0[tile + 1];
@@ -540,9 +577,12 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     // rounds: consecutive entries of a list sorted by decreasing length, up to 32
     // per round and none shorter than half the round's longest (a long duplicate
     // sum, e.g. a hub bus's diagonal, does not pad 31 short ones to its length);
-    // a round of width w keeps term j of lane l at base + w j + l.  J, H and
-    // balance sums share one list (fuller rounds); a what-mask that needs only
-    // some of them computes the others from stale terms into slots nobody reads
+    // a round of width w and stride S keeps term j of lane l at base + S j + l.
+    // J, H and balance sums share one list (fuller rounds); a what-mask that
+    // needs only some of them computes the others from stale terms into slots
+    // nobody reads.  Each round's base shift (0-15 slots), stride (w or w + 1)
+    // and lane order are chosen to spread the phase-A stores of one instruction
+    // over the shared-memory banks (StoreModel).
     {
         std::stable_sort(sums.begin(), sums.end(), [](const Sum& x, const Sum& y) { return x.t.size() > y.t.size(); });
         std::vector<std::pair<int, int>> rr;       // (first, width)
@@ -554,22 +594,107 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             rr.push_back({(int)i, (int)(k - i)});
             i = k;
         }
-        for (auto [first, width] : rr) {
+        std::vector<int> rep_e(nB, -1);
+        for (int bl = 0; bl < nB; ++bl)
+            if (tt.busptr[bl + 1] > tt.busptr[bl]) rep_e[bl] = tt.bend[tt.busptr[bl]];
+        StoreModel M;
+        M.init(nE, (int)rr.size());
+        for (int e = 0; e < nE; ++e)
+            for (int q = 0; q < NST; ++q)
+                if (loc_e[(size_t)q * nE + e] >= 0) M.add(M.end_grp(e, q), loc_e[(size_t)q * nE + e], false);
+        for (int bl = 0; bl < nB; ++bl)
+            for (int q = 0; q < 5; ++q)
+                if (rep_e[bl] >= 0 && loc_b[(size_t)q * nB + bl] >= 0)
+                    M.add(M.bus_grp(rep_e[bl], q), loc_b[(size_t)q * nB + bl], false);
+        auto grp = [&](const Sym& y) -> int {
+            if (y.kind == 0) {
+                const int e = end_pos.at(y.a);
+                const int q = loc_e[(size_t)y.q * nE + e] >= 0 ? ST_X13 : y.q;
+                return M.end_grp(e, q);
+            }
+            if (y.kind == 1) {
+                const int r = rep_e[y.a - b0];
+                return r < 0 ? -1 : M.bus_grp(r, y.q);
+            }
+            return -1;
+        };
+        // cost of putting sum sm in lane l of round r at (base, stride)
+        auto sum_cost = [&](const Sum& sm, int r, int l, int base, int st) {
+            int c = 0;
+            for (size_t j = 0; j < sm.t.size(); ++j) {
+                const int gi = grp(sm.t[j]);
+                if (gi >= 0) c += M.add(gi, base + st * (int)j + l, true);
+            }
+            c += M.add(M.res_grp(r, l), sm.dst, true);
+            return c;
+        };
+        for (size_t r = 0; r < rr.size(); ++r) {
+            const int first = rr[r].first, width = rr[r].second;
             const int cmax = (int)sums[first].t.size();
-            const int base = next;
-            next += width * cmax;
+            // (shift, stride) by the identity lane order, then a greedy lane order
+            // for the best few
+            std::vector<std::array<int, 3>> cand;     // cost, shift, stride
+            for (int st = width; st <= width + (width % 2 == 0 ? 1 : 0); ++st)
+                for (int sh = 0; sh < 16; ++sh) {
+                    int c = 0;
+                    for (int l = 0; l < width; ++l) c += sum_cost(sums[first + l], (int)r, l, next + sh, st);
+                    M.rollback();
+                    cand.push_back({c, sh, st});
+                }
+            std::sort(cand.begin(), cand.end());
+            int best_c = cand[0][0], best_sh = cand[0][1], best_st = cand[0][2];
+            std::vector<int> best_lane(width);
+            for (int l = 0; l < width; ++l) best_lane[l] = l;
+            for (size_t ci = 0; ci < std::min<size_t>(4, cand.size()); ++ci) {
+                const int sh = cand[ci][1], st = cand[ci][2], base = next + sh;
+                std::vector<int> lane(width, -1);
+                std::vector<char> used(width, 0);
+                int total = 0;
+                for (int s = 0; s < width; ++s) {
+                    int bl = -1, bc = 1 << 30;
+                    for (int l = 0; l < width; ++l) {
+                        if (used[l]) continue;
+                        const size_t mark = M.journal.size();
+                        const int c = sum_cost(sums[first + s], (int)r, l, base, st);
+                        // undo this trial only
+                        for (size_t u = M.journal.size(); u-- > mark;) {
+                            auto& x = M.g[M.journal[u].gi];
+                            --x.cnt[M.journal[u].bank];
+                            x.mx = (int16_t)M.journal[u].mx;
+                        }
+                        M.journal.resize(mark);
+                        if (c < bc) { bc = c; bl = l; }
+                    }
+                    used[bl] = 1;
+                    lane[s] = bl;
+                    total += sum_cost(sums[first + s], (int)r, bl, base, st);
+                }
+                M.rollback();
+                if (total < best_c) { best_c = total; best_sh = sh; best_st = st; best_lane = lane; }
+            }
+            const int base = next + best_sh;
+            next = base + best_st * cmax;
             tt.sround.push_back((uint16_t)base);
             tt.sround.push_back((uint16_t)cmax);
+            tt.sround.push_back((uint16_t)best_st);
             tt.sround.push_back((uint16_t)width);
-            tt.sround.push_back(0);
+            std::vector<int> sum_at(32, -1);
+            for (int s = 0; s < width; ++s) sum_at[best_lane[s]] = s;
             for (int l = 0; l < 32; ++l) {
                 if (l >= width) { tt.sdst.push_back((uint16_t)tt.tslot); continue; }
-                const Sum& sm = sums[first + l];
+                const Sum& sm = sums[first + sum_at[l]];
                 tt.sdst.push_back((uint16_t)sm.dst);
                 for (int j = 0; j < cmax; ++j) {
-                    if (j < (int)sm.t.size()) place(sm.t[j], base + width * j + l);
-                    else nega.push_back(base + width * j + l);
+                    const int v = base + best_st * j + l;
+                    if (j < (int)sm.t.size()) {
+                        const int gi = grp(sm.t[j]);
+                        if (gi >= 0) M.add(gi, v, false);
+                        place(sm.t[j], v);
+                    } else {
+                        nega.push_back(v);
+                    }
                 }
+                M.add(M.res_grp((int)r, l), sm.dst, false);
             }
         }
         tt.nRJ = (int)rr.size();
@@ -586,10 +711,8 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         tt.gptr.push_back((uint16_t)(tt.gptr.back() + T.gen_ptr[b0 + bl + 1] - T.gen_ptr[b0 + bl]));
     next += 32;        // margin: lanes beyond a round's width read (and discard) up to 31 slots past it
     // pd, qd of every bus; the representative (first) end of every bus
-    for (int bl = 0; bl < nB; ++bl) {
-        loc_b[(size_t)5 * nB + bl] = next++;
-        loc_b[(size_t)6 * nB + bl] = next++;
-    }
+    for (int bl = 0; bl < nB; ++bl) loc_b[(size_t)5 * nB + bl] = next++;     // consecutive: the
+    for (int bl = 0; bl < nB; ++bl) loc_b[(size_t)6 * nB + bl] = next++;     // stores spread over banks
     tt.rep.assign(nE, -1);
     for (int bl = 0; bl < nB; ++bl) {
         if (tt.busptr[bl + 1] == tt.busptr[bl]) tt.orph.push_back((uint16_t)bl);
@@ -606,6 +729,63 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
     tt.bqd.resize(loc_b.size());
     for (size_t i = 0; i < loc_b.size(); ++i) tt.bqd[i] = (uint16_t)(loc_b[i] < 0 ? tt.tslot : loc_b[i]);
     return tt;
+}
+
+// Modeled shared-memory wavefronts of one 64-bit store instruction over n <= 32
+// lanes (slot < 0: lane inactive).  half: per half-warp, the largest number of
+// distinct slots on one 8-byte bank pair (slot mod 16), summed; else over the
+// whole warp, at least 2.
+inline int sts_wavefronts(const int* slot, int n, bool half) {
+    auto group = [&](int lo, int hi) {
+        int u[32], nu = 0, cnt[16] = {0}, best = 0;
+        for (int i = lo; i < hi; ++i) {
+            if (slot[i] < 0) continue;
+            bool dup = false;
+            for (int k = 0; k < nu && !dup; ++k) dup = u[k] == slot[i];
+            if (!dup) u[nu++] = slot[i];
+        }
+        for (int k = 0; k < nu; ++k) best = std::max(best, ++cnt[u[k] & 15]);
+        return best;
+    };
+    if (half) return group(0, std::min(n, 16)) + (n > 16 ? group(16, n) : 0);
+    const int g = group(0, n);
+    return g == 0 ? 0 : std::max(2, g);
+}
+
+// Modeled wavefronts of a tile's per-stage area stores (all callbacks): the 18
+// end stores, the bus-term stores of representative ends, the sum-round
+// results.  out[0]: half-warp model, out[1]: whole-warp model, out[2]: ideal.
+inline void tile_store_cost(const TileTable& tt, int64_t out[3]) {
+    const int nE = (int)tt.ends.size(), nB = tt.nB;
+    const int TW = 2;
+    int sl[32];
+    auto add = [&](int n) {
+        out[0] += sts_wavefronts(sl, n, true);
+        out[1] += sts_wavefronts(sl, n, false);
+        int act = 0;
+        for (int i = 0; i < n; ++i) act += sl[i] >= 0;
+        out[2] += act == 0 ? 0 : (act > 16 ? 2 : 1);
+    };
+    for (int w = 0; w * 32 < nE; ++w) {
+        const int lo = 32 * w, n = std::min(32, nE - lo);
+        for (int q = 0; q < NST; ++q) {
+            for (int i = 0; i < n; ++i) sl[i] = tt.dst[(size_t)q * nE + lo + i];
+            add(n);
+        }
+        for (int q = 0; q < 7; ++q) {
+            for (int i = 0; i < n; ++i) {
+                const int rb = tt.rep[lo + i];
+                sl[i] = rb < 0 ? -1 : tt.bqd[(size_t)q * nB + rb];
+            }
+            add(n);
+        }
+    }
+    const int nR = tt.nRJ + tt.nRH;
+    for (int r = 0; r < nR; ++r) {
+        for (int l = 0; l < 32; ++l) sl[l] = tt.sdst[32 * r + l];
+        add(32);
+    }
+    (void)TW;
 }
 
 // Planner invariants of one tile table (host check, used by acopf_batch_verify):
@@ -646,9 +826,11 @@ inline std::string verify_tile(const TileTable& tt) {
     const int nR = tt.nRJ + tt.nRH;
     if ((int)tt.sround.size() != 4 * nR || (int)tt.sdst.size() != 32 * nR) return "sum round tables have the wrong size";
     for (int r = 0; r < nR; ++r) {
-        const int base = tt.sround[4 * r], c = tt.sround[4 * r + 1], w = tt.sround[4 * r + 2];
+        const int base = tt.sround[4 * r], c = tt.sround[4 * r + 1], S = tt.sround[4 * r + 2];
+        const int w = tt.sround[4 * r + 3];
         if (w < 1 || w > 32) return "sum round width out of range";
-        if (base + w * c + 31 >= tt.nArea + 1) return "sum round reads past the area";
+        if (S < w) return "sum round stride below its width";
+        if (base + S * c + 31 >= tt.nArea + 1) return "sum round reads past the area";
         for (int l = 0; l < 32; ++l) {
             const int d = tt.sdst[32 * r + l];
             if (!slot_ok(d)) return "sum destination outside the area";
@@ -657,7 +839,7 @@ inline std::string verify_tile(const TileTable& tt) {
                 continue;
             }
             if (d != tt.tslot) prod[d]++;
-            for (int j = 0; j < c; ++j) read[base + w * j + l]++;
+            for (int j = 0; j < c; ++j) read[base + S * j + l]++;
         }
     }
     const int nRB = (int)tt.bround.size() / 6;

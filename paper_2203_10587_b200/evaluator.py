@@ -281,10 +281,11 @@ class BatchEvaluator:
 
     def verify_plan(self) -> dict:
         """Host check of the tile tables' invariants (acopf_batch_verify); no GPU needed."""
-        st = np.zeros(9, dtype=np.int64)
+        st = np.zeros(12, dtype=np.int64)
         L.check(L.lib().acopf_batch_verify(self._h, L.ptr(st, ctypes.c_int64)))
         keys = ("tables", "tiles", "ends", "area_doubles", "pad_slots", "max_smem_bytes",
-                "sum_rounds", "round_lane_terms", "round_chain_terms")
+                "sum_rounds", "round_lane_terms", "round_chain_terms", "store_wavefronts_half",
+                "store_wavefronts_warp", "store_wavefronts_ideal")
         return dict(zip(keys, (int(v) for v in st)))
 
     def __del__(self):
