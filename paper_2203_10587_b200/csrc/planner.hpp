@@ -618,26 +618,30 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             }
             return -1;
         };
-        // cost of putting sum sm in lane l of round r at (base, stride)
-        auto sum_cost = [&](const Sum& sm, int r, int l, int base, int st) {
+        // store groups of the current round's terms (tg[s]: sum s's terms)
+        std::vector<std::vector<int>> tg;
+        // cost of putting sum s in lane l of round r at (base, stride)
+        auto sum_cost = [&](int s, const Sum& sm, int r, int l, int base, int st) {
             int c = 0;
-            for (size_t j = 0; j < sm.t.size(); ++j) {
-                const int gi = grp(sm.t[j]);
-                if (gi >= 0) c += M.add(gi, base + st * (int)j + l, true);
-            }
+            const std::vector<int>& g = tg[s];
+            for (size_t j = 0; j < g.size(); ++j)
+                if (g[j] >= 0) c += M.add(g[j], base + st * (int)j + l, true);
             c += M.add(M.res_grp(r, l), sm.dst, true);
             return c;
         };
         for (size_t r = 0; r < rr.size(); ++r) {
             const int first = rr[r].first, width = rr[r].second;
             const int cmax = (int)sums[first].t.size();
+            tg.assign(width, {});
+            for (int q = 0; q < width; ++q)
+                for (const Sym& y : sums[first + q].t) tg[q].push_back(grp(y));
             // (shift, stride) by the identity lane order, then a greedy lane order
             // for the best few
             std::vector<std::array<int, 3>> cand;     // cost, shift, stride
             for (int st = width; st <= width + (width % 2 == 0 ? 1 : 0); ++st)
                 for (int sh = 0; sh < 16; ++sh) {
                     int c = 0;
-                    for (int l = 0; l < width; ++l) c += sum_cost(sums[first + l], (int)r, l, next + sh, st);
+                    for (int l = 0; l < width; ++l) c += sum_cost(l, sums[first + l], (int)r, l, next + sh, st);
                     M.rollback();
                     cand.push_back({c, sh, st});
                 }
@@ -655,7 +659,7 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
                     for (int l = 0; l < width; ++l) {
                         if (used[l]) continue;
                         const size_t mark = M.journal.size();
-                        const int c = sum_cost(sums[first + s], (int)r, l, base, st);
+                        const int c = sum_cost(s, sums[first + s], (int)r, l, base, st);
                         // undo this trial only
                         for (size_t u = M.journal.size(); u-- > mark;) {
                             auto& x = M.g[M.journal[u].gi];
@@ -667,7 +671,7 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
                     }
                     used[bl] = 1;
                     lane[s] = bl;
-                    total += sum_cost(sums[first + s], (int)r, bl, base, st);
+                    total += sum_cost(s, sums[first + s], (int)r, bl, base, st);
                 }
                 M.rollback();
                 if (total < best_c) { best_c = total; best_sh = sh; best_st = st; best_lane = lane; }
