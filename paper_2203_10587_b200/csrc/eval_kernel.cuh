@@ -214,7 +214,11 @@ __device__ __forceinline__ void prefetch(const EvalParams& P, const DRec& R, con
         cp_async8s(sG, P.pd + R.pd_off + i);
         cp_async8s(sG + st, P.qd + R.pd_off + i);
     }
+#ifdef ACOPF_DIAG_OWN_ONLY
+    const int f = V.f[e], t = f, r = V.ridx[e];
+#else
     const int f = V.f[e], t = V.t[e], r = V.ridx[e];
+#endif
     const double* xm = x + R.nb;
     in.vaf = __ldg(x + f);
     in.vat = __ldg(x + t);
@@ -357,7 +361,9 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
         flw[R.nbr] = fq;
     }
     const bool rated = in.rs >= 0;
+#ifndef ACOPF_DIAG_NO_CONSQ
     if (rated && need_c) P.cons[R.ineq_row + 2 * in.rs + (int)sd] = fp * fp + fq * fq;
+#endif
     const int rb = V.rep[e];
     if (rb >= 0) {
         double pdv = 0.0, qdv = 0.0;
@@ -398,9 +404,16 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
             double* out = P.jval + R.jineq + in.fo + (f == t ? 2 : 4) * (int)sd;
             // rows have even lengths: 16-byte alignment is the stage's block's
             const bool v2 = (reinterpret_cast<uintptr_t>(P.jval + R.jineq) & 15) == 0;
+#ifdef ACOPF_DIAG_NO_JINEQ
+            if (f >= 0) return;
+#endif
             if (f != t) {
                 const double a0 = f < t ? r0 : r1, a1 = f < t ? r1 : r0, a2 = f < t ? r2 : r3, a3 = f < t ? r3 : r2;
-                if (v2) {
+                if ((reinterpret_cast<uintptr_t>(out) & 31) == 0) {      // the row is one 32-byte sector
+                    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(out), "d"(a0), "d"(a1), "d"(a2),
+                                 "d"(a3)
+                                 : "memory");
+                } else if (v2) {
                     reinterpret_cast<double2*>(out)[0] = make_double2(a0, a1);
                     reinterpret_cast<double2*>(out)[1] = make_double2(a2, a3);
                 } else { out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3; }

@@ -22,7 +22,7 @@
 #ifdef __CUDACC__
 #define SC_HD __host__ __device__ __forceinline__
 __device__ static const double sc_table_dev[SC_NJ * 4] = {SC_TABLE_VALUES};
-__device__ static const double __align__(16) sc_gl_table_dev[SC_GL_NK * 4] = {SC_GL_TABLE_VALUES};
+__device__ static const double __align__(32) sc_gl_table_dev[SC_GL_NK * 4] = {SC_GL_TABLE_VALUES};
 #else
 #define SC_HD static inline
 #endif
@@ -175,8 +175,8 @@ __constant__ double sc_gl_k[11] = {GL_SN3, GL_SN5, GL_CS2, GL_CS4, GL_CS6, GL_S1
 #define GLK_BIG GL_BIG
 #endif
 
-// table: sc_gl_table_* (SC_GL_NK entries of sin hi, sin lo, cos hi, cos lo),
-// or a copy of it (the tile kernel keeps one in shared memory)
+// table: sc_gl_table_* (SC_GL_NK entries of sin hi, sin lo, cos hi, cos lo;
+// on the device, the 32-byte aligned global copy)
 SC_HD void libm_sincos_t(const double* table, double x, double* sp, double* cp) {
     const double ax = fabs(x);
     const bool core = ax < 0.85546875;
@@ -190,9 +190,9 @@ SC_HD void libm_sincos_t(const double* table, double x, double* sp, double* cp) 
     const int k = (int)(xk * 128.0);
     const double* tab = table + 4 * k;
 #ifdef __CUDA_ARCH__
-    // an entry is 32 bytes (16-byte aligned table): two 128-bit loads
-    const double2 e01 = *reinterpret_cast<const double2*>(tab), e23 = *reinterpret_cast<const double2*>(tab + 2);
-    const double sn = e01.x, ssn = e01.y, cs = e23.x, ccs = e23.y;
+    // an entry is 32 bytes of the 32-byte aligned global table: one 256-bit load
+    double sn, ssn, cs, ccs;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(sn), "=d"(ssn), "=d"(cs), "=d"(ccs) : "l"(tab));
 #else
     const double sn = tab[0], ssn = tab[1], cs = tab[2], ccs = tab[3];
 #endif
