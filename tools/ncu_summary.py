@@ -10,6 +10,9 @@ d = dict(zip(rows[0], rows[2]))
 pat = (r"gpu__time_duration.sum|dram__bytes_(read|write).sum$|smsp__inst_executed.sum$|smsp__issue_active.avg.pct|"
        r"sm__warps_active.avg.pct|registers_per_thread$|pipe_fp64_cycles.*avg.*active$|"
        r"l1tex__data_pipe_lsu_wavefronts_mem_shared.sum$|warps_eligible.avg|occupancy_limit_(reg|shared)|"
+       r"l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed|"
+       r"l1tex__data_pipe_lsu_wavefronts_mem_shared_op_(ld|st).sum$|TriageCompute.l1tex__data_pipe_lsu_wavefronts.*avg$|"
+       r"l1tex__t_sector_hit_rate.pct|memory_l1_wavefronts_shared(_ideal)?$|"
        r"smsp__pcsamp_warps_issue_stalled_[a-z_]*_not_issued$|shared_mem_per_block_dynamic|grid_size")
 for k in sorted(d):
     if re.search(pat, k) and d[k] not in ("0", "0.0"):
