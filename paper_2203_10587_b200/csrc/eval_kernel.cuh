@@ -2,9 +2,9 @@
 // atomics, built with -fmad=false so every expression rounds exactly like the
 // reference's numpy evaluation).
 //
-// acopf_tile_kernel -- one 64-thread CTA = one tile of consecutive buses
-// (<= 64 branch ends) evaluated for a run of stages that share the tile's
-// table.  Per stage, threads are branch ends in phase A, sum-round lanes in
+// acopf_tile_kernel -- one CTA of 32 x TILE_WARPS threads = one tile of
+// consecutive buses (one branch end per thread) evaluated for a run of stages
+// that share the tile's table.  Per stage, threads are branch ends in phase A, sum-round lanes in
 // phase B, and issue the bulk copy-out of the staged CSR segments and the
 // balance epilogue in phase C; three CTA barriers per stage, CTAs never wait
 // on each other.  Details at the kernel.
@@ -126,10 +126,7 @@ __device__ __forceinline__ double hval(double cpf, double cqf, double cpt, doubl
     return v;
 }
 
-#ifndef ACOPF_TILE_WARPS
-#define ACOPF_TILE_WARPS 2
-#endif
-constexpr int TILE_WARPS = ACOPF_TILE_WARPS;
+constexpr int TILE_WARPS = ACOPF_TILE_WARPS;     // planner.hpp
 constexpr int TILE_THREADS = 32 * TILE_WARPS;   // one branch end per thread
 
 constexpr int GQ = 4;    // doubles per thread in the gather buffer: pd qd (bus representative), Pg Qg (generator)
@@ -523,7 +520,7 @@ __device__ __forceinline__ void copy_seg16(double* g, const double* s, int L, in
 }
 
 // ---------------------------------------------------------------------------
-// Tile kernel: one 64-thread CTA evaluates one tile for a run of stages.
+// Tile kernel: one CTA (one thread per branch end) evaluates one tile for a run of stages.
 //
 //   0. one thread bulk-copies the tile table (cp.async.bulk + mbarrier) into
 //      shared memory; the constant 1.0 entries and -0.0 paddings are written
@@ -539,7 +536,7 @@ __device__ __forceinline__ void copy_seg16(double* g, const double* s, int L, in
 //      order), left-to-right over its contiguous -0.0-padded run.
 //   C. the four staged segments leave by TMA bulk stores; the balance
 //      epilogue finishes the P/Q balance rows (loads and generators).
-// Three CTA barriers per stage (two warps); CTAs never wait on each other.
+// Three CTA barriers per stage; CTAs never wait on each other.
 template <unsigned WHAT>
 __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_tile_kernel(const EvalParams P, int item0) {
     extern __shared__ __align__(128) unsigned char smem[];

@@ -56,12 +56,13 @@ constexpr int POS_B[10] = {0, 1, 2, 3, 1, 2, 3, 2, 3, 3};
 constexpr int HSLOT_F[10] = {0, 1, 5, 2, -1, 3, -1, 6, 4, -1};
 constexpr int HSLOT_T[10] = {-1, 1, -1, 2, 0, 3, 5, -1, 4, 6};
 
-#ifndef ACOPF_TILE_ENDS
-#ifdef ACOPF_TILE_WARPS
-#define ACOPF_TILE_ENDS (32 * ACOPF_TILE_WARPS)
-#else
-#define ACOPF_TILE_ENDS 64
+// warps per tile CTA (one branch end per thread); 4 measured best over the
+// four benchmark configurations
+#ifndef ACOPF_TILE_WARPS
+#define ACOPF_TILE_WARPS 4
 #endif
+#ifndef ACOPF_TILE_ENDS
+#define ACOPF_TILE_ENDS (32 * ACOPF_TILE_WARPS)
 #endif
 #ifndef ACOPF_TILE_BUSES
 #define ACOPF_TILE_BUSES 64
@@ -256,7 +257,7 @@ inline void flow_row_cols(const Topo& T, int k, std::vector<int>& cols) {
 // Tiles (serialised into one device blob)
 //
 // A tile is a run of consecutive buses with at most TILE_MAX_ENDS branch
-// ends; one 64-thread CTA (an end per thread) evaluates it for a list of
+// ends; one CTA (an end per thread) evaluates it for a list of
 // stages.  Its table (header + sections, 16-byte aligned) is
 // bulk-copied into shared memory once; after it comes the working "area":
 //
