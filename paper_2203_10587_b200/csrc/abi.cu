@@ -101,7 +101,8 @@ struct acopf_batch {
     // device
     cudaStream_t stream = nullptr;
     DevBuf d_topo, d_stage, d_items, d_recs, d_aux, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
-    DevBuf d_cprow, d_cpj, d_cpa, d_cpb, d_cpf, d_objterms, d_counter;
+    DevBuf d_cprow, d_cpj, d_cpa, d_cpb, d_cpf, d_objterms, d_counter, d_xi;
+    int max_nb = 0;
     std::vector<std::unique_ptr<DevBuf>> topo_bufs;
     EvalParams params{};
     size_t smem = 0, aux_smem = 0;
@@ -327,6 +328,20 @@ static void upload(acopf_batch* b) {
     P.obj_mode = b->obj_mode;
     P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
     P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
+    // interleaved (VA, VM, muP, muQ) per stage and bus, indexed 4 (var_off + bus)
+    {
+        int64_t xi_len = 4;
+        b->max_nb = 0;
+        for (const DStage& d : ds) {
+            xi_len = std::max<int64_t>(xi_len, 4 * (d.var_off + d.nb));
+            b->max_nb = std::max(b->max_nb, d.nb);
+        }
+        // networks whose per-stage inputs (32 B per bus) exceed what L1 keeps
+        // resident; ACOPF_INTERLEAVE=0/1 overrides (development aid)
+        const char* ie = getenv("ACOPF_INTERLEAVE");
+        const bool use = ie ? atoi(ie) != 0 : b->max_nb >= INTERLEAVE_MIN_BUSES;
+        P.xi = use ? static_cast<double*>(b->d_xi.alloc(sizeof(double) * (size_t)xi_len)) : nullptr;
+    }
     b->smem = (max_smem + 15) & ~size_t(15);
     // development aid: extra shared memory per CTA (lowers the resident CTAs per SM)
     if (const char* e = getenv("ACOPF_SMEM_PAD_KB")) b->smem += 1024 * (size_t)atoi(e);
@@ -550,6 +565,17 @@ int acopf_batch_set_layout(acopf_batch* b, const int64_t* offsets6, int32_t obj_
     });
 }
 
+// The tile kernel's bus inputs for stages [s0, s1): acopf_interleave_kernel on st.
+static void launch_interleave(acopf_batch* b, const EvalParams& P, int s0, int s1, cudaStream_t st) {
+    if (!P.xi) return;
+    for (int a = s0; a < s1; a += 65535) {
+        const dim3 grid((unsigned)std::max(1, (b->max_nb + BLOCK - 1) / BLOCK), (unsigned)std::min(65535, s1 - a));
+        acopf_interleave_kernel<<<grid, BLOCK, 0, st>>>(P, a);
+        cuda_check(cudaGetLastError(), "acopf_interleave_kernel launch");
+        b->launches++;
+    }
+}
+
 int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const double* mult, uint32_t what,
                      double* obj, double* grad, double* cons, double* jval, double* hval, void* stream) {
     return guard([&] {
@@ -581,6 +607,7 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
             b->launches++;
         }
         if (bus) {
+            launch_interleave(b, P, 0, (int)b->stages.size(), st);
             if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
             else acopf_tile_kernel<0u><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
             cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
@@ -605,6 +632,7 @@ int acopf_batch_flows(acopf_batch* b, const double* x, double* flows, double* in
         P.flows = flows; P.inj = inj;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
         if (P.n_bus_items > 0) {
+            launch_interleave(b, P, 0, (int)b->stages.size(), st);
             acopf_tile_kernel<0u><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
             cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
             b->launches++;
@@ -666,6 +694,7 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
                     b->launches++;
                 }
                 if (pc.bus_count && (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS))) {
+                    launch_interleave(b, P, pc.s0, pc.s1, cs);
                     if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<pc.bus_count, TILE_THREADS, b->smem, cs>>>(P, pc.bus_first);
                     else acopf_tile_kernel<0u><<<pc.bus_count, TILE_THREADS, b->smem, cs>>>(P, pc.bus_first);
                     cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");

@@ -96,6 +96,7 @@ struct EvalParams {
     double* flows;            // W_FLOWS: per stage pf, qf, pt, qt by topology branch (pu)
     double* inj;              // W_FLOWS: per stage p, q network injections by bus (pu)
     unsigned* counter;
+    double* xi;               // per stage and bus (VA, VM, muP, muQ) at 4 (var_off + bus): acopf_interleave_kernel
 };
 
 #ifndef ACOPF_WARP_MINB
@@ -105,6 +106,7 @@ constexpr int BLOCK = 256;                     // aux kernel
 constexpr int WARP_MINB = ACOPF_WARP_MINB;     // resident warps per SM the tile kernel is built for
 constexpr int GEN_CHUNK = 256;
 constexpr int CP_CHUNK = 1024;
+constexpr int INTERLEAVE_MIN_BUSES = 4096;     // interleaved bus inputs from this network size on
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -211,26 +213,37 @@ __device__ __forceinline__ void prefetch(const EvalParams& P, const DRec& R, con
         cp_async8s(sG, P.pd + R.pd_off + i);
         cp_async8s(sG + st, P.qd + R.pd_off + i);
     }
-#ifdef ACOPF_DIAG_OWN_ONLY
-    const int f = V.f[e], t = f, r = V.ridx[e];
-#else
     const int f = V.f[e], t = V.t[e], r = V.ridx[e];
-#endif
-    const double* xm = x + R.nb;
-    in.vaf = __ldg(x + f);
-    in.vat = __ldg(x + t);
-    in.vf = __ldg(xm + f);
-    in.vt = __ldg(xm + t);
+    if (P.xi) {
+        // both buses' (VA, VM, muP, muQ): one 256-bit load each from the
+        // interleaved copy (the multipliers are zeros unless the Hessian is asked)
+        const double* xi = opaque(static_cast<const double*>(P.xi) + 4 * R.var_off);
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(in.vaf), "=d"(in.vf), "=d"(in.mpf), "=d"(in.mqf)
+            : "l"(xi + 4 * f));
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(in.vat), "=d"(in.vt), "=d"(in.mpt), "=d"(in.mqt)
+            : "l"(xi + 4 * t));
+    } else {
+        // small networks: the stage's inputs stay L1-resident, gather directly
+        const double* xm = x + R.nb;
+        in.vaf = __ldg(x + f);
+        in.vat = __ldg(x + t);
+        in.vf = __ldg(xm + f);
+        in.vt = __ldg(xm + t);
+        if (need_h) {
+            const double* mu = opaque(P.mult + R.eq_row);
+            const double* mq = mu + R.nb;
+            in.mpf = __ldg(mu + f);
+            in.mqf = __ldg(mq + f);
+            in.mpt = __ldg(mu + t);
+            in.mqt = __ldg(mq + t);
+        }
+    }
     in.rs = -1;
     in.fo = 0;
     if (r >= 0) rated_shift(P, R, r, V.foff[e], in.rs, in.fo);
     if (need_h) {
-        const double* mu = opaque(P.mult + R.eq_row);
-        const double* mq = mu + R.nb;
-        in.mpf = __ldg(mu + f);
-        in.mqf = __ldg(mq + f);
-        in.mpt = __ldg(mu + t);
-        in.mqt = __ldg(mq + t);
         in.sf = 0.0;
         in.st = 0.0;
         if (r >= 0) {
@@ -358,9 +371,7 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
         flw[R.nbr] = fq;
     }
     const bool rated = in.rs >= 0;
-#ifndef ACOPF_DIAG_NO_CONSQ
     if (rated && need_c) P.cons[R.ineq_row + 2 * in.rs + (int)sd] = fp * fp + fq * fq;
-#endif
     const int rb = V.rep[e];
     if (rb >= 0) {
         double pdv = 0.0, qdv = 0.0;
@@ -401,9 +412,6 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
             double* out = P.jval + R.jineq + in.fo + (f == t ? 2 : 4) * (int)sd;
             // rows have even lengths: 16-byte alignment is the stage's block's
             const bool v2 = (reinterpret_cast<uintptr_t>(P.jval + R.jineq) & 15) == 0;
-#ifdef ACOPF_DIAG_NO_JINEQ
-            if (f >= 0) return;
-#endif
             if (f != t) {
                 const double a0 = f < t ? r0 : r1, a1 = f < t ? r1 : r0, a2 = f < t ? r2 : r3, a3 = f < t ? r3 : r2;
                 if ((reinterpret_cast<uintptr_t>(out) & 31) == 0) {      // the row is one 32-byte sector
@@ -848,6 +856,27 @@ __device__ void coupling_chunk(const EvalParams& P, int chunk) {
             else { o[0] = 1.0; o[1] = -1.0; }
         }
     }
+}
+
+// Per stage s0 + blockIdx.y and bus: (VA, VM, muP, muQ) into one 32-byte
+// record at xi + 4 (var_off + bus), so a branch end gathers each of its two
+// buses with one 256-bit load (the tile kernel's far-bus gathers are scattered).
+__global__ void __launch_bounds__(BLOCK) acopf_interleave_kernel(const EvalParams P, int s0) {
+    const DStage& S = P.stages[s0 + blockIdx.y];
+    const int nb = S.nb;
+    const int i = blockIdx.x * BLOCK + threadIdx.x;
+    if (i >= nb) return;
+    const double* x = P.x + S.var_off;
+    const double va = x[i], vm = x[nb + i];
+    double mp = 0.0, mq = 0.0;
+    if (P.mult && (P.what & W_HESS)) {
+        const double* mu = P.mult + S.eq_row;
+        mp = mu[i];
+        mq = mu[nb + i];
+    }
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(P.xi + 4 * (S.var_off + i)), "d"(va), "d"(vm),
+                 "d"(mp), "d"(mq)
+                 : "memory");
 }
 
 __global__ void __launch_bounds__(BLOCK) acopf_aux_kernel(const EvalParams P, int item0) {

@@ -42,3 +42,25 @@ def bit_diffs(a, b) -> int:
 
 def points(g):
     return [(g[f"px{i}"], g[f"pmult{i}"], float(g[f"pof{i}"])) for i in range(int(g["npoints"]))]
+
+
+def hub_case(n_hub=200, n_gen_hub=150, seed=5):
+    """A network with one hub bus carrying n_hub extra branches (half as the from-bus, half as
+    the to-bus, some parallel) and n_gen_hub generators: exercises a tile whose one bus has
+    more branch ends than the tile CTA has threads (128), long duplicate sums, and more
+    generators than threads per tile."""
+    from dataclasses import replace
+    case = syn.make_case(200, 40, 20, seed=seed, features=True)
+    rng = np.random.default_rng(seed)
+    hub = case.buses[3].id
+    others = [b.id for b in case.buses if b.id != hub and b.btype != 4]
+    extra = []
+    for k, j in enumerate(rng.choice(others, size=n_hub, replace=True)):
+        base = case.branches[k % 50]
+        fb, tb = (hub, int(j)) if k % 2 == 0 else (int(j), hub)
+        extra.append(replace(base, fbus=fb, tbus=tb, r=float(rng.uniform(0.005, 0.02)),
+                             x=float(rng.uniform(0.05, 0.2)), status=1))
+    g0 = case.gens[1]
+    gens = [replace(g0, bus=hub, pmax=float(rng.uniform(50, 300)),
+                    cost=replace(g0.cost, c1=float(rng.uniform(1, 40)))) for _ in range(n_gen_hub)]
+    return replace(case, branches=case.branches + tuple(extra), gens=case.gens + tuple(gens))

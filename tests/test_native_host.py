@@ -178,3 +178,12 @@ def test_tile_tables_config1_network():
     assert st["ends"] == 2 * 12999
     assert st["ends"] / st["tiles"] > 80          # tile fill (128 ends per 4-warp CTA)
     assert st["max_smem_bytes"] <= 75 * 1024      # 3 CTAs (12 warps) per SM
+
+
+def test_tile_tables_hub_network():
+    """A hub bus with more branch ends than a tile CTA has threads: invariants and the
+    modeled shared-memory store cost (conflicts included) against its conflict-free bound."""
+    p, _ = pkg.build_acopf(C.hub_case())
+    st = p.evaluator.verify_plan()
+    assert st["ends"] > 128 and st["max_smem_bytes"] <= 220 * 1024
+    assert st["store_wavefronts_ideal"] <= st["store_wavefronts_half"] <= 4 * st["store_wavefronts_ideal"]
