@@ -569,7 +569,8 @@ int acopf_batch_set_layout(acopf_batch* b, const int64_t* offsets6, int32_t obj_
 static void launch_interleave(acopf_batch* b, const EvalParams& P, int s0, int s1, cudaStream_t st) {
     if (!P.xi) return;
     for (int a = s0; a < s1; a += 65535) {
-        const dim3 grid((unsigned)std::max(1, (b->max_nb + BLOCK - 1) / BLOCK), (unsigned)std::min(65535, s1 - a));
+        const dim3 grid((unsigned)std::max(1, (b->max_nb + BLOCK * IL_BUSES - 1) / (BLOCK * IL_BUSES)),
+                        (unsigned)std::min(65535, s1 - a));
         acopf_interleave_kernel<<<grid, BLOCK, 0, st>>>(P, a);
         cuda_check(cudaGetLastError(), "acopf_interleave_kernel launch");
         b->launches++;

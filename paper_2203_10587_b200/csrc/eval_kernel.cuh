@@ -106,7 +106,8 @@ constexpr int BLOCK = 256;                     // aux kernel
 constexpr int WARP_MINB = ACOPF_WARP_MINB;     // resident warps per SM the tile kernel is built for
 constexpr int GEN_CHUNK = 256;
 constexpr int CP_CHUNK = 1024;
-constexpr int INTERLEAVE_MIN_BUSES = 4096;     // interleaved bus inputs from this network size on
+constexpr int INTERLEAVE_MIN_BUSES = 4096;
+constexpr int IL_BUSES = 4;                     // buses per thread of acopf_interleave_kernel     // interleaved bus inputs from this network size on
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -864,19 +865,31 @@ __device__ void coupling_chunk(const EvalParams& P, int chunk) {
 __global__ void __launch_bounds__(BLOCK) acopf_interleave_kernel(const EvalParams P, int s0) {
     const DStage& S = P.stages[s0 + blockIdx.y];
     const int nb = S.nb;
-    const int i = blockIdx.x * BLOCK + threadIdx.x;
-    if (i >= nb) return;
     const double* x = P.x + S.var_off;
-    const double va = x[i], vm = x[nb + i];
-    double mp = 0.0, mq = 0.0;
-    if (P.mult && (P.what & W_HESS)) {
-        const double* mu = P.mult + S.eq_row;
-        mp = mu[i];
-        mq = mu[nb + i];
+    const bool mu_on = P.mult && (P.what & W_HESS);
+    const double* mu = P.mult + (mu_on ? S.eq_row : 0);
+    double* xi = P.xi + 4 * S.var_off;
+    const int stride = gridDim.x * BLOCK;
+    // IL_BUSES buses per thread, all loads before the stores
+    double v[IL_BUSES][4];
+#pragma unroll
+    for (int k = 0; k < IL_BUSES; ++k) {
+        const int i = blockIdx.x * BLOCK + threadIdx.x + k * stride;
+        if (i < nb) {
+            v[k][0] = x[i];
+            v[k][1] = x[nb + i];
+            v[k][2] = mu_on ? mu[i] : 0.0;
+            v[k][3] = mu_on ? mu[nb + i] : 0.0;
+        }
     }
-    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(P.xi + 4 * (S.var_off + i)), "d"(va), "d"(vm),
-                 "d"(mp), "d"(mq)
-                 : "memory");
+#pragma unroll
+    for (int k = 0; k < IL_BUSES; ++k) {
+        const int i = blockIdx.x * BLOCK + threadIdx.x + k * stride;
+        if (i < nb)
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(xi + 4 * i), "d"(v[k][0]), "d"(v[k][1]),
+                         "d"(v[k][2]), "d"(v[k][3])
+                         : "memory");
+    }
 }
 
 __global__ void __launch_bounds__(BLOCK) acopf_aux_kernel(const EvalParams P, int item0) {
