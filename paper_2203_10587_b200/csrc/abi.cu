@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <numeric>
 #include <stdexcept>
@@ -101,7 +102,7 @@ struct acopf_batch {
     // device
     cudaStream_t stream = nullptr;
     DevBuf d_topo, d_stage, d_items, d_recs, d_aux, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
-    DevBuf d_cprow, d_cpj, d_cpa, d_cpb, d_cpf, d_objterms, d_counter, d_xi;
+    DevBuf d_cpruns, d_objterms, d_counter, d_xi;
     int max_nb = 0;
     std::vector<std::unique_ptr<DevBuf>> topo_bufs;
     EvalParams params{};
@@ -138,8 +139,9 @@ static void upload(acopf_batch* b) {
     // topologies (only what the aux kernel needs; the bus kernel reads tile tables)
     std::vector<DTopo> dt;
     b->topo_bufs.clear();
-    size_t max_leaf = 1;
+    size_t max_leaf = 1, max_ng = 0;
     for (const Topo* T : b->topos) {
+        max_ng = std::max<size_t>(max_ng, (size_t)T->ng);
         DTopo d{};
         d.nb = T->nb; d.nbr = T->nbr; d.ng = T->ng; d.nr = T->nr;
         std::vector<int> leaf;
@@ -297,8 +299,27 @@ static void upload(acopf_batch* b) {
         for (auto& ps : b->pipe_streams)
             if (!ps) cuda_check(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking), "stream");
     }
-    const int n_cp = (int)((n_coupling + CP_CHUNK - 1) / CP_CHUNK);
-    for (int c = 0; c < n_cp; ++c) aux.push_back(DAuxItem{1, 0, c, 0});
+    // coupling rows as runs (row, J position, child and base columns advancing
+    // together), packed into items of at most CP_CHUNK rows
+    std::vector<DCpRun> runs;
+    for (int64_t i = 0; i < n_coupling; ++i) {
+        if (!runs.empty()) {
+            DCpRun& R = runs.back();
+            if (R.n < CP_CHUNK && b->cp_row[i] == R.row0 + R.n && b->cp_jpos[i] == R.jpos0 + 2 * R.n &&
+                b->cp_a[i] == R.a0 + R.n && b->cp_b[i] == R.b0 + R.n && (int)b->cp_first[i] == R.base_first) {
+                R.n++;
+                continue;
+            }
+        }
+        runs.push_back(DCpRun{b->cp_row[i], b->cp_jpos[i], b->cp_a[i], b->cp_b[i], 1, (int)b->cp_first[i]});
+    }
+    for (size_t r = 0; r < runs.size();) {
+        size_t e = r;
+        int rows = 0;
+        while (e < runs.size() && (e == r || rows + runs[e].n <= CP_CHUNK)) rows += runs[e++].n;
+        aux.push_back(DAuxItem{1, (int)r, (int)(e - r), 0});
+        r = e;
+    }
     b->n_obj = S;
 
     EvalParams& P = b->params;
@@ -316,12 +337,7 @@ static void upload(acopf_batch* b) {
     P.cc = b->d_cc.upload(b->cc);
     P.rem_ridx = b->d_rem.upload(rem);
     P.rem_rowsz = b->d_remsz.upload(remsz);
-    P.cp_row = reinterpret_cast<const long long*>(b->d_cprow.upload(b->cp_row));
-    P.cp_jpos = reinterpret_cast<const long long*>(b->d_cpj.upload(b->cp_jpos));
-    P.cp_a = reinterpret_cast<const long long*>(b->d_cpa.upload(b->cp_a));
-    P.cp_b = reinterpret_cast<const long long*>(b->d_cpb.upload(b->cp_b));
-    P.cp_base_first = reinterpret_cast<const signed char*>(b->d_cpf.upload(b->cp_first));
-    P.ncp = n_coupling;
+    P.cp_runs = b->d_cpruns.upload(runs);
     P.n_bus_items = (int)items.size();
     P.n_aux_items = (int)aux.size();
     P.n_obj = S;
@@ -345,13 +361,31 @@ static void upload(acopf_batch* b) {
     b->smem = (max_smem + 15) & ~size_t(15);
     // development aid: extra shared memory per CTA (lowers the resident CTAs per SM)
     if (const char* e = getenv("ACOPF_SMEM_PAD_KB")) b->smem += 1024 * (size_t)atoi(e);
-    b->aux_smem = sizeof(double) * max_leaf;
-    for (auto fn : {acopf_tile_kernel<0u>, acopf_tile_kernel<ACOPF_ALL>})
-        cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)std::max<size_t>(b->smem, 1)), "cudaFuncSetAttribute(tile)");
-    if (b->aux_smem > 48 * 1024)
-        cuda_check(cudaFuncSetAttribute(acopf_aux_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)b->aux_smem), "cudaFuncSetAttribute(aux)");
+    // objective blocks stage their stage's cost terms when they fit (64 KB)
+    // (up to 16 KB: larger aux blocks crowd the tile kernel's CTAs off the SMs;
+    // a full carve-out preference for both kernels costs the tile kernel its L1)
+    const char* se = getenv("ACOPF_OBJ_STAGE_KB");          // development aid
+    P.obj_staged = sizeof(double) * (max_leaf + max_ng) <= 1024 * (size_t)(se ? atoi(se) : 16) ? 1 : 0;
+    b->aux_smem = sizeof(double) * (max_leaf + (P.obj_staged ? max_ng : 0));
+    // the dynamic shared-memory limits only grow (per device): every live batch
+    // keeps launching with its own size
+    {
+        static std::mutex mu;
+        static std::map<int, std::pair<size_t, size_t>> limit;     // device -> (tile, aux)
+        std::lock_guard<std::mutex> lock(mu);
+        auto& lim = limit[b->device];
+        if (b->smem > lim.first) {
+            for (auto fn : {acopf_tile_kernel<0u>, acopf_tile_kernel<ACOPF_ALL>})
+                cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem),
+                           "cudaFuncSetAttribute(tile)");
+            lim.first = b->smem;
+        }
+        if (b->aux_smem > lim.second) {          // (the kernel also has static shared memory)
+            cuda_check(cudaFuncSetAttribute(acopf_aux_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)b->aux_smem), "cudaFuncSetAttribute(aux)");
+            lim.second = b->aux_smem;
+        }
+    }
     b->uploaded = true;
 }
 
@@ -604,7 +638,7 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         }
         if (aux) {
             acopf_aux_kernel<<<P.n_aux_items, BLOCK, b->aux_smem, fork ? b->aux_stream : st>>>(P, 0);
-            cuda_check(cudaGetLastError(), "acopf_aux_kernel launch");
+            cuda_check(cudaGetLastError(), ("acopf_aux_kernel launch (" + std::to_string(b->aux_smem) + " B shared)").c_str());
             b->launches++;
         }
         if (bus) {
@@ -691,7 +725,7 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
                 if (mult && nm) cuda_check(cudaMemcpyAsync(dm + m0, mult + m0, 8 * (m1 - m0), cudaMemcpyHostToDevice, cs), "H2D mult");
                 if (pc.aux_count) {
                     acopf_aux_kernel<<<pc.aux_count, BLOCK, b->aux_smem, cs>>>(P, pc.aux_first);
-                    cuda_check(cudaGetLastError(), "acopf_aux_kernel launch");
+                    cuda_check(cudaGetLastError(), ("acopf_aux_kernel launch (" + std::to_string(b->aux_smem) + " B shared)").c_str());
                     b->launches++;
                 }
                 if (pc.bus_count && (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS))) {

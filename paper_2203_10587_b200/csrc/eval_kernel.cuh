@@ -56,8 +56,15 @@ struct alignas(16) DRec {
 static_assert(sizeof(DRec) == 128, "DRec layout");
 
 struct DAuxItem {
-    int kind;                 // 0 generator chunk, 1 coupling chunk
+    int kind;                 // 0 generator chunk (stage, chunk); 1 coupling runs [stage, stage + chunk)
     int stage, chunk, pad;
+};
+
+// A run of coupling rows whose row, J position, child and base columns all
+// advance together (row0 + i, jpos0 + 2 i, a0 + i, b0 + i)
+struct DCpRun {
+    long long row0, jpos0, a0, b0;
+    int n, base_first;
 };
 
 struct EvalParams {
@@ -74,15 +81,11 @@ struct EvalParams {
     const double* cc;
     const int* rem_ridx;      // removed rated indices per stage (sorted)
     const int* rem_rowsz;
-    const long long* cp_row;
-    const long long* cp_jpos;
-    const long long* cp_a;
-    const long long* cp_b;
-    const signed char* cp_base_first;
-    long long ncp;
+    const DCpRun* cp_runs;    // coupling rows as runs (composer.py:229-242, 274-276)
     int n_bus_items, n_aux_items;
     int n_obj;                // objective stages (chunk-0 generator items)
     int obj_mode;             // 0: f_s into obj[slot]; 1: weighted sum into obj[0]; 2: weighted terms only
+    int obj_staged;           // 1: the objective block stages its stage's cost terms in shared memory
     const double* x;
     const double* mult;
     double obj_factor;
@@ -796,24 +799,33 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
         }
     }
     if (chunk != 0 || !(P.what & W_OBJ)) return;
-    // stage objective: numpy's pairwise sum over the ng cost terms (acopf.py:266-269)
+    // stage objective: numpy's pairwise sum over the ng cost terms (acopf.py:266-269).
+    // The block first computes every term in parallel into shared memory (after
+    // the leaves), so a leaf's sequential sum does not wait on global loads.
+    const double* tq = Q + T.nleaf;
+    if (P.obj_staged) {
+        double* tw = Q + T.nleaf;
+        for (int i = threadIdx.x; i < ng; i += blockDim.x) tw[i] = cost_term(P, S, pg, i);
+        __syncthreads();
+    }
+    auto term = [&](int i) { return P.obj_staged ? tq[i] : cost_term(P, S, pg, i); };
     for (int l = threadIdx.x; l < T.nleaf; l += blockDim.x) {
         const int st = T.leaf[2 * l], n = T.leaf[2 * l + 1];
         double res;
         if (n < 8) {
             res = 0.0;
-            for (int i = 0; i < n; ++i) res = res + cost_term(P, S, pg, st + i);
+            for (int i = 0; i < n; ++i) res = res + term(st + i);
         } else {
             double r[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = cost_term(P, S, pg, st + j);
+            for (int j = 0; j < 8; ++j) r[j] = term(st + j);
             int i = 8;
             for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) r[j] = r[j] + cost_term(P, S, pg, st + i + j);
+                for (int j = 0; j < 8; ++j) r[j] = r[j] + term(st + i + j);
             }
             res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-            for (; i < n; ++i) res = res + cost_term(P, S, pg, st + i);
+            for (; i < n; ++i) res = res + term(st + i);
         }
         Q[l] = res;
     }
@@ -835,26 +847,37 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
     }
     __syncthreads();
     if (!last) return;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (P.obj_mode == 1) {
-            const volatile double* terms = P.obj_terms;
-            double acc = 0.0;
-            for (int i = 0; i < P.n_obj; ++i) acc = acc + terms[i];
-            P.obj[0] = acc;
+    __threadfence();
+    if (P.obj_mode == 1) {
+        // the weighted terms in stage order (composer.py:256-258): the block
+        // stages them from L2 (__ldcg: written by other CTAs) 256 at a time and
+        // one thread adds them in order
+        __shared__ double buf[BLOCK];
+        double acc = 0.0;
+        for (int i0 = 0; i0 < P.n_obj; i0 += BLOCK) {
+            const int n = min(BLOCK, P.n_obj - i0);
+            if ((int)threadIdx.x < n) buf[threadIdx.x] = __ldcg(P.obj_terms + i0 + threadIdx.x);
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int i = 0; i < n; ++i) acc = acc + buf[i];
+            __syncthreads();
         }
-        *P.counter = 0u;
+        if (threadIdx.x == 0) P.obj[0] = acc;
     }
+    if (threadIdx.x == 0) *P.counter = 0u;
 }
 
-__device__ void coupling_chunk(const EvalParams& P, int chunk) {
-    const long long c = (long long)chunk * CP_CHUNK;
-    for (long long i = c + threadIdx.x; i < c + CP_CHUNK && i < P.ncp; i += blockDim.x) {
-        if (P.what & W_CONS) P.cons[P.cp_row[i]] = P.x[P.cp_a[i]] - P.x[P.cp_b[i]];
-        if (P.what & W_JAC) {
-            double* o = P.jval + P.cp_jpos[i];
-            if (P.cp_base_first[i]) { o[0] = -1.0; o[1] = 1.0; }
-            else { o[0] = 1.0; o[1] = -1.0; }
+__device__ void coupling_runs(const EvalParams& P, int first, int count) {
+    for (int r = first; r < first + count; ++r) {
+        const DCpRun R = P.cp_runs[r];
+        const double j0 = R.base_first ? -1.0 : 1.0;
+        for (int i = threadIdx.x; i < R.n; i += blockDim.x) {
+            if (P.what & W_CONS) P.cons[R.row0 + i] = P.x[R.a0 + i] - P.x[R.b0 + i];
+            if (P.what & W_JAC) {
+                double* o = P.jval + R.jpos0 + 2 * i;
+                o[0] = j0;
+                o[1] = -j0;
+            }
         }
     }
 }
@@ -896,7 +919,7 @@ __global__ void __launch_bounds__(BLOCK) acopf_aux_kernel(const EvalParams P, in
     extern __shared__ __align__(16) double leaves[];
     const DAuxItem it = P.aux_items[item0 + blockIdx.x];
     if (it.kind == 0) gen_chunk(P, it.stage, it.chunk, leaves);
-    else coupling_chunk(P, it.chunk);
+    else coupling_runs(P, it.stage, it.chunk);
 }
 
 }  // namespace acopf
