@@ -278,12 +278,13 @@ static void upload(acopf_batch* b) {
         for (int c = 0; c < nch; ++c) aux.push_back(DAuxItem{0, s, c, 0});
     }
     aux_first_of_stage[S] = (int)aux.size();
-    // pipeline chunks for host-buffer evaluation of independent layouts: about 4
+    // pipeline chunks for host-buffer evaluation of independent layouts: about 8
     // chunks of whole stage groups (bus items are stage-group-major)
     b->pipe.clear();
     if (b->obj_mode == 0 && n_coupling == 0 && S >= 2) {
         const int ngroups = (S + G - 1) / G;
-        const int per = std::max(1, (ngroups + 3) / 4);
+        const int nchunks = getenv("ACOPF_PIPE_CHUNKS") ? std::max(1, atoi(getenv("ACOPF_PIPE_CHUNKS"))) : 8;   // development aid
+        const int per = std::max(1, (ngroups + nchunks - 1) / nchunks);
         int item = 0;
         for (int g0 = 0; g0 < ngroups; g0 += per) {
             acopf_batch::Pipe pc{};
