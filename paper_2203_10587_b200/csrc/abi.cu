@@ -102,7 +102,7 @@ struct acopf_batch {
     // device
     cudaStream_t stream = nullptr;
     DevBuf d_topo, d_stage, d_items, d_recs, d_aux, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
-    DevBuf d_cpruns, d_objterms, d_counter, d_xi;
+    DevBuf d_cpruns, d_objterms, d_xi;
     int max_nb = 0;
     std::vector<std::unique_ptr<DevBuf>> topo_bufs;
     EvalParams params{};
@@ -344,7 +344,6 @@ static void upload(acopf_batch* b) {
     P.n_obj = S;
     P.obj_mode = b->obj_mode;
     P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
-    P.counter = static_cast<unsigned*>(b->d_counter.alloc(sizeof(unsigned)));
     // interleaved (VA, VM, muP, muQ) per stage and bus, indexed 4 (var_off + bus)
     {
         int64_t xi_len = 4;
@@ -641,6 +640,11 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
             acopf_aux_kernel<<<P.n_aux_items, BLOCK, b->aux_smem, fork ? b->aux_stream : st>>>(P, 0);
             cuda_check(cudaGetLastError(), ("acopf_aux_kernel launch (" + std::to_string(b->aux_smem) + " B shared)").c_str());
             b->launches++;
+            if (P.obj_mode == 1 && (what & ACOPF_OBJ)) {
+                acopf_objsum_kernel<<<1, BLOCK, 0, fork ? b->aux_stream : st>>>(P);
+                cuda_check(cudaGetLastError(), "acopf_objsum_kernel launch");
+                b->launches++;
+            }
         }
         if (bus) {
             launch_interleave(b, P, 0, (int)b->stages.size(), st);

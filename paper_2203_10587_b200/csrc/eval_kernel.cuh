@@ -98,7 +98,6 @@ struct EvalParams {
     double* obj_terms;        // per objective stage: w_s * f_s
     double* flows;            // W_FLOWS: per stage pf, qf, pt, qt by topology branch (pu)
     double* inj;              // W_FLOWS: per stage p, q network injections by bus (pu)
-    unsigned* counter;
     double* xi;               // per stage and bus (VA, VM, muP, muQ) at 4 (var_off + bus): acopf_interleave_kernel
 };
 
@@ -830,41 +829,32 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
         Q[l] = res;
     }
     __syncthreads();
-    __shared__ bool last;
     if (threadIdx.x == 0) {
         int idx = 0;
         const double fs = pairwise_tree(ng, Q, idx);
         if (P.obj_mode == 0) {
             P.obj[S.obj_slot] = fs;
-            last = false;
-        } else {
+        } else {           // the weighted term; acopf_objsum_kernel adds them in stage order
             P.obj_terms[S.obj_slot] = S.w * fs;
             if (P.obj_mode == 2) P.obj[S.obj_slot] = S.w * fs;
-            __threadfence();
-            const unsigned done = atomicAdd(P.counter, 1u);
-            last = (done == (unsigned)P.n_obj - 1);
         }
     }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    if (P.obj_mode == 1) {
-        // the weighted terms in stage order (composer.py:256-258): the block
-        // stages them from L2 (__ldcg: written by other CTAs) 256 at a time and
-        // one thread adds them in order
-        __shared__ double buf[BLOCK];
-        double acc = 0.0;
-        for (int i0 = 0; i0 < P.n_obj; i0 += BLOCK) {
-            const int n = min(BLOCK, P.n_obj - i0);
-            if ((int)threadIdx.x < n) buf[threadIdx.x] = __ldcg(P.obj_terms + i0 + threadIdx.x);
-            __syncthreads();
-            if (threadIdx.x == 0)
-                for (int i = 0; i < n; ++i) acc = acc + buf[i];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) P.obj[0] = acc;
+}
+
+// The composite objective (composer.py:256-258): the weighted stage terms in
+// stage order.  One block stages them 256 at a time; one thread adds them.
+__global__ void __launch_bounds__(BLOCK) acopf_objsum_kernel(const EvalParams P) {
+    __shared__ double buf[BLOCK];
+    double acc = 0.0;
+    for (int i0 = 0; i0 < P.n_obj; i0 += BLOCK) {
+        const int n = min(BLOCK, P.n_obj - i0);
+        if ((int)threadIdx.x < n) buf[threadIdx.x] = P.obj_terms[i0 + threadIdx.x];
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int i = 0; i < n; ++i) acc = acc + buf[i];
+        __syncthreads();
     }
-    if (threadIdx.x == 0) *P.counter = 0u;
+    if (threadIdx.x == 0) P.obj[0] = acc;
 }
 
 __device__ void coupling_runs(const EvalParams& P, int first, int count) {
