@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <atomic>
 #include <memory>
 #include <numeric>
 #include <stdexcept>
@@ -426,6 +428,35 @@ int acopf_topo_destroy(acopf_topo* t) {
     return 0;
 }
 
+// Build tile tables in parallel: out[i] = build_tile(*topo[i], tile[i], live[i]).
+struct TableTask { const Topo* topo; int topo_id, tile; const std::vector<int>* removed; };
+static void build_tables(const std::vector<TableTask>& tasks, std::vector<TileTable>& tables, size_t first) {
+    if (tasks.empty()) return;
+    tables.resize(first + tasks.size());
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nt = (int)std::min<size_t>({(size_t)hw, (size_t)32, tasks.size()});
+    std::atomic<size_t> next{0};
+    std::string err;
+    std::mutex mu;
+    auto work = [&] {
+        for (size_t i; (i = next.fetch_add(1)) < tasks.size();) {
+            const TableTask& k = tasks[i];
+            try {
+                tables[first + i] = build_tile(*k.topo, k.tile, Live{k.removed});
+                tables[first + i].topo = k.topo_id;
+            } catch (const std::exception& e) {
+                std::lock_guard<std::mutex> lock(mu);
+                if (err.empty()) err = e.what();
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+    if (!err.empty()) throw std::runtime_error(err);
+}
+
 int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos, int32_t n_stages,
                        const int32_t* stage_topo, const int64_t* removed_ptr, const int32_t* removed_idx,
                        const int32_t* stage_load, const int64_t* load_off, int64_t n_load_values,
@@ -436,16 +467,23 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
         std::unique_ptr<acopf_batch> B(new acopf_batch());
         B->device = device;
         for (int i = 0; i < n_topos; ++i) B->topos.push_back(&topos[i]->t);
-        // base tile tables
+        // base tile tables (built in parallel)
+        {
+            std::vector<TableTask> tasks;
+            for (int i = 0; i < n_topos; ++i) {
+                const Topo& T = *B->topos[i];
+                std::vector<int> ids;
+                for (size_t t = 0; t + 1 < T.tile_b0.size(); ++t) {
+                    ids.push_back((int)tasks.size());
+                    tasks.push_back(TableTask{&T, i, (int)t, nullptr});
+                }
+                B->base_table.push_back(ids);
+            }
+            build_tables(tasks, B->tables, 0);
+        }
         for (int i = 0; i < n_topos; ++i) {
             const Topo& T = *B->topos[i];
-            std::vector<int> ids;
-            for (size_t t = 0; t + 1 < T.tile_b0.size(); ++t) {
-                B->tables.push_back(build_tile(T, (int)t, Live{}));
-                B->tables.back().topo = i;
-                ids.push_back((int)B->tables.size() - 1);
-            }
-            B->base_table.push_back(ids);
+            const std::vector<int>& ids = B->base_table[i];
             if (getenv("ACOPF_DEBUG_PLAN")) {     // planner statistics (development aid)
                 size_t tb = 0, ar = 0, mx = 0, ends = 0, terms = 0, slots = 0;
                 for (int id : ids) {
@@ -480,6 +518,8 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
         B->cb.assign(cb, cb + n_cost_values);
         B->cc.assign(cc, cc + n_cost_values);
         B->stages.resize(n_stages);
+        std::vector<TableTask> patch_tasks;             // patched tables, built in parallel below
+        const size_t patch_first = B->tables.size();
         for (int s = 0; s < n_stages; ++s) {
             StageInfo& S = B->stages[s];
             S.topo = stage_topo[s];
@@ -522,12 +562,16 @@ int acopf_batch_create(int32_t device, int32_t n_topos, acopf_topo* const* topos
                 auto key = std::make_pair(S.topo, std::make_pair(S.removed, t));
                 auto it = B->patch_cache.find(key);
                 if (it == B->patch_cache.end()) {
-                    B->tables.push_back(build_tile(T, t, Live{&S.removed}));
-                    B->tables.back().topo = S.topo;
-                    it = B->patch_cache.emplace(key, (int)B->tables.size() - 1).first;
+                    it = B->patch_cache.emplace(key, (int)(patch_first + patch_tasks.size())).first;
+                    patch_tasks.push_back(TableTask{&T, S.topo, t, &S.removed});
                 }
                 S.table[t] = it->second;
             }
+        }
+        build_tables(patch_tasks, B->tables, patch_first);
+        for (int s = 0; s < n_stages; ++s) {
+            StageInfo& S = B->stages[s];
+            const Topo& T = *B->topos[S.topo];
             // sizes and stage-local segment offsets
             const int ntile = (int)S.table.size();
             int64_t LP = 0, LQ = 0, LA = 0, LV = 0;
