@@ -220,14 +220,19 @@ static void upload(acopf_batch* b) {
     // enough that the inputs (x, multipliers) of the stage groups in flight stay
     // L2-resident (ACOPF_L2_INPUT_MB per group; gathers otherwise re-read HBM)
     const char* wenv = getenv("ACOPF_ITEM_WAVES");     // development aid: items per resident CTA slot
-    const int64_t target_items = 148LL * (WARP_MINB / TILE_WARPS) * (wenv ? std::max(1, atoi(wenv)) : 4);
+    const int64_t target_items = 148LL * (WARP_MINB / TILE_WARPS) * (wenv ? std::max(1, atoi(wenv)) : 6);
     double in_bytes = 0.0;
     for (const StageInfo& st : b->stages) in_bytes += 8.0 * (double)(st.n + st.m_eq + st.m_ineq);
     const double per_stage = in_bytes / std::max(1, S);
     const char* l2env = getenv("ACOPF_L2_INPUT_MB");
     const double l2_budget = (l2env ? atof(l2env) : 8.0) * 1048576.0;
     const int64_t g_l2 = std::max<int64_t>(1, (int64_t)(l2_budget / std::max(1.0, per_stage)));
-    const int G = (int)std::max<int64_t>(1, std::min<int64_t>({64, total_recs / target_items, g_l2}));
+    const char* genv = getenv("ACOPF_MAX_G");          // development aid
+    const int64_t g_max = genv ? std::max(1, atoi(genv)) : 64;
+    // at least two stages per item where the L2 budget allows (one-stage items
+    // pay the table load per stage)
+    const int G = (int)std::max<int64_t>(std::min<int64_t>(2, g_l2),
+                                         std::min<int64_t>({g_max, total_recs / target_items, g_l2}));
     std::vector<DBusItem> items;
     std::vector<DRec> recs;
     size_t max_smem = 0;
