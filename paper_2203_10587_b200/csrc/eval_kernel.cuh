@@ -775,8 +775,7 @@ __device__ __forceinline__ double cost_term(const EvalParams& P, const DStage& S
 
 __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
     const DStage S = P.stages[s];
-    const DTopo T = P.topos[S.topo];
-    const int nb = T.nb, ng = T.ng;
+    const int nb = S.nb, ng = S.ng;
     const double* pg = P.x + S.var_off + 2 * nb;
     const int g = chunk * GEN_CHUNK + threadIdx.x;
     if (P.what & W_GRAD) {
@@ -798,6 +797,7 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
         }
     }
     if (chunk != 0 || !(P.what & W_OBJ)) return;
+    const DTopo T = P.topos[S.topo];
     // stage objective: numpy's pairwise sum over the ng cost terms (acopf.py:266-269).
     // The block first computes every term in parallel into shared memory (after
     // the leaves), so a leaf's sequential sum does not wait on global loads.
