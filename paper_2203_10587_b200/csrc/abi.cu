@@ -50,14 +50,21 @@ struct DevBuf {
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { if (p) cudaFree(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
     template <class T>
     T* upload(const std::vector<T>& v) {
+        release();                      // a re-upload (new layout) replaces the buffer
         n = std::max<size_t>(sizeof(T) * v.size(), 16);
         cuda_check(cudaMalloc(&p, n), "cudaMalloc");
         if (!v.empty()) cuda_check(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "H2D");
         return static_cast<T*>(p);
     }
     void* alloc(size_t bytes) {
+        release();
         n = std::max<size_t>(bytes, 16);
         cuda_check(cudaMalloc(&p, n), "cudaMalloc");
         // setup-time zeroing on the legacy stream: synchronise so it cannot land
