@@ -152,10 +152,26 @@ __device__ __forceinline__ void cp_async8s(unsigned dst, const void* src) {
     // has one) and the CTA barrier that follows it
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src));
 }
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// One 128-byte stage record by a TMA bulk copy completing on mbarrier mb
+// (issued by one thread; generic-proxy reads of dst finished before a barrier).
+__device__ __forceinline__ void record_load(unsigned mb, void* dst, const void* src) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 128;" ::"r"(mb) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(mb)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned mb, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(mb), "r"(parity)
+                     : "memory");
+    }
+}
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
@@ -551,12 +567,14 @@ __device__ __forceinline__ void copy_seg16(double* g, const double* s, int L, in
 template <unsigned WHAT>
 __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_tile_kernel(const EvalParams P, int item0) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) unsigned long long bar;
+    __shared__ __align__(8) unsigned long long bar, rbar;      // table load; stage records
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const DBusItem it = P.bus_items[item0 + blockIdx.x];
+    const unsigned rb_ = smem_u32(&rbar);
     if (tid == 0) {
         const unsigned b = smem_u32(&bar);
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rb_));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(it.bytes) : "memory");
         asm volatile(
@@ -614,11 +632,9 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
     const int my_e = tid;
     const bool any_a = need_j || need_h || need_c || need_f;
 
-    // first record and its inputs
-    if (tid < 8) cp_async16(reinterpret_cast<unsigned char*>(ctx) + 16 * tid,
-                            reinterpret_cast<const unsigned char*>(P.bus_recs + it.first) + 16 * tid);
-    cp_commit();
-    cp_wait<0>();
+    // first record (record k completes phase k of rbar) and its inputs
+    if (tid == 0) record_load(rb_, ctx, P.bus_recs + it.first);
+    mbar_wait(rb_, 0);
     __syncthreads();
     EndIn pre;
     prefetch(P, ctx[0], V, my_e, tid, sG, need_h, need_c, pre);
@@ -630,10 +646,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         if ((tid & 15) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
         __syncthreads();
         const bool more = ri + 1 < it.count;
-        if (more && tid < 8)
-            cp_async16(reinterpret_cast<unsigned char*>(ctx + ((ri + 1) & 1)) + 16 * tid,
-                       reinterpret_cast<const unsigned char*>(P.bus_recs + it.first + ri + 1) + 16 * tid);
-        cp_commit();
+        if (more && tid == 0) record_load(rb_, ctx + ((ri + 1) & 1), P.bus_recs + it.first + ri + 1);
         const long long eq_row = R.eq_row;
         const int nb = R.nb;
         // ---- A: branch ends (one side per warp), generator set-points ----------
@@ -652,7 +665,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
                           need_h ? __ldg(mu + nb + i) : 0.0, need_c ? __ldg(P.pd + R.pd_off + i) : 0.0,
                           need_c ? __ldg(P.qd + R.pd_off + i) : 0.0, sA, need_j, need_h, need_c, need_f);
             }
-        cp_wait<0>();          // the next record
+        if (more) mbar_wait(rb_, (ri + 1) & 1);       // the next record
         __syncthreads();
         // the gather buffer is free again: prefetch the next stage's inputs
 #ifndef ACOPF_DIAG_NO_PF
