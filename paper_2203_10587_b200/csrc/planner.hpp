@@ -716,8 +716,12 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         tt.gptr.push_back((uint16_t)(tt.gptr.back() + T.gen_ptr[b0 + bl + 1] - T.gen_ptr[b0 + bl]));
     next += 32;        // margin: lanes beyond a round's width read (and discard) up to 31 slots past it
     // pd, qd of every bus; the representative (first) end of every bus
-    for (int bl = 0; bl < nB; ++bl) loc_b[(size_t)5 * nB + bl] = next++;     // consecutive: the
-    for (int bl = 0; bl < nB; ++bl) loc_b[(size_t)6 * nB + bl] = next++;     // stores spread over banks
+    // consecutive, so the stores spread over the banks; qd starts 8 banks after pd
+    // (mod 16), so the epilogue's alternating pd / qd reads do not collide
+    const int pd0 = next;
+    for (int bl = 0; bl < nB; ++bl) loc_b[(size_t)5 * nB + bl] = next++;
+    next += ((pd0 + 8 - next) % 16 + 16) % 16;
+    for (int bl = 0; bl < nB; ++bl) loc_b[(size_t)6 * nB + bl] = next++;
     tt.rep.assign(nE, -1);
     for (int bl = 0; bl < nB; ++bl) {
         if (tt.busptr[bl + 1] == tt.busptr[bl]) tt.orph.push_back((uint16_t)bl);
