@@ -92,9 +92,16 @@ def test_shape_errors_before_any_device_work():
 
 # -- GPU: the device flows mode -------------------------------------------------
 
+@pytest.fixture(params=["0", "1"], ids=["gather", "interleaved"])
+def bus_inputs(request, monkeypatch):
+    """Both bus-input paths of the tile kernel (see test_gpu_parity.bus_inputs)."""
+    monkeypatch.setenv("ACOPF_INTERLEAVE", request.param)
+    return request.param
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", STAGES)
-def test_device_extract_matches_reference(name):
+def test_device_extract_matches_reference(name, bus_inputs):
     g = C.load("solution_" + name)
     case = stage_case(json.loads(str(g["spec"])))
     _, lay = pkg.build_acopf(case)
@@ -110,7 +117,7 @@ def test_device_extract_matches_reference(name):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", COMPOSITES)
-def test_device_composite_extract_matches_reference(name):
+def test_device_composite_extract_matches_reference(name, bus_inputs):
     """All stages' flows from one launch over the composite evaluator."""
     g = C.load("solution_" + name)
     p, imap = _composite(name)
