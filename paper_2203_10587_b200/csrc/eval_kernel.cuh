@@ -235,12 +235,13 @@ __device__ __forceinline__ void prefetch(const EvalParams& P, const DRec& R, con
     const int f = V.f[e], t = V.t[e], r = V.ridx[e];
     if (P.xi) {
         // both buses' (VA, VM, muP, muQ): one 256-bit load each from the
-        // interleaved copy (the multipliers are zeros unless the Hessian is asked)
+        // interleaved copy (the multipliers are zeros unless the Hessian is asked),
+        // cached in L2 only (scattered, little L1 reuse)
         const double* xi = opaque(static_cast<const double*>(P.xi) + 4 * R.var_off);
-        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        asm("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
             : "=d"(in.vaf), "=d"(in.vf), "=d"(in.mpf), "=d"(in.mqf)
             : "l"(xi + 4 * f));
-        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        asm("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
             : "=d"(in.vat), "=d"(in.vt), "=d"(in.mpt), "=d"(in.mqt)
             : "l"(xi + 4 * t));
     } else {
@@ -268,7 +269,7 @@ __device__ __forceinline__ void prefetch(const EvalParams& P, const DRec& R, con
         if (r >= 0) {
             const double* mi = P.mult + R.ineq_row + 2 * in.rs;
             if ((reinterpret_cast<uintptr_t>(P.mult + R.ineq_row) & 15) == 0) {   // stage-uniform
-                const double2 m2 = __ldg(reinterpret_cast<const double2*>(mi));
+                const double2 m2 = __ldcg(reinterpret_cast<const double2*>(mi));   // L2 only
                 in.sf = m2.x;
                 in.st = m2.y;
             } else {
