@@ -435,8 +435,10 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
             if (f != t) {
                 const double a0 = f < t ? r0 : r1, a1 = f < t ? r1 : r0, a2 = f < t ? r2 : r3, a3 = f < t ? r3 : r2;
                 if ((reinterpret_cast<uintptr_t>(out) & 31) == 0) {      // the row is one 32-byte sector
-                    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(out), "d"(a0), "d"(a1), "d"(a2),
-                                 "d"(a3)
+                    unsigned long long pol;                                // written once: evict-first
+                    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+                    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(out), "d"(a0),
+                                 "d"(a1), "d"(a2), "d"(a3), "l"(pol)
                                  : "memory");
                 } else if (v2) {
                     reinterpret_cast<double2*>(out)[0] = make_double2(a0, a1);
@@ -727,9 +729,14 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
                         const int n16 = (L - peel) >> 1;
                         if (peel) g[0] = sp[0];
                         if (n16 > 0) {
-                            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g + peel),
-                                         "r"(smem_u32(sp + peel)), "r"(16 * n16)
-                                         : "memory");
+                            // written once: evict-first in L2, so the stage inputs stay
+                            unsigned long long pol;
+                            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+                            asm volatile(
+                                "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                                    g + peel),
+                                "r"(smem_u32(sp + peel)), "r"(16 * n16), "l"(pol)
+                                : "memory");
                             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                         }
                         if ((L - peel) & 1) g[L - 1] = sp[L - 1];
