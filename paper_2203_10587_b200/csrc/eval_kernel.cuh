@@ -580,10 +580,13 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rb_));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(it.bytes) : "memory");
+        // tile tables are read by every item of their tile: evict-last in L2
+        unsigned long long pol;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
         asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(smem)),
-            "l"(P.blob + it.blob_off), "r"(it.bytes), "r"(b)
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+            "%4;" ::"r"(smem_u32(smem)),
+            "l"(P.blob + it.blob_off), "r"(it.bytes), "r"(b), "l"(pol)
             : "memory");
     }
     // WHAT != 0: the mask is a compile-time constant (the all-callbacks path)
