@@ -232,7 +232,7 @@ static void upload(acopf_batch* b) {
     for (const StageInfo& st : b->stages) in_bytes += 8.0 * (double)(st.n + st.m_eq + st.m_ineq);
     const double per_stage = in_bytes / std::max(1, S);
     const char* l2env = getenv("ACOPF_L2_INPUT_MB");
-    const double l2_budget = (l2env ? atof(l2env) : 8.0) * 1048576.0;
+    const double l2_budget = (l2env ? atof(l2env) : 32.0) * 1048576.0;
     const int64_t g_l2 = std::max<int64_t>(1, (int64_t)(l2_budget / std::max(1.0, per_stage)));
     const char* genv = getenv("ACOPF_MAX_G");          // development aid
     const int64_t g_max = genv ? std::max(1, atoi(genv)) : 64;
