@@ -187,3 +187,15 @@ def test_tile_tables_hub_network():
     st = p.evaluator.verify_plan()
     assert st["ends"] > 128 and st["max_smem_bytes"] <= 220 * 1024
     assert st["store_wavefronts_ideal"] <= st["store_wavefronts_half"] <= 4 * st["store_wavefronts_ideal"]
+
+
+def test_parallel_planner_is_deterministic():
+    """Tile tables are built on all host cores: two builds of a contingency composite
+    give identical plans (table counts, areas, rounds, modeled store cost)."""
+    spec = COMPOSITE_SPECS["scopf_corrective"]
+    stats = []
+    for _ in range(2):
+        a, _ = composite_inputs(spec)
+        p, _ = compose(pkg, spec["kind"], a)
+        stats.append(p.evaluator.verify_plan())
+    assert stats[0] == stats[1]
