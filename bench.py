@@ -1,25 +1,34 @@
 #!/usr/bin/env python
 """Benchmark: ACOPF callback evaluations/sec on B200 (BASELINE.json metric).
 
-Default workload = BASELINE config 1: the synthetic 10,000-bus network
-(tree + 3,000 chords, 2,500 generators), 100 seeded evaluation points; one
-step = one batched evaluation of objective + gradient + constraints +
-Jacobian values + Lagrangian-Hessian values at all 100 points (one kernel
-launch).  ``--config 2|3|4`` benches the composite configs instead (one step
-= one evaluation of the whole composite).
+Default workload = BASELINE config 4, the largest configuration that fits one
+GPU: the stochastic SCOPF composite on the synthetic 25,000-bus network
+(32 scenarios x (base + 31 N-1 contingencies) = 1,024 stages).  One step =
+one evaluation of objective + gradient + constraints (incl. coupling rows) +
+Jacobian values + Lagrangian-Hessian values of the whole composite.
+``--config 1|2|3`` benches the other configurations (config 1: 100 seeded
+points of the 10,000-bus network per step, one launch).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-Under torchrun (N > 1) every rank evaluates its own 100-point batch on its
-GPU (config 1 does not shard: replicas, weak scaling); the time is the max
-over ranks of the device-measured time.  ``--impl reference`` times the
-reference algorithm's CPU implementation (the numpy oracle port, bit-exact to
-the reference) on all host cores instead.
+Under torchrun (N > 1) the composite configs are sharded over the ranks
+(contiguous stage blocks, scenario-aligned for config 4) with the NCCL halo
+and ordered objective inside the C ABI's multi-GPU entry point (strong
+scaling); config 1 runs one 100-point batch per rank (replicas, weak).  The
+time is the max over ranks of the device-measured time.
 
-Timing: W untimed warm-up steps; each timed step is bracketed by CUDA events
-on the launching stream; a 256 MiB buffer is written between timed steps to
-flush the 126 MB L2 (not timed).  nvidia-smi clocks are sampled during the
-timed region.  Rank 0 prints one JSON line.
+``--impl reference`` times the reference algorithm's CPU implementation (the
+numpy/scipy oracle port, bit-exact to the reference's callbacks) on all host
+cores, on stage slices of the same workload (EMPAR-style process pool,
+runner.py:305-312), extrapolated linearly to the whole composite (composite
+cost is linear in the stage count).
+
+Timing: W untimed warm-up steps.  Config 4's inputs (1.5 GB) and outputs
+(9.9 GB) are far larger than the 126 MB L2, so its K steps run back to back
+between one pair of CUDA events (write-back inside the timed window); for
+configs 1-3 a 256 MiB buffer is written between timed steps (untimed) and each
+step is bracketed by events on the launching stream.  nvidia-smi clocks are
+sampled during the timed region.  Rank 0 prints one JSON line.
 """
 
 from __future__ import annotations
@@ -41,6 +50,8 @@ sys.path.insert(0, HERE)
 METRIC = "ACOPF callback evals/sec (obj+grad+g+h+J+H), 1/2/4/8 GPU; % HBM roofline"
 UNIT = "evals/s"
 FALLBACK_HBM_GBS = 6650.0
+DEFAULT_CONFIG = 4
+STAGES = {1: 1, 2: 1025, 3: 96, 4: 1024}
 
 
 def parse():
@@ -49,7 +60,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", type=int, default=1, choices=(1, 2, 3, 4))
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=(1, 2, 3, 4))
     ap.add_argument("--points", type=int, default=100, help="evaluation points per step (config 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -68,8 +79,8 @@ def dist_env():
 
 def workload_desc(cfg: int, points: int) -> dict:
     return {
-        1: dict(workload=f"cfg1: synthetic 10,000-bus network (tree + 3,000 chords, 12,999 branches, "
-                         f"2,500 generators), {points} seeded points per step, batch=1 each"),
+        1: dict(workload="cfg1: synthetic 10,000-bus network (tree + 3,000 chords, 12,999 branches, "
+                         "2,500 generators), batch=1 evaluations at seeded points"),
         2: dict(workload="cfg2: N-1 SCOPF composite, 2,000-bus network (tree + 600 chords, 500 gens), "
                          "base + 1,024 non-bridge branch contingencies (1,025 stages), corrective dc=0.1 pu"),
         3: dict(workload="cfg3: multiperiod composite, 2,000-bus network, 96 periods, seeded daily load "
@@ -95,8 +106,9 @@ def _composite_args(cfg: int):
 class Runner:
     """One benchmark step = one evaluation of the workload on this rank's GPU."""
 
-    def __init__(self, ev, x_h, m_h, units, sharded=None):
+    def __init__(self, ev, x_h, m_h, units, sharded=None, n_coupling=0):
         self.ev, self.x_h, self.m_h, self.units, self.sharded = ev, x_h, m_h, units, sharded
+        self.n_coupling = n_coupling          # coupling rows of this rank's evaluator
 
 
 def build_ours(cfg: int, points: int, device: int, seed0: int, dist=None, rank=0, world=1):
@@ -130,21 +142,22 @@ def build_ours(cfg: int, points: int, device: int, seed0: int, dist=None, rank=0
         xl, xu = np.zeros(len(kinds)), np.ones(len(kinds))
         x, _ = syn.random_point(kinds, xl + 0.1, xu, 1, seed0)
         x = np.concatenate([x, np.zeros(sc.n_x - sc.plan.n_loc)])
-        return Runner(sc.ev, x, rng.standard_normal(sc.ev.m), 1, sharded=sc)
+        return Runner(sc.ev, x, rng.standard_normal(sc.ev.m), 1, sharded=sc, n_coupling=len(sc.plan.coupling.row))
     fn = {"scopf": compose_scopf, "multiperiod": compose_multiperiod, "general": compose_general}[kind]
     p, imap = fn(*args, device=device)
     ev = p.evaluator
     kinds = syn.variable_kinds([(pl.topo.nb, pl.topo.ng) for pl in ev.plans])
     x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, seed0)
-    return Runner(ev, x, mult, 1)
+    return Runner(ev, x, mult, 1, n_coupling=len(imap.coupling_rows))
 
 
-def algorithmic_bytes(ev) -> int:
-    """fp64 reads of x, mult, per-stage loads, topology once; writes of all outputs."""
+def algorithmic_bytes(ev, n_coupling: int = 0) -> int:
+    """fp64 reads of x, the stage multipliers (coupling-row multipliers are never
+    read), per-stage varying loads and the topology once; writes of every output value."""
     topo_bytes = sum(72 * t.nbr + 32 * t.nb + 28 * t.ng for t in ev.topos)
     load_sets = {(id(p.topo), p.load_key) for p in ev.plans}
     extra_loads = 16 * sum(ev.plans[0].topo.nb for _ in range(max(0, len(load_sets) - len(ev.topos))))
-    reads = 8 * (ev.n + ev.m) + topo_bytes + extra_loads
+    reads = 8 * (ev.n + ev.m - n_coupling) + topo_bytes + extra_loads
     writes = 8 * (ev.n_obj + ev.n + ev.m + ev.nnz_j + ev.nnz_h)
     return int(reads + writes)
 
@@ -168,7 +181,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
         time.sleep(0.25)
@@ -203,25 +216,49 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline / reference arm (oracle port of the reference algorithm)
+# CPU baseline / reference arm: the oracle port of the reference algorithm on
+# stage slices of the workload (test infrastructure; never the measured GPU path)
 
+SLICE_STAGES = {1: 1, 2: 2, 3: 4, 4: 2}       # stages per slice (one slice ~0.1-0.4 s on one core)
 _ORACLE = {}
 
 
-def _oracle_init(cfg):
+def _slice_oracle(cfg: int, which: int):
+    """The reference's composite callbacks (oracle port) on slice `which` of config cfg: cfg1 one
+    stage; cfg2 base + 1 contingency; cfg3 4 consecutive periods; cfg4 one scenario's base + 1
+    contingency.  Returns (callbacks object, stages in the slice)."""
     from paper_2203_10587_b200 import synthetic as syn
+    from paper_2203_10587_b200.grid import ContingencySet, ScenarioSet
+    from paper_2203_10587_b200.types import CouplingMode
+    from oracle.composite import CompositeOracle
     from oracle.stage import StageOracle
-    case = syn.config_case(1)
-    o = StageOracle(case)
-    kinds = syn.variable_kinds([(o.nb, o.ng)])
-    _ORACLE["o"] = o
-    _ORACLE["kinds"] = kinds
+    k = SLICE_STAGES[cfg]
+    if cfg == 1:
+        return StageOracle(syn.config_case(1)), 1
+    if cfg == 2:
+        base, ctgs = _ORACLE.setdefault("in2", None) or _ORACLE.setdefault("in2", syn.config2_inputs())
+        c = tuple(ctgs.by_id())
+        sub = ContingencySet(tuple(c[(which * (k - 1) + j) % len(c)] for j in range(k - 1)))
+        return CompositeOracle.general(None, sub, [base], CouplingMode(), 30.0), k
+    if cfg == 3:
+        periods = _ORACLE.get("in3") or _ORACLE.setdefault("in3", syn.config3_periods())
+        t0 = (which * k) % (len(periods) - k + 1)
+        return CompositeOracle.general(None, None, periods[t0:t0 + k], CouplingMode(), 15.0), k
+    base, scens, ctgs = _ORACLE.get("in4") or _ORACLE.setdefault("in4", syn.config4_inputs())
+    c = tuple(ctgs.by_id())
+    sc = scens.scenarios[which % len(scens.scenarios)]
+    sub = ContingencySet(tuple(c[(which * (k - 1) + j) % len(c)] for j in range(k - 1)))
+    return CompositeOracle.general(ScenarioSet((sc,)), sub, [base], CouplingMode(), 30.0), k
 
 
-def _oracle_eval(seed):
+def _slice_points(o, n: int, seed: int):
     from paper_2203_10587_b200 import synthetic as syn
-    o = _ORACLE["o"]
-    x, mult = syn.random_point(_ORACLE["kinds"], o.xl, o.xu, o.m_eq + o.m_ineq, seed)
+    stages = getattr(o, "stage", [o])
+    kinds = syn.variable_kinds([(s.nb, s.ng) for s in stages])
+    return [syn.random_point(kinds, o.xl, o.xu, o.m_eq + o.m_ineq, seed + i) for i in range(n)]
+
+
+def _slice_eval(o, x, mult) -> float:
     t = time.perf_counter()
     o.objective(x)
     o.gradient(x)
@@ -231,47 +268,94 @@ def _oracle_eval(seed):
     return time.perf_counter() - t
 
 
-def cpu_baseline_single(seconds: float = 12.0) -> dict:
-    """1-core oracle port, bounded sample of config-1 points."""
-    _oracle_init(1)
-    _oracle_eval(0)
+def _worker_init(cfg, counter):
+    with counter.get_lock():
+        wid = counter.value
+        counter.value += 1
+    o, k = _slice_oracle(cfg, wid)
+    _ORACLE["slice"] = (o, k, _slice_points(o, 2, 7_000 + 10 * wid))
+    _ORACLE["calls"] = 0
+
+
+def _worker_task(_):
+    o, k, pts = _ORACLE["slice"]
+    x, m = pts[_ORACLE["calls"] % len(pts)]     # points made at init: only the callbacks are timed
+    _ORACLE["calls"] += 1
+    _slice_eval(o, x, m)
+    return k
+
+
+def sample_desc(cfg: int, k: int) -> str:
+    return {1: "one cfg1 evaluation point",
+            2: f"a {k}-stage slice of the cfg2 composite (base + {k - 1} contingencies)",
+            3: f"a {k}-period slice of the cfg3 composite",
+            4: f"a {k}-stage slice of the cfg4 composite (one scenario's base + {k - 1} contingencies)"}[cfg]
+
+
+def cpu_baseline_single(cfg: int, seconds: float = 12.0) -> dict:
+    """1-core oracle port on a bounded sample of the workload, extrapolated to one full eval."""
+    o, k = _slice_oracle(cfg, 0)
+    pts = _slice_points(o, 4, 1000)
+    _slice_eval(o, *pts[0])
     spent, n = 0.0, 0
     while spent < seconds and n < 400:
-        spent += _oracle_eval(1000 + n)
+        spent += _slice_eval(o, *pts[n % len(pts)])
         n += 1
-    return {"value": n / spent, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"cfg1 10k-bus network, {n} seeded points x (obj+grad+cons+jac+hess), "
-                      f"numpy/scipy oracle port (bit-exact to the reference), 1 thread, {spent:.1f} s"}
+    per_slice = spent / n
+    value = 1.0 / (per_slice * STAGES[cfg] / k)
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{n} evaluations (obj+grad+cons+jac+hess) of {sample_desc(cfg, k)}, "
+                      f"{1000 * per_slice:.1f} ms each, extrapolated linearly x{STAGES[cfg] // k} to the "
+                      f"{STAGES[cfg]}-stage workload; numpy/scipy oracle port (bit-exact to the "
+                      f"reference), 1 thread, {spent:.1f} s"}
 
 
 def run_reference(args, rank: int, world: int) -> None:
+    """The reference algorithm (oracle port) on all host cores: each step, every worker evaluates
+    its own prebuilt stage slice once (EMPAR-style pool, runner.py:305-312)."""
     if rank != 0:
         return
     import multiprocessing as mp
+    cfg = args.config
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     ctx = mp.get_context("fork")
-    per_step = 2 * cores
-    with ctx.Pool(cores, initializer=_oracle_init, initargs=(1,)) as pool:
-        for w in range(max(args.warmup, 1)):
-            pool.map(_oracle_eval, range(per_step))
+    counter = ctx.Value("i", 0)
+    k = SLICE_STAGES[cfg]
+    tasks = cores * (2 if cfg == 1 else 1)
+    with ctx.Pool(cores, initializer=_worker_init, initargs=(cfg, counter)) as pool:
+        for _ in range(max(args.warmup, 1)):
+            pool.map(_worker_task, range(tasks), chunksize=1)
         times = []
-        for k in range(args.steps):
+        for _ in range(args.steps):
             t = time.perf_counter()
-            pool.map(_oracle_eval, range(10_000 + k * per_step, 10_000 + (k + 1) * per_step))
+            stages = sum(pool.map(_worker_task, range(tasks), chunksize=1))
             times.append(time.perf_counter() - t)
     total = sum(times)
-    value = per_step * args.steps / total
+    evals_per_step = stages / STAGES[cfg]
+    value = evals_per_step * args.steps / total
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": dict(workload_desc(1, per_step), points_per_step=per_step, parallelism=f"{cores} host processes"),
+        "scaling": "weak" if (cfg == 1 or world == 1) else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, SURVEY §8d)", "impl": "reference",
+        "config": workload_config(cfg),
+        "parallelism": f"{cores} host processes",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{per_step} cfg1 points per step over {cores} worker processes "
-                                   "(EMPAR-style pool, runner.py:305-312), numpy/scipy oracle port"},
+                         "sample": f"per step, {tasks} evaluations (obj+grad+cons+jac+hess) of "
+                                   f"{sample_desc(cfg, k)} over {cores} worker processes (EMPAR-style pool, "
+                                   f"runner.py:305-312) = {evals_per_step:.4g} of one full evaluation "
+                                   f"(linear extrapolation over {STAGES[cfg]} stages); numpy/scipy oracle "
+                                   "port, bit-exact to the reference's callbacks"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg: int) -> dict:
+    """The `config` object of both arms (identical for the same workload)."""
+    d = workload_desc(cfg, 0)
+    d["stages_per_eval"] = STAGES[cfg]
+    return d
 
 
 # ---------------------------------------------------------------------------
@@ -284,11 +368,9 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    torch.cuda.set_device(local)
     if world > 1:
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     run = build_ours(args.config, args.points, local, seed0=1_000_000 * (rank + 1), dist=dist if world > 1 else None,
                      rank=rank, world=world)
@@ -300,7 +382,8 @@ def main():
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    back_to_back = args.config == 4          # inputs and outputs >> L2
+    flush = None if back_to_back else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     from paper_2203_10587_b200 import _lib as L
 
     def step():
@@ -317,19 +400,25 @@ def main():
     launches0 = ev.launches()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
+        if back_to_back:
+            t0.record(stream)
         for k in range(args.steps):
-            flush.zero_()
+            if flush is not None:
+                flush.zero_()
             starts[k].record(stream)
             step()
             ends[k].record(stream)
+        if back_to_back:
+            t1.record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     gpu_launches = ev.launches() - launches0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = float(sum(step_ms))
+    total_ms = t0.elapsed_time(t1) if back_to_back else float(sum(step_ms))
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -337,19 +426,20 @@ def main():
     # config 1: every rank evaluates its own batch (weak); composites: one composite over all ranks (strong)
     value = (units * world if sc is None else units) * args.steps / (total_ms / 1000.0)
 
-    # roofline of the (single) evaluation kernel
-    bytes_step = algorithmic_bytes(ev)
+    # roofline of the evaluation (the tile kernel dominates; the generator/coupling kernel
+    # runs beside it on a forked stream and is inside the measured step)
+    bytes_step = algorithmic_bytes(ev, run.n_coupling)
     if world > 1 and sc is not None:
         b = torch.tensor([float(bytes_step)], dtype=torch.float64, device=dev)
         dist.all_reduce(b)              # the whole composite's bytes
         bytes_step = int(b.item())
-    kernel_ms = statistics.mean(step_ms)
+    kernel_ms = total_ms / args.steps
     peaks_path = os.path.join(HERE, "MEASURED_PEAKS.json")
     if os.path.exists(peaks_path):
-        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured"
+        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     else:
-        peak, peak_src = FALLBACK_HBM_GBS, "fallback"
-    achieved = bytes_step / (kernel_ms / 1000.0) / 1e9 / (world if sc is not None else 1)
+        peak, peak_src = FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+    achieved = bytes_step / (kernel_ms / 1000.0) / 1e9
     traffic = None
     tpath = os.path.join(HERE, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -360,48 +450,52 @@ def main():
     if not args.no_e2e and sc is None:
         xp = torch.from_numpy(x_h).pin_memory()
         mp_ = torch.from_numpy(m_h).pin_memory()
-        hout = {k: torch.empty(v.numel(), dtype=torch.float64).pin_memory() for k, v in out.items()}
         sizes = dict(obj=ev.n_obj, grad=ev.n, cons=ev.m, jac=ev.nnz_j, hess=ev.nnz_h)
-        hout = {k: hout[k][:sizes[k]] for k in hout}
+        del out                         # the device outputs are not needed any more (HBM for the host path)
+        hout = {k: torch.empty(max(n, 1), dtype=torch.float64).pin_memory()[:n] for k, n in sizes.items()}
         for _ in range(2):
             ev.eval_host_ptrs(xp.data_ptr(), mp_.data_ptr(), 1.0, L.ALL, hout, stream=sptr)
         e_steps = max(3, min(args.steps, 10))
-        es = [torch.cuda.Event(enable_timing=True) for _ in range(e_steps)]
-        ee = [torch.cuda.Event(enable_timing=True) for _ in range(e_steps)]
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        es.record(stream)
         for k in range(e_steps):
-            es[k].record(stream)
             ev.eval_host_ptrs(xp.data_ptr(), mp_.data_ptr(), 1.0, L.ALL, hout, stream=sptr)
-            ee[k].record(stream)
+        ee.record(stream)
         torch.cuda.synchronize(dev)
-        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(es, ee))], dtype=torch.float64, device=dev)
+        e_ms = torch.tensor([es.elapsed_time(ee)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": units * world * e_steps / (float(e_ms.item()) / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": 8 * (ev.n + ev.m),
                "d2h_bytes_per_step": 8 * sum(sizes.values()),
-               "path": "acopf_batch_eval_host (C ABI) on pinned host buffers"}
+               "path": "acopf_batch_eval_host (C ABI) on pinned host buffers, "
+                       f"{e_steps} steps back to back"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == 1:
-        cpu = cpu_baseline_single()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_single(args.config)
 
     if rank == 0:
-        cfg = workload_desc(args.config, args.points)
-        cfg.update(points_per_step=units if args.config == 1 else None, stages_per_step=len(ev.plans),
-                   l2="256 MiB buffer written between timed steps (untimed)",
-                   parallelism=(f"replicas x{world}" if sc is None else f"stage shards x{world} (NCCL halo + objective)")
-                   if world > 1 else "single GPU",
-                   algorithmic_bytes_per_step=bytes_step)
+        cfg = workload_config(args.config)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if (args.config == 1 or world == 1) else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded, SURVEY §8d)",
             "config": cfg,
+            "parallelism": (f"replicas x{world}" if sc is None else f"stage shards x{world} (NCCL halo + objective)")
+                           if world > 1 else "single GPU",
+            "units_per_step": units * (world if sc is None else 1),
+            "l2": ("inputs (x + multipliers) and outputs exceed the 126 MB L2 many times over; the K steps "
+                   "run back to back between one pair of CUDA events" if back_to_back else
+                   "256 MiB buffer written between timed steps (untimed); each step bracketed by CUDA events"),
+            "algorithmic_bytes_per_step": bytes_step,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "acopf_tile_kernel (one launch per step; the generator/objective kernel "
-                                   "runs concurrently on a forked stream and is included in kernel_ms)",
+                         "traffic_source": "profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum "
+                                           "of the tile kernel per launch, from the committed ncu capture",
+                         "kernel": "acopf_tile_kernel (one launch per step; the generator/coupling kernel "
+                                   "runs concurrently on a forked stream and is inside the step)",
                          "kernel_ms": kernel_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -26,8 +26,9 @@
  * function returns 0 on success and nonzero on failure; the message is in
  * acopf_last_error() (thread-local).  Device pointers are CUDA global memory on
  * the handle's device.  Evaluation is stream-ordered on the given stream
- * (NULL = the handle's own stream); one handle must not be evaluated
- * concurrently from two streams (it owns one objective scratch buffer).
+ * (NULL = the legacy default stream, CUDA's convention; torch's default
+ * stream is that stream); one handle must not be evaluated concurrently from
+ * two streams (it owns one objective scratch buffer).
  */
 #ifndef ACOPF_B200_H
 #define ACOPF_B200_H
@@ -100,8 +101,15 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
                      double* hval, void* stream);
 
 /* Same, host pointers (pinned memory gives asynchronous copies); sizes of the
- * flat buffers in doubles.  Copies in, evaluates and copies out on `stream`
- * (NULL = the handle's stream), then synchronises that stream. */
+ * flat buffers in doubles.  Every requested output must be non-NULL with at
+ * least the layout's size (x: the flat variable count, obj: 1 or the largest
+ * objective slot + 1, cons: rows, jval / hval: values), and the Hessian needs
+ * mult with at least the row count; otherwise the call fails before any copy.
+ * Copies in, evaluates and copies out on `stream` (NULL = the handle's own
+ * stream; its device buffers are internal), then synchronises that stream.
+ * Layouts whose stages are contiguous and in order (independent points) are
+ * pipelined in chunks over three streams; any other layout runs as one
+ * H2D / evaluate / D2H sequence. */
 int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double obj_factor,
                           const double* mult, int64_t nm, uint32_t what, double* obj, int64_t nobj,
                           double* grad, int64_t ngrad, double* cons, int64_t ncons, double* jval,

@@ -108,6 +108,9 @@ struct acopf_batch {
     std::vector<int64_t> cp_row, cp_jpos, cp_a, cp_b;
     std::vector<int8_t> cp_first;
     int obj_mode = 0, n_obj = 0;
+    // flat-buffer totals implied by the layout (set_layout): x rows, constraint
+    // rows, J values, H values, objective slots
+    int64_t tot_n = 0, tot_m = 0, tot_j = 0, tot_h = 0, tot_obj = 0;
     // device
     cudaStream_t stream = nullptr;
     DevBuf d_topo, d_stage, d_items, d_recs, d_aux, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
@@ -295,7 +298,22 @@ static void upload(acopf_batch* b) {
     // pipeline chunks for host-buffer evaluation of independent layouts: about 8
     // chunks of whole stage groups (bus items are stage-group-major)
     b->pipe.clear();
-    if (b->obj_mode == 0 && n_coupling == 0 && S >= 2) {
+    // the chunked copies move [off6(s0), off6(s1)) ranges: only valid when every
+    // stage's blocks are contiguous and in stage order ([eq; ineq] rows, [Jeq; Jineq]
+    // values, x, H values, objective slot s)
+    bool contiguous = true;
+    for (int s = 0; s < S && contiguous; ++s) {
+        const StageInfo& st = b->stages[s];
+        const int64_t* o = &b->off6[6 * s];
+        const int64_t nx[6] = {o[0] + st.n, o[2] + st.m_ineq, 0, o[4] + st.nnz_jin, 0, o[5] + st.nnz_h};
+        contiguous = b->obj_slot[s] == s && o[1] + st.m_eq == o[2] && o[3] + st.nnz_jeq == o[4];
+        if (s == 0) contiguous = contiguous && o[0] == 0 && o[1] == 0 && o[3] == 0 && o[5] == 0;
+        if (s + 1 < S) {
+            const int64_t* q = &b->off6[6 * (s + 1)];
+            contiguous = contiguous && q[0] == nx[0] && q[1] == nx[1] && q[3] == nx[3] && q[5] == nx[5];
+        }
+    }
+    if (b->obj_mode == 0 && n_coupling == 0 && S >= 2 && contiguous) {
         const int ngroups = (S + G - 1) / G;
         const int nchunks = getenv("ACOPF_PIPE_CHUNKS") ? std::max(1, atoi(getenv("ACOPF_PIPE_CHUNKS"))) : 8;   // development aid
         const int per = std::max(1, (ngroups + nchunks - 1) / nchunks);
@@ -650,6 +668,29 @@ int acopf_batch_set_layout(acopf_batch* b, const int64_t* offsets6, int32_t obj_
         b->cp_b.assign(cp_b, cp_b + n_coupling);
         b->cp_first.assign(cp_base_first, cp_base_first + n_coupling);
         b->obj_mode = obj_mode;
+        int64_t tn = 0, tm = 0, tj = 0, th = 0, to = obj_mode == 1 ? 1 : 0;
+        for (int s = 0; s < S; ++s) {
+            const StageInfo& st = b->stages[s];
+            const int64_t* o = &b->off6[6 * s];
+            if (o[0] < 0 || o[1] < 0 || o[2] < 0 || o[3] < 0 || o[4] < 0 || o[5] < 0)
+                throw std::runtime_error("negative layout offset");
+            tn = std::max(tn, o[0] + st.n);
+            tm = std::max({tm, o[1] + st.m_eq, o[2] + st.m_ineq});
+            tj = std::max({tj, o[3] + st.nnz_jeq, o[4] + st.nnz_jin});
+            th = std::max(th, o[5] + st.nnz_h);
+            if (obj_mode != 1) {
+                if (obj_slot[s] < 0) throw std::runtime_error("negative objective slot");
+                to = std::max<int64_t>(to, (int64_t)obj_slot[s] + 1);
+            }
+        }
+        for (int64_t c = 0; c < n_coupling; ++c) {
+            if (cp_row[c] < 0 || cp_jpos[c] < 0 || cp_a[c] < 0 || cp_b[c] < 0)
+                throw std::runtime_error("negative coupling index");
+            tm = std::max(tm, cp_row[c] + 1);
+            tj = std::max(tj, cp_jpos[c] + 2);
+            tn = std::max({tn, cp_a[c] + 1, cp_b[c] + 1});
+        }
+        b->tot_n = tn; b->tot_m = tm; b->tot_j = tj; b->tot_h = th; b->tot_obj = to;
         b->laid_out = true;
         b->uploaded = false;
     });
@@ -682,7 +723,8 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         EvalParams P = b->params;
         P.x = x; P.mult = mult; P.obj_factor = obj_factor; P.what = what;
         P.obj = obj; P.grad = grad; P.cons = cons; P.jval = jval; P.hval = hval;
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
+        // NULL = the legacy default stream (CUDA's convention, and torch's default stream)
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
         const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) && P.n_bus_items > 0;
         static const bool no_aux = getenv("ACOPF_EXP_NO_AUX") != nullptr;   // development aid: tile kernel alone
         const bool aux = !no_aux && (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
@@ -726,7 +768,7 @@ int acopf_batch_flows(acopf_batch* b, const double* x, double* flows, double* in
         P.x = x; P.mult = nullptr; P.obj_factor = 0.0; P.what = W_FLOWS;
         P.obj = P.grad = P.cons = P.jval = P.hval = nullptr;
         P.flows = flows; P.inj = inj;
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);     // NULL = legacy default stream
         if (P.n_bus_items > 0) {
             launch_interleave(b, P, 0, (int)b->stages.size(), st);
             acopf_tile_kernel<0u><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
@@ -742,6 +784,22 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
                           void* stream) {
     return guard([&] {
         if (!b->laid_out) throw std::runtime_error("acopf_batch_set_layout was not called");
+        // every requested output needs a host buffer of at least the layout's size;
+        // every evaluation reads x, the Hessian also the multipliers
+        auto need = [&](bool on, const void* p, int64_t have, int64_t want, const char* name) {
+            if (!on) return;
+            if (!p) throw std::runtime_error(std::string(name) + " is NULL");
+            if (have < want)
+                throw std::runtime_error(std::string(name) + " has " + std::to_string(have) + " doubles, the layout needs " +
+                                         std::to_string(want));
+        };
+        need(what & ACOPF_ALL, x, nx, b->tot_n, "x");
+        need(what & ACOPF_OBJ, obj, nobj, b->tot_obj, "obj");
+        need(what & ACOPF_GRAD, grad, ngrad, b->tot_n, "grad");
+        need(what & ACOPF_CONS, cons, ncons, b->tot_m, "cons");
+        need(what & ACOPF_JAC, jval, nj, b->tot_j, "jval");
+        need(what & ACOPF_HESS, hval, nh, b->tot_h, "hval");
+        need(what & ACOPF_HESS, mult, nm, b->tot_m, "mult");
         cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
         auto ensure = [&](DevBuf& d, int64_t n) -> double* {
             size_t bytes = sizeof(double) * (size_t)std::max<int64_t>(n, 1);

@@ -428,7 +428,9 @@ inline void TileTable::serialise(const Topo& T, std::vector<uint8_t>& blob, unsi
         std::vector<uint32_t> dw(9 * (size_t)nE);
         for (int e = 0; e < nE; ++e)
             for (int k = 0; k < 9; ++k)
-                dw[9 * (size_t)e + k] = (uint32_t)(8 * dstR[(size_t)(2 * k) * nE + e]) |
+                if (8 * dstR[(size_t)(2 * k) * nE + e] > 0xffff || 8 * dstR[(size_t)(2 * k + 1) * nE + e] > 0xffff)
+                    throw std::runtime_error("planner: area byte offset exceeds 16 bits");
+                else dw[9 * (size_t)e + k] = (uint32_t)(8 * dstR[(size_t)(2 * k) * nE + e]) |
                                         ((uint32_t)(8 * dstR[(size_t)(2 * k + 1) * nE + e]) << 16);
         put(h.o_dst, dw.data(), 4 * dw.size());
     }
@@ -728,7 +730,8 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         else tt.rep[tt.bend[tt.busptr[bl]]] = bl;
     }
     tt.nArea = next;
-    if (tt.nArea >= 8192) throw std::runtime_error("tile working area exceeds 64 KB");
+    // (+4: serialise() may insert up to four staging-parity slots; byte offsets are 16-bit)
+    if (tt.nArea + 4 >= 8192) throw std::runtime_error("tile working area exceeds 64 KB");
     if (nB >= 0x8000) throw std::runtime_error("tile has too many buses");
     for (int v : cpos) tt.cpos.push_back((uint16_t)v);
     for (int v : nega) tt.nega.push_back((uint16_t)v);

@@ -224,11 +224,23 @@ class BatchEvaluator:
         return dict(obj=mk(self.n_obj), grad=mk(self.n), cons=mk(self.m),
                     jac=mk(self.nnz_j), hess=mk(self.nnz_h))
 
+    def stream_handle(self, stream=None) -> ctypes.c_void_p:
+        """The cudaStream_t to launch on: ``stream`` (a raw handle or a torch stream), else
+        torch's current stream on this device, so the kernels are ordered with the torch
+        work that produced the inputs and that reads the outputs."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(torch.device("cuda", self.device))
+        if hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        return ctypes.c_void_p(int(stream) or None)
+
     def eval_device(self, x, mult, obj_factor: float = 1.0, what: int = L.ALL, out=None, stream=None):
-        """Evaluate with torch device tensors; returns the output dict."""
+        """Evaluate with torch device tensors on ``stream`` (default: torch's current
+        stream); returns the output dict."""
         out = out if out is not None else self.alloc(what)
         ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
-        st = ctypes.c_void_p(stream) if stream else None
+        st = self.stream_handle(stream)
         L.check(L.lib().acopf_batch_eval(
             self._h, ptr(x), float(obj_factor), ptr(mult), int(what), ptr(out["obj"]), ptr(out["grad"]),
             ptr(out["cons"]), ptr(out["jac"]), ptr(out["hess"]), st))

@@ -64,7 +64,7 @@ def device_flows(ev: BatchEvaluator, x_dev, stream=None):
     dev = torch.device("cuda", ev.device)
     flows = torch.zeros(max(nf, 1), dtype=torch.float64, device=dev)
     inj = torch.zeros(max(ni, 1), dtype=torch.float64, device=dev)
-    st = ctypes.c_void_p(stream) if stream else None
+    st = ev.stream_handle(stream)        # torch's current stream unless given: ordered with the zero-fills
     L.check(L.lib().acopf_batch_flows(ev._h, ctypes.c_void_p(x_dev.data_ptr()),
                                       ctypes.c_void_p(flows.data_ptr()), ctypes.c_void_p(inj.data_ptr()), st))
     return flows, inj
