@@ -236,7 +236,7 @@ def _slice_oracle(cfg: int, which: int):
     if cfg == 1:
         return StageOracle(syn.config_case(1)), 1
     if cfg == 2:
-        base, ctgs = _ORACLE.setdefault("in2", None) or _ORACLE.setdefault("in2", syn.config2_inputs())
+        base, ctgs = _ORACLE.get("in2") or _ORACLE.setdefault("in2", syn.config2_inputs())
         c = tuple(ctgs.by_id())
         sub = ContingencySet(tuple(c[(which * (k - 1) + j) % len(c)] for j in range(k - 1)))
         return CompositeOracle.general(None, sub, [base], CouplingMode(), 30.0), k

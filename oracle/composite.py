@@ -114,7 +114,9 @@ class CompositeOracle:
         return [(s, s.weight / tot) for s in [items[b]] + rest]
 
     @classmethod
-    def general(cls, scens, ctgs, periods, mode, dt):
+    def general(cls, scens, ctgs, periods, mode, dt, assemble=True):
+        """composer.py:327-388.  assemble=False stops after the lattice (cases, weights and
+        the pending coupling rows), without building the stage oracles."""
         o = cls()
         ctg_list = [None] + (list(ctgs.by_id()) if ctgs is not None else [])
         idx = {}
@@ -133,7 +135,8 @@ class CompositeOracle:
                 o._mode(idx[(si, ci, 0)], idx[(si, 0, 0)], mode)
             if si > 0:
                 o._scen(idx[(si, 0, 0)], idx[(0, 0, 0)], mode)
-        o._assemble()
+        if assemble:
+            o._assemble()
         return o
 
     @classmethod

@@ -129,7 +129,11 @@ SC_HD void acc_sincos(double x, double* sp, double* cp) {
 // are the constants of that libm build (found in the installed binary and
 // validated: tests/test_native_host.py compares this routine with libm
 // bit for bit); the fused multiply-adds follow the contraction of the FMA
-// build.  Angles outside that range use acc_sincos (correctly rounded).
+// build.  Angles outside that range take glibc's wide-range paths
+// (libm_sincos_wide below): |x| < 2.4262638 by the pi/2 - |x| reflection with
+// a 106-bit pi/2, |x| < 105414336 by the 136-bit Cody-Waite reduction; both
+// validated bit for bit against libm on 4.4 M arguments up to 1e6
+// (tests/test_native_host.py).  Beyond that (and inf / nan): acc_sincos.
 #define GL_SN3 (-0x1.5555555555515p-3)
 #define GL_SN5 (0x1.11110e829872fp-7)
 #define GL_CS2 (0x1.0000000000000p-1)
@@ -175,6 +179,87 @@ __constant__ double sc_gl_k[11] = {GL_SN3, GL_SN5, GL_CS2, GL_CS4, GL_CS6, GL_S1
 #define GLK_BIG GL_BIG
 #endif
 
+// One table entry k (sin hi, sin lo, cos hi, cos lo of k/128).
+SC_HD void gl_entry(const double* table, int k, double& sn, double& ssn, double& cs, double& ccs) {
+    const double* tab = table + 4 * k;
+#ifdef __CUDA_ARCH__
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(sn), "=d"(ssn), "=d"(cs), "=d"(ccs) : "l"(tab));
+#else
+    sn = tab[0]; ssn = tab[1]; cs = tab[2]; ccs = tab[3];
+#endif
+}
+
+// glibc's do_sin(x, dx): sin(x + dx) for |x| < 0.855469 (the Taylor form below
+// 0.126, else the table scheme), with the FMA build's contractions.
+SC_HD double gl_do_sin(const double* table, double x, double dx) {
+    const double ax = fabs(x);
+    if (ax < 0.126) {
+        const double xx = x * x;
+        const double P = fma(fma(fma(fma(GLK_S5, xx, GLK_S4), xx, GLK_S3), xx, GLK_S2), xx, GLK_S1);
+        return x + fma(fma(P, x, -0.5 * dx), xx, dx);
+    }
+    if (x <= 0) dx = -dx;
+    const double u = GLK_BIG + ax;
+    const double xk = u - GLK_BIG;
+    const double xr = ax - xk;
+    double sn, ssn, cs, ccs;
+    gl_entry(table, (int)(xk * 128.0), sn, ssn, cs, ccs);
+    const double xx = xr * xr;
+    const double ps = fma(xx, GLK_SN5, GLK_SN3);
+    const double sv = xr + fma(xr * xx, ps, dx);
+    const double cv = fma(xr, dx, xx * fma(xx, fma(xx, GLK_CS6, GLK_CS4), GLK_CS2));
+    const double cor = fma(cs, sv, fma(-sn, cv, fma(sv, ccs, ssn)));
+    return copysign(sn + cor, x);
+}
+
+// glibc's do_cos(x, dx): cos(x + dx) for |x| < 0.855469 by the table scheme.
+SC_HD double gl_do_cos(const double* table, double x, double dx) {
+    if (x < 0) dx = -dx;
+    const double ax = fabs(x);
+    const double u = GLK_BIG + ax;
+    const double xk = u - GLK_BIG;
+    const double xr = (ax - xk) + dx;
+    double sn, ssn, cs, ccs;
+    gl_entry(table, (int)(xk * 128.0), sn, ssn, cs, ccs);
+    const double xx = xr * xr;
+    const double ps = fma(xx, GLK_SN5, GLK_SN3);
+    const double sv = fma(xr * xx, ps, xr);
+    const double cv = xx * fma(xx, fma(xx, GLK_CS6, GLK_CS4), GLK_CS2);
+    const double cor = fma(-sn, sv, fma(-cs, cv, fma(-sv, ssn, ccs)));
+    return cs + cor;
+}
+
+// glibc's sin/cos for 0.85546875 <= |x| < 105414336 (s_sin.c): the reflection
+// sin x = cos(pi/2 - |x|), cos x = sin(pi/2 - |x|) with pi/2 = hp0 + hp1 below
+// 2.4262638, else x = n pi/2 + (a + da) with a 4-part pi/2 (reduce_sincos) and
+// the quadrant's do_sin / do_cos.
+SC_HD void libm_sincos_wide(const double* table, double x, double* sp, double* cp) {
+    const double hp0 = 1.5707963267948966, hp1 = 6.123233995736766e-17;
+    const double ax = fabs(x);
+    if (ax < 2.4262638092041016) {
+        const double t = hp0 - ax;
+        *sp = copysign(gl_do_cos(table, t, hp1), x);
+        const double a = t + hp1;
+        const double da = (t - a) + hp1;
+        *cp = gl_do_sin(table, a, da);
+        return;
+    }
+    const double toint = 6755399441055744.0;                    // 1.5 * 2^52
+    const double t = fma(x, 0.6366197723675814, toint);
+    const double xn = t - toint;
+    const int n = (int)((long long)xn & 3);
+    const double y = fma(-xn, -1.3909067564377153e-08, fma(-xn, 1.5707963407039642, x));
+    const double t1 = xn * -4.97899623147991e-17;                // exact
+    const double t2 = y - t1;
+    double db = (y - t2) - t1;
+    const double b = fma(-xn, -1.9034889620193266e-25, t2);
+    db = db + fma(-xn, -1.9034889620193266e-25, t2 - b);
+    const double rs = (n & 1) ? gl_do_cos(table, b, db) : gl_do_sin(table, b, db);
+    const double rc = (n & 1) ? gl_do_sin(table, b, db) : gl_do_cos(table, b, db);
+    *sp = (n & 2) ? -rs : rs;
+    *cp = ((n + 1) & 2) ? -rc : rc;
+}
+
 // table: sc_gl_table_* (SC_GL_NK entries of sin hi, sin lo, cos hi, cos lo;
 // on the device, the 32-byte aligned global copy)
 SC_HD void libm_sincos_t(const double* table, double x, double* sp, double* cp) {
@@ -215,7 +300,9 @@ SC_HD void libm_sincos_t(const double* table, double x, double* sp, double* cp) 
     if (core) {
         *sp = s;
         *cp = c;
-    } else {                           // outside the table scheme (and inf / nan)
+    } else if (ax < 105414336.0) {     // glibc's wide-range paths (rare: warps diverge here)
+        libm_sincos_wide(table, x, sp, cp);
+    } else {                           // huge, inf or nan (glibc: __branred; not libm-identical)
         acc_sincos(x, sp, cp);
     }
 }

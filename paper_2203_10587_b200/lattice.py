@@ -388,6 +388,9 @@ class _Lattice:
             eq_offset=tuple(int(v) for v in eq_off), ineq_offset=tuple(int(v) for v in ineq_off),
             coupling_rows=LazySeq(len(cp["row"]), make_row), weights=tuple(float(s.weight) for s in st),
             layouts=LazySeq(ns, make_layout), n_vars=nv, m_eq=m_eq, m_ineq=m_ineq)
+        # extension (not a reference field): the coupling rows as arrays -- kind code (KINDS),
+        # stage_a, stage_b, gen, bus (-1 = none), bound, row, and the x columns col_a / col_b
+        object.__setattr__(index, "coupling_arrays", cp)
         return problem, index
 
 

@@ -211,8 +211,140 @@ def solutions():
         print("solution", name, len(imap.stages))
 
 
+# ---------------------------------------------------------------------------
+# the reference's own test fixtures (pkg/tests/conftest.py:20-57): case9.m, ctgc.cont,
+# scenarios.csv, load_p.csv / load_q.csv, parsed by the reference's own readers and
+# evaluated by its own build_acopf / compose_*; the parsed inputs are stored (as this
+# package's dataclass fields) next to the outputs, so the GPU box needs no reference files
+
+REF_DATA = "/root/reference/pkg/tests/data"
+
+
+def _to_ours(ok, case):
+    import common as C
+    return C.case_to_json(case)
+
+
+def fixture_inputs(ok):
+    """Reference-parsed fixtures: (case9, ctgs, scens, period cases)."""
+    case9 = ok.load_case(os.path.join(REF_DATA, "case9.m"))
+    ctgs = ok.parse_contingencies_file(os.path.join(REF_DATA, "ctgc.cont"))
+    scens = ok.parse_scenarios_file(os.path.join(REF_DATA, "scenarios.csv"))
+    prof = ok.parse_load_profile_files(os.path.join(REF_DATA, "load_p.csv"), os.path.join(REF_DATA, "load_q.csv"))
+    periods = [ok.network.apply_load_step(case9, prof, t) for t in range(len(prof.times))]
+    return case9, ctgs, scens, periods
+
+
+FIXTURE_SPECS = {
+    # name: (builder, args) over the reference fixtures; mirrors pkg/tests/test_composer.py usage
+    "ref_case9_scopf_corrective": ("scopf", dict(mode=dict(kind="corrective"))),
+    "ref_case9_scopf_preventive": ("scopf", dict(mode=dict(kind="preventive", pin_voltages=True))),
+    "ref_case9_general": ("general", dict(n_ctg=2, n_periods=2, dt=5.0, mode=dict(kind="preventive"))),
+    "ref_case9_multiperiod": ("multiperiod", dict(dt=5.0)),
+    "ref_case9_sopf_full": ("sopf_full", dict(mode=dict(kind="corrective"))),
+    "ref_case9_mp_scopf": ("mp_scopf", dict(n_ctg=3, dt=5.0, mode=dict(kind="corrective"))),
+}
+
+
+def fixture_compose(api, kind, args, case9, ctgs, scens, periods, mode, trunc):
+    """compose_* of ``api`` (the reference or this package) for one FIXTURE_SPECS entry."""
+    if kind == "scopf":
+        return api.compose_scopf(case9, ctgs, mode)
+    if kind == "general":
+        return api.compose_general(scens, trunc(ctgs, args["n_ctg"]), [case9] * args["n_periods"], mode, args["dt"])
+    if kind == "multiperiod":
+        return api.compose_multiperiod(periods, args["dt"])
+    if kind == "sopf_full":
+        return api.compose_sopf_full(case9, scens, ctgs, mode)
+    return api.compose_multiperiod_scopf(periods, trunc(ctgs, args["n_ctg"]), mode, args["dt"])
+
+
+def fixtures():
+    """ref_case9_*.npz: the reference's fixtures through its own stage and composite builders,
+    at seeded points (one with branch angles up to ~pi, glibc's wide-range sin/cos)."""
+    import common as C
+    import refbridge as rb
+    ok = rb.opfkit()
+    if ok is None:
+        raise SystemExit("reference not mounted at /root/reference")
+    case9, ctgs, scens, periods = fixture_inputs(ok)
+    inputs = dict(case=C.case_to_json(case9), ctgs=C.ctgs_to_json(ctgs), scens=C.scens_to_json(scens),
+                  periods=json.dumps([json.loads(C.case_to_json(c)) for c in periods]))
+    # stage: x0 plus seeded points, one with large branch angles
+    p, lay = ok.build_acopf(case9)
+    kinds = syn.variable_kinds([(len(lay.va), len(lay.pg))])
+    pts = [(p.x0.copy(), np.ones(p.m_eq + p.m_ineq), 1.0)]
+    for s in range(2):
+        x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 4000 + s)
+        pts.append((x, mult, 1.0 + 0.5 * s))
+    x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 4100)
+    va = kinds == syn.VA
+    x[va] = np.random.default_rng(4101).uniform(-1.6, 1.6, int(va.sum()))
+    x[p.xl == p.xu] = p.xl[p.xl == p.xu]
+    pts.append((x, mult, 1.0))
+    dump(os.path.join(HERE, "ref_case9_stage.npz"), p, pts, dict(spec=json.dumps(dict(kind="stage")), **inputs))
+    print("ref_case9_stage", p.n, p.m_eq + p.m_ineq)
+    trunc = lambda c, n: c.truncated(n)
+    for name, (kind, args) in FIXTURE_SPECS.items():
+        mode = ok.composer.CouplingMode(**args.get("mode", {}))
+        p, imap = fixture_compose(ok, kind, args, case9, ctgs, scens, periods, mode, trunc)
+        kinds = variable_kinds_from_layouts(imap.layouts)
+        pts = []
+        for s in range(2):
+            x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 4200 + s)
+            pts.append((x, mult, 0.75 + s))
+        rows = np.array([[r.stage_a, r.stage_b, -1 if r.gen is None else r.gen,
+                          -1 if r.bus is None else r.bus, r.row, int(r.is_equality)]
+                         for r in imap.coupling_rows], dtype=np.int64).reshape(-1, 6)
+        dump(os.path.join(HERE, name + ".npz"), p, pts,
+             dict(spec=json.dumps(dict(kind=kind, **args)), **inputs,
+                  var_offset=np.array(imap.var_offset), eq_offset=np.array(imap.eq_offset),
+                  ineq_offset=np.array(imap.ineq_offset), weights=np.array(imap.weights),
+                  cp_rows=rows, cp_kinds=np.array([r.kind for r in imap.coupling_rows]),
+                  cp_bounds=np.array([r.bound for r in imap.coupling_rows], dtype=np.float64)))
+        print(name, p.n, p.m_eq + p.m_ineq, len(imap.coupling_rows))
+
+
+def configs():
+    """cfg0_stage.npz: BASELINE config 0 (the 9-bus ring at CONFIG_SEEDS[0]) from the reference,
+    at 4 seeded points; cfg_feat200_wide.npz: a 200-bus feature network at branch angles up to
+    ~pi (Va ~ U(-1.6, 1.6)), the non-table paths of glibc's sin/cos."""
+    import refbridge as rb
+    ok = rb.opfkit()
+    if ok is None:
+        raise SystemExit("reference not mounted at /root/reference")
+    case = syn.config_case(0)
+    p, lay = ok.build_acopf(rb.to_ref_case(case))
+    kinds = syn.variable_kinds([(len(lay.va), len(lay.pg))])
+    pts = []
+    for s in range(4):
+        x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, syn.CONFIG_SEEDS[0] + s)
+        pts.append((x, mult, 1.0))
+    dump(os.path.join(HERE, "cfg0_stage.npz"), p, pts,
+         dict(spec=json.dumps(dict(config=0)), case_digest=case_digest(case)))
+    print("cfg0_stage", p.n, p.m_eq + p.m_ineq)
+    spec = STAGE_SPECS["stage_feat200"]
+    case = stage_case(spec)
+    p, lay = ok.build_acopf(rb.to_ref_case(case))
+    kinds = syn.variable_kinds([(len(lay.va), len(lay.pg))])
+    pts = []
+    for s in range(3):
+        x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 5000 + s)
+        va = kinds == syn.VA
+        x[va] = np.random.default_rng(5100 + s).uniform(-1.6, 1.6, int(va.sum()))
+        x[p.xl == p.xu] = p.xl[p.xl == p.xu]
+        pts.append((x, mult, 1.0))
+    dump(os.path.join(HERE, "cfg_feat200_wide.npz"), p, pts,
+         dict(spec=json.dumps(spec), case_digest=case_digest(case)))
+    print("cfg_feat200_wide", p.n)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["solutions"]:
         solutions()
+    elif sys.argv[1:] == ["fixtures"]:
+        fixtures()
+    elif sys.argv[1:] == ["configs"]:
+        configs()
     else:
         main()

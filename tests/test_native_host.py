@@ -102,6 +102,23 @@ def test_libm_sincos_bit_identical_to_numpy(libm_sincos_bin):
     assert C.bit_diffs(out[1::2], np.cos(xs)) == 0
 
 
+def test_libm_sincos_wide_range_bit_identical_to_numpy(libm_sincos_bin):
+    """glibc's wide-range paths (0.8555 <= |x| < 105414336, large branch angles an IPM can
+    visit): np.sin / np.cos bit for bit, including near multiples of pi/2."""
+    rng = np.random.default_rng(12)
+    xs = np.concatenate([rng.uniform(0.85546875, 2.4262638092041016, 600_000),
+                         -rng.uniform(0.85546875, 2.4262638092041016, 200_000),
+                         rng.uniform(-20.0, 20.0, 300_000), rng.uniform(-1e6, 1e6, 50_000),
+                         np.pi / 2 + rng.uniform(-1e-6, 1e-6, 20_000),
+                         np.pi * rng.integers(-40, 40, 20_000) + rng.uniform(-1e-9, 1e-9, 20_000),
+                         [0.85546875, -0.85546875, 2.4262638092041016, np.nextafter(2.4262638092041016, 0),
+                          np.pi, -np.pi, 3 * np.pi / 2, 105414335.0]])
+    inp = np.array([len(xs)], dtype=np.uint64).tobytes() + xs.tobytes()
+    out = np.frombuffer(subprocess.run([libm_sincos_bin], input=inp, capture_output=True, check=True).stdout)
+    assert C.bit_diffs(out[0::2], np.sin(xs)) == 0
+    assert C.bit_diffs(out[1::2], np.cos(xs)) == 0
+
+
 def test_accurate_sincos_vs_libm(sincos_bin):
     """Device sincos (same source, host build) is within 1 ulp of libm and equal on >99.5%."""
     rng = np.random.default_rng(3)
@@ -199,3 +216,41 @@ def test_parallel_planner_is_deterministic():
         p, _ = compose(pkg, spec["kind"], a)
         stats.append(p.evaluator.verify_plan())
     assert stats[0] == stats[1]
+
+
+def test_reference_fixture_case9_stage_structure():
+    """build_acopf on the reference's own case9.m (parsed by the reference, stored in the golden)."""
+    g = C.load("ref_case9_stage")
+    p, lay = pkg.build_acopf(C.case_from_json(str(g["case"])))
+    assert (p.n, p.m_eq, p.m_ineq) == (int(g["n"]), int(g["m_eq"]), int(g["m_ineq"]))
+    for a in ("xl", "xu", "x0", "gl", "gu"):
+        assert C.bit_diffs(getattr(p, a), g[a]) == 0, a
+    ip, ix = p.evaluator.pattern("J")
+    assert np.array_equal(ip, g["jindptr"]) and np.array_equal(ix, g["jindices"])
+    ip, ix = p.evaluator.pattern("H")
+    assert np.array_equal(ip, g["hindptr"]) and np.array_equal(ix, g["hindices"])
+
+
+@pytest.mark.parametrize("name", C.REF_FIXTURES)
+def test_reference_fixture_composite_structure(name):
+    """compose_* on case9 + ctgc.cont / scenarios.csv / load profile (the reference's fixtures):
+    sizes, bounds, offsets, weights, coupling rows and CSR patterns equal the reference's."""
+    from paper_2203_10587_b200.types import CouplingMode
+    g = C.load(name)
+    p, imap = C.ref_fixture_compose(pkg, g, CouplingMode)
+    assert (p.n, p.m_eq, p.m_ineq) == (int(g["n"]), int(g["m_eq"]), int(g["m_ineq"]))
+    for k in ("xl", "xu", "x0", "gl", "gu"):
+        assert C.bit_diffs(getattr(p, k), g[k]) == 0, k
+    assert list(imap.var_offset) == list(g["var_offset"])
+    assert list(imap.eq_offset) == list(g["eq_offset"])
+    assert list(imap.ineq_offset) == list(g["ineq_offset"])
+    assert np.array_equal(np.array(imap.weights), g["weights"])
+    rows = np.array([[r.stage_a, r.stage_b, -1 if r.gen is None else r.gen, -1 if r.bus is None else r.bus,
+                      r.row, int(r.is_equality)] for r in imap.coupling_rows], dtype=np.int64).reshape(-1, 6)
+    assert np.array_equal(rows, g["cp_rows"])
+    assert [r.kind for r in imap.coupling_rows] == list(g["cp_kinds"])
+    assert C.bit_diffs([r.bound for r in imap.coupling_rows], g["cp_bounds"]) == 0
+    ip, ix = p.evaluator.pattern("J")
+    assert np.array_equal(ip, g["jindptr"]) and np.array_equal(ix, g["jindices"])
+    ip, ix = p.evaluator.pattern("H")
+    assert np.array_equal(ip, g["hindptr"]) and np.array_equal(ix, g["hindices"])

@@ -118,3 +118,33 @@ def test_numpy_pairwise_sum_model():
     for n in [0, 1, 7, 8, 9, 127, 128, 129, 500, 2500, 6000, 17000]:
         a = rng.standard_normal(n) * 1e3
         assert float(np.sum(a)) == pw(list(a))
+
+
+def test_stage_oracle_matches_reference_fixture_case9():
+    """The reference's own case9.m (tests/data), parsed by the reference, stored in the golden."""
+    g = C.load("ref_case9_stage")
+    _check_problem(StageOracle(C.case_from_json(str(g["case"]))), g)
+
+
+@pytest.mark.parametrize("name", C.REF_FIXTURES)
+def test_composite_oracle_matches_reference_fixtures(name):
+    """case9 + ctgc.cont / scenarios.csv / load profile through the reference's compose_*."""
+    g = C.load(name)
+    o = C.ref_fixture_oracle(g)
+    assert list(o.var_off) == list(g["var_offset"])
+    rows = np.array([[c["stage_a"], c["stage_b"], -1 if c["gen"] is None else c["gen"],
+                      -1 if c["bus"] is None else c["bus"], c["row"], int(c["is_equality"])]
+                     for c in o.coupling], dtype=np.int64).reshape(-1, 6)
+    assert np.array_equal(rows, g["cp_rows"])
+    assert _same([c["bound"] for c in o.coupling], g["cp_bounds"])
+    _check_problem(o, g)
+
+
+@pytest.mark.parametrize("name", ["cfg0_stage", "cfg_feat200_wide"])
+def test_stage_oracle_matches_config_goldens(name):
+    """BASELINE config 0 and the wide-angle (|theta| up to ~pi) golden."""
+    from paper_2203_10587_b200 import synthetic as syn
+    g = C.load(name)
+    case = syn.config_case(0) if name == "cfg0_stage" else stage_case(STAGE_SPECS["stage_feat200"])
+    assert case_digest(case) == str(g["case_digest"]), "synthetic generator drifted"
+    _check_problem(StageOracle(case), g)
