@@ -20,6 +20,7 @@
  *                          solution_from_case                        (acopf.py:448-546, 230-264)
  *   acopf_batch_pattern    CSR indptr/indices of J or H (stage or composite) -- the fixed
  *                          pattern scipy would produce (acopf.py:308-311, 370-373)
+ *   acopf_format_matrix    MATPOWER text of a solved stage's matrices   (matpower.py:151-190)
  *   acopf_last_error       error text (Python raises DeviceError / Disconnected ...)
  *
  * Conventions: plain pointers and sizes, no exceptions across the ABI.  Every
@@ -140,6 +141,15 @@ int acopf_batch_pattern(const acopf_batch* b, int32_t stage, int32_t which, int6
  * the t-th term; equal columns are adjacent and summed left to right.  Used by
  * the tests to pin the replay against scipy itself. */
 int acopf_canonical_order(int64_t n, const int32_t* cols, int32_t* perm);
+
+/* MATPOWER text of one matrix section of a solved stage (the reference's
+ * matpower._fmt_matrix, matpower.py:151-157): "mpc.<section> = [", one line
+ * per row ("\t" + the row's values as "%.10g" joined by "\t" + ";"), "];",
+ * lines joined by "\n".  Row r holds values[row_ptr[r] .. row_ptr[r+1]).
+ * Writes at most cap bytes to out (no terminating NUL); *len receives the
+ * text's length (out may be NULL to size it).  Host only, thread-safe. */
+int acopf_format_matrix(const char* section, int64_t rows, const int64_t* row_ptr, const double* values,
+                        char* out, int64_t cap, int64_t* len);
 
 /* Kernel launches issued by this handle since creation (evidence counter). */
 int64_t acopf_batch_launches(const acopf_batch* b);

@@ -50,6 +50,7 @@ _SIGNATURES = {
     "acopf_batch_launches": (c_int64, [c_void_p]),
     "acopf_canonical_order": (c_int32, [c_int64, _i32p, _i32p]),
     "acopf_batch_verify": (c_int32, [c_void_p, _i64p]),
+    "acopf_format_matrix": (c_int32, [c_char_p, c_int64, _i64p, _f64p, c_void_p, c_int64, _i64p]),
 }
 
 

@@ -18,6 +18,7 @@
 #include "../../include/acopf_b200.h"
 #include "eval_kernel.cuh"
 #include "planner.hpp"
+#include "writer.hpp"
 
 using namespace acopf;
 
@@ -1012,6 +1013,21 @@ int acopf_batch_verify(const acopf_batch* b, int64_t* stats) {
             stats[3] = area; stats[4] = pads; stats[5] = smem;
             stats[6] = rounds; stats[7] = lane_terms; stats[8] = chain;
             stats[9] = cost[0]; stats[10] = cost[1]; stats[11] = cost[2];
+        }
+    });
+}
+
+int acopf_format_matrix(const char* section, int64_t rows, const int64_t* row_ptr, const double* values,
+                        char* out, int64_t cap, int64_t* len) {
+    return guard([&] {
+        if (!section || rows < 0 || (rows > 0 && (!row_ptr || !values))) throw std::runtime_error("bad arguments");
+        std::string s;
+        s.reserve((size_t)std::max<int64_t>(64, rows > 0 ? 12 * (row_ptr[rows] - row_ptr[0]) + 4 * rows : 64));
+        fmt_matrix(section, rows, row_ptr, values, s);
+        if (len) *len = (int64_t)s.size();
+        if (out) {
+            if ((int64_t)s.size() > cap) throw std::runtime_error("output buffer too small");
+            std::memcpy(out, s.data(), s.size());
         }
     });
 }

@@ -47,8 +47,9 @@ class SolvedCase:
     objective: float
 
     def to_raw(self, name=None):
-        """MATPOWER export (acopf.py:433-446) is outside this package."""
-        raise NotImplementedError("MATPOWER export is not part of the B200 callback path")
+        """RawCase with solved voltages, dispatch and flow columns (acopf.py:433-446)."""
+        from .matpower import solved_to_raw
+        return solved_to_raw(self, name=name)
 
 
 def device_flows(ev: BatchEvaluator, x_dev, stream=None):

@@ -339,6 +339,35 @@ def configs():
     print("cfg_feat200_wide", p.n)
 
 
+def writer():
+    """matpower_text.npz: the reference's write_case text (matpower.py:180-187) of solved cases --
+    extract_solution outputs of the stage goldens' cases and of case9 (reference-parsed, with
+    its ramp / tail columns) at seeded points."""
+    import common as C
+    import refbridge as rb
+    ok = rb.opfkit()
+    if ok is None:
+        raise SystemExit("reference not mounted at /root/reference")
+    out = {}
+    case9, _, _, _ = fixture_inputs(ok)
+    cases = [("case9", case9, C.case_to_json(case9))]
+    for name in ("stage_ring9", "stage_feat30", "stage_feat200"):
+        c = stage_case(STAGE_SPECS[name])
+        cases.append((name, rb.to_ref_case(c), C.case_to_json(c)))
+    for i, (name, rc, js) in enumerate(cases):
+        p, lay = ok.build_acopf(rc)
+        kinds = syn.variable_kinds([(len(lay.va), len(lay.pg))])
+        x, _ = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 6000 + i)
+        sol = ok.extract_solution(rc, lay, x)
+        out[f"case{i}"] = js
+        out[f"x{i}"] = x
+        out[f"text{i}"] = ok.matpower.write_case(sol, name=f"t_{i}")
+        out[f"text_default{i}"] = ok.matpower.write_case(sol)
+    out["n"] = len(cases)
+    np.savez_compressed(os.path.join(HERE, "matpower_text.npz"), **out)
+    print("matpower_text", len(cases))
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["solutions"]:
         solutions()
@@ -346,5 +375,7 @@ if __name__ == "__main__":
         fixtures()
     elif sys.argv[1:] == ["configs"]:
         configs()
+    elif sys.argv[1:] == ["writer"]:
+        writer()
     else:
         main()

@@ -59,6 +59,8 @@ class Tally:
 
     def finish(self, name, **extra):
         C.record(name, gate_misses=self.misses, bit_diffs=self.bits, values=self.values, **extra)
+        if self.bits:
+            print(name, extra)
         assert self.misses == 0, f"{name}: {self.misses} values outside the gate"
         assert self.bits == 0, f"{name}: {self.bits} values differ in some bit"
 
@@ -260,10 +262,15 @@ def _cfg4_stage(k):
              (np.concatenate([out["jac"][jb:jb + njeq], out["jac"][jn:jn + njin]]), J.data),
              (out["hess"][hb:hb + nh], H.data)]
     t = Tally()
-    for u, v in pairs:
+    where = []
+    for name, (u, v) in zip(("grad", "cons", "jac", "hess"), pairs):
+        b0 = t.bits
         t.add(u, v)
+        if t.bits > b0:
+            d = np.flatnonzero(np.asarray(u).view(np.int64) != np.asarray(v).view(np.int64))[:4]
+            where.append((k, name, [(int(i), float(u[i]), float(v[i])) for i in d]))
     pg = so.layout_maps()["pg"]
-    return k, so.objective(xk), t.misses, t.bits, t.values, pat, pg
+    return k, so.objective(xk), t.misses, t.bits, t.values, pat, pg, where
 
 
 @pytest.mark.slow
@@ -286,17 +293,25 @@ def test_config4_full_all_stages():
     t = Tally()
     fs = [None] * S
     pgs = [None] * S
+    where = []
     with mp.get_context("fork").Pool(workers) as pool:
-        for k, f, mi, bi, vi, pat, pg in pool.imap_unordered(_cfg4_stage, range(S), chunksize=4):
+        for k, f, mi, bi, vi, pat, pg, wh in pool.imap_unordered(_cfg4_stage, range(S), chunksize=4):
             assert pat, f"stage {k}: CSR pattern differs"
             fs[k], pgs[k] = f, pg
+            where += wh
             t.misses += mi
             t.bits += bi
             t.values += vi
     _W.clear()
-    # composite objective: sum(w_k f_k) left to right (composer.py:256-258)
-    ref_obj = float(sum(lat.weights[k] * fs[k] for k in range(S)))
+    # composite objective: sum(w[k] f_k) with w = np.asarray(weights) (composer.py:244,256-258):
+    # np.float64 items, so CPython's sum adds them left to right (its compensated float
+    # path, 3.12+, only applies to exact Python floats)
+    w = np.asarray(lat.weights)
+    ref_obj = float(sum(w[k] * fs[k] for k in range(S)))
+    b0 = t.bits
     t.add(out["obj"][:1], [ref_obj])
+    if t.bits > b0:
+        where.append(("objective", float(out["obj"][0]), ref_obj))
     # coupling rows: the oracle lattice's pending rows, in order (pins first, then boxes)
     cp = imap.coupling_arrays
     pend = [r for r in lat.pending if r[6]] + [r for r in lat.pending if not r[6]]
@@ -327,4 +342,17 @@ def test_config4_full_all_stages():
     first = np.where(cb < ca, -1.0, 1.0)
     t.add(out["jac"][pos], first)
     t.add(out["jac"][pos + 1], -first)
-    t.finish("oracle:cfg4-full", stages=S, coupling_rows=int(len(rows)))
+    t.finish("oracle:cfg4-full", stages=S, coupling_rows=int(len(rows)), differing=repr(where[:20]))
+
+
+def test_matpower_text_from_gpu_solutions():
+    """extract_solution on the GPU, then write_case (acopf_format_matrix): the reference's text."""
+    from paper_2203_10587_b200 import matpower as M
+    from paper_2203_10587_b200.solution import extract_solution
+    g = C.load("matpower_text")
+    for i in range(int(g["n"])):
+        case = C.case_from_json(str(g[f"case{i}"]))
+        _, lay = pkg.build_acopf(case)
+        sol = extract_solution(case, lay, g[f"x{i}"])
+        assert M.write_case(sol, name=f"t_{i}") == str(g[f"text{i}"])
+        assert M.write_case(sol) == str(g[f"text_default{i}"])
