@@ -86,7 +86,7 @@ def test_shape_errors_before_any_device_work():
                        qg=np.zeros(len(case.gens)), pf=None, qf=None, pt=None, qt=None, objective=0.0)
     with pytest.raises(pkg.DimensionMismatch):
         S.residuals_at(case, bad)
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(IndexError):           # the reference's to_raw indexes vm per bus too
         bad.to_raw()
 
 
