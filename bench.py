@@ -445,31 +445,55 @@ def main():
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(f"cfg{args.config}")
 
-    # end to end through the C ABI with pinned host buffers (H2D + eval + D2H per step)
+    # end to end with pinned host buffers (H2D of the step's inputs + evaluation + D2H of every
+    # output, per step): one GPU through acopf_batch_eval_host (the C ABI's host-buffer entry
+    # point); sharded, each rank copies its shard's x / multipliers in, runs
+    # acopf_batch_eval_multi and copies its outputs and the objective out
     e2e = None
-    if not args.no_e2e and sc is None:
+    if not args.no_e2e:
+        sizes = dict(obj=ev.n_obj, grad=ev.n, cons=ev.m, jac=ev.nnz_j, hess=ev.nnz_h)
         xp = torch.from_numpy(x_h).pin_memory()
         mp_ = torch.from_numpy(m_h).pin_memory()
-        sizes = dict(obj=ev.n_obj, grad=ev.n, cons=ev.m, jac=ev.nnz_j, hess=ev.nnz_h)
-        del out                         # the device outputs are not needed any more (HBM for the host path)
+        if sc is None:
+            del out                     # the device outputs are not needed any more (HBM for the host path)
         hout = {k: torch.empty(max(n, 1), dtype=torch.float64).pin_memory()[:n] for k, n in sizes.items()}
+
+        def e2e_step():
+            if sc is None:
+                ev.eval_host_ptrs(xp.data_ptr(), mp_.data_ptr(), 1.0, L.ALL, hout, stream=sptr)
+                return
+            x.copy_(xp, non_blocking=True)
+            mult.copy_(mp_, non_blocking=True)
+            _, obj = sc.evaluate(x, mult, 1.0, L.ALL, out=out, stream=sptr)
+            for k in ("grad", "cons", "jac", "hess"):
+                hout[k].copy_(out[k][:sizes[k]], non_blocking=True)
+            hout["obj"][:1].copy_(obj, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+
         for _ in range(2):
-            ev.eval_host_ptrs(xp.data_ptr(), mp_.data_ptr(), 1.0, L.ALL, hout, stream=sptr)
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
         e_steps = max(3, min(args.steps, 10))
         es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         es.record(stream)
         for k in range(e_steps):
-            ev.eval_host_ptrs(xp.data_ptr(), mp_.data_ptr(), 1.0, L.ALL, hout, stream=sptr)
+            e2e_step()
         ee.record(stream)
         torch.cuda.synchronize(dev)
         e_ms = torch.tensor([es.elapsed_time(ee)], dtype=torch.float64, device=dev)
+        bytes_io = torch.tensor([8.0 * (ev.n + ev.m), 8.0 * sum(sizes.values())], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": units * world * e_steps / (float(e_ms.item()) / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": 8 * (ev.n + ev.m),
-               "d2h_bytes_per_step": 8 * sum(sizes.values()),
-               "path": "acopf_batch_eval_host (C ABI) on pinned host buffers, "
-                       f"{e_steps} steps back to back"}
+            dist.all_reduce(bytes_io)
+        e2e = {"value": (units * world if sc is None else units) * e_steps / (float(e_ms.item()) / 1000.0),
+               "unit": UNIT,
+               "h2d_bytes_per_step": int(bytes_io[0].item()),
+               "d2h_bytes_per_step": int(bytes_io[1].item()),
+               "path": ("acopf_batch_eval_host (C ABI) on pinned host buffers" if sc is None else
+                        "per rank: pinned H2D of its shard, acopf_batch_eval_multi, pinned D2H of its outputs")
+                       + f", {e_steps} steps back to back"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

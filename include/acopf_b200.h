@@ -20,6 +20,8 @@
  *                          solution_from_case                        (acopf.py:448-546, 230-264)
  *   acopf_batch_pattern    CSR indptr/indices of J or H (stage or composite) -- the fixed
  *                          pattern scipy would produce (acopf.py:308-311, 370-373)
+ *   acopf_multi_create / acopf_batch_eval_multi   the sharded evaluation over GPUs with the
+ *                          NCCL communicator inside (EMPAR pool analogue, runner.py:305-312)
  *   acopf_format_matrix    MATPOWER text of a solved stage's matrices   (matpower.py:151-190)
  *   acopf_last_error       error text (Python raises DeviceError / Disconnected ...)
  *
@@ -141,6 +143,43 @@ int acopf_batch_pattern(const acopf_batch* b, int32_t stage, int32_t which, int6
  * the t-th term; equal columns are adjacent and summed left to right.  Used by
  * the tests to pin the replay against scipy itself. */
 int acopf_canonical_order(int64_t n, const int32_t* cols, int32_t* perm);
+
+/* ---- multi-GPU: one process per GPU, a composite sharded into contiguous stage
+ * blocks (the reference's EMPAR pool analogue, runner.py:305-312).
+ * Each rank makes a batch of its own stages with a composite layout whose
+ * coupling rows may read base-stage values owned by other ranks from a halo at
+ * x[halo_dst0 ...], and objective mode ACOPF_OBJ_TERMS. */
+typedef struct acopf_multi acopf_multi;
+
+/* ncclGetUniqueId: rank 0 makes the 128-byte id, the caller broadcasts it. */
+int acopf_nccl_unique_id(void* id128);
+
+/* The exchange plan and (with nccl_id) the NCCL communicator, made inside with
+ * ncclCommInitRank (collective: every rank calls it).  x_lo/x_hi: every rank's
+ * global x range; need_ptr (world+1) / need_idx: every rank's sorted global x
+ * indices it reads from other ranks (the halo, in this rank's halo order);
+ * halo_dst0: local x index of this rank's first halo value; obj_counts: stages
+ * (objective terms) per rank.  nccl_id NULL makes a plan-only handle (host,
+ * acopf_multi_plan).  The batch must stay alive while the handle is used. */
+int acopf_multi_create(acopf_batch* b, int32_t rank, int32_t world, const int64_t* x_lo, const int64_t* x_hi,
+                       const int64_t* need_ptr, const int64_t* need_idx, int64_t halo_dst0,
+                       const int32_t* obj_counts, const void* nccl_id, acopf_multi** out);
+
+/* Host view of the plan: sizes3 = (exports, export slots per rank, halo values);
+ * export_idx = local x indices this rank sends; halo_src = position of each halo
+ * value in the gathered [world][export slots] buffer (either may be NULL). */
+int acopf_multi_plan(const acopf_multi* m, int64_t* sizes3, int64_t* export_idx, int64_t* halo_src);
+int acopf_multi_destroy(acopf_multi* m);
+
+/* One sharded evaluation on this rank (device pointers, stream-ordered on
+ * `stream`, NULL = legacy default stream): the halo chain (pack kernel ->
+ * ncclAllGather -> unpack kernel -> coupling rows) runs on a forked stream and
+ * overlaps the tile kernel; every rank's w_s f_s terms are all-gathered and
+ * summed in global stage order on the device into obj[0] (bit-identical to one
+ * GPU).  x must hold the halo slots (it is written there); outputs are this
+ * rank's local blocks in its layout. */
+int acopf_batch_eval_multi(acopf_multi* m, double* x, double obj_factor, const double* mult, uint32_t what,
+                           double* obj, double* grad, double* cons, double* jval, double* hval, void* stream);
 
 /* MATPOWER text of one matrix section of a solved stage (the reference's
  * matpower._fmt_matrix, matpower.py:151-157): "mpc.<section> = [", one line

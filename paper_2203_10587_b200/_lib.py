@@ -50,6 +50,13 @@ _SIGNATURES = {
     "acopf_batch_launches": (c_int64, [c_void_p]),
     "acopf_canonical_order": (c_int32, [c_int64, _i32p, _i32p]),
     "acopf_batch_verify": (c_int32, [c_void_p, _i64p]),
+    "acopf_nccl_unique_id": (c_int32, [c_void_p]),
+    "acopf_multi_create": (c_int32, [c_void_p, c_int32, c_int32, _i64p, _i64p, _i64p, _i64p, c_int64, _i32p,
+                                     c_void_p, POINTER(c_void_p)]),
+    "acopf_multi_plan": (c_int32, [c_void_p, _i64p, _i64p, _i64p]),
+    "acopf_multi_destroy": (c_int32, [c_void_p]),
+    "acopf_batch_eval_multi": (c_int32, [c_void_p, c_void_p, c_double, c_void_p, c_uint32, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_void_p, c_void_p]),
     "acopf_format_matrix": (c_int32, [c_char_p, c_int64, _i64p, _f64p, c_void_p, c_int64, _i64p]),
 }
 

@@ -20,7 +20,21 @@ DEPS = ["abi.cu", "eval_kernel.cuh", "planner.hpp", "sincos.cuh", "writer.hpp", 
         os.path.join("..", "..", "include", "acopf_b200.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-shared"]
+              "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-shared", "-ldl"]
+
+
+def nccl_include() -> list:
+    """-I for nccl.h (declarations only: NCCL is dlopen'ed at run time): torch's bundled
+    NCCL headers, else the system's."""
+    try:
+        import nvidia.nccl
+        for p in nvidia.nccl.__path__:
+            inc = os.path.join(p, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return ["-I", inc]
+    except ImportError:
+        pass
+    return []
 
 
 def nvcc() -> str:
@@ -45,7 +59,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     target = out or OUT
     if not force and not defines and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", target] + [os.path.join(CSRC, s) for s in SOURCES]
+    cmd = [nvcc(), *NVCC_FLAGS, *nccl_include(), *[f"-D{d}" for d in defines], "-o", target] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

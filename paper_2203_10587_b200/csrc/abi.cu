@@ -1,6 +1,8 @@
 // C ABI of libacopf_b200.so: batch planning on the host, device residency,
 // and the evaluation launch.  See include/acopf_b200.h for the contract.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -117,6 +119,7 @@ struct acopf_batch {
     DevBuf d_topo, d_stage, d_items, d_recs, d_aux, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
     DevBuf d_cpruns, d_objterms, d_xi;
     int max_nb = 0;
+    int n_gen_items = 0;             // aux items [0, n_gen_items) are generator chunks, the rest coupling runs
     std::vector<std::unique_ptr<DevBuf>> topo_bufs;
     EvalParams params{};
     size_t smem = 0, aux_smem = 0;
@@ -136,6 +139,68 @@ struct acopf_batch {
         for (auto& ps : pipe_streams) if (ps) cudaStreamDestroy(ps);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Multi-GPU (one process per GPU): NCCL loaded at run time (dlopen), so the
+// library has no link-time NCCL dependency and shares the process's NCCL
+// (torch's) when one is already loaded.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        void* h = nullptr;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            h = dlopen(name, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);     // the process's NCCL (torch's) first
+            if (!h) h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) { err = "libnccl.so.2 not found"; return; }
+        api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+        api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+        api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+        api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    });
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.CommDestroy)
+        throw std::runtime_error("NCCL unavailable: " + (err.empty() ? std::string("missing symbols") : err));
+    return api;
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw std::runtime_error(std::string(what) + ": " +
+                                 (nccl().GetErrorString ? nccl().GetErrorString(r) : std::to_string((int)r)));
+}
+
+// One rank's share of a sharded composite: its batch (its stages, composite
+// layout with a halo, ACOPF_OBJ_TERMS) plus the exchange plan and buffers.
+struct acopf_multi {
+    acopf_batch* b = nullptr;
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    std::vector<int64_t> export_idx;         // local x indices this rank sends (sorted)
+    std::vector<int64_t> halo_src;           // per halo value: position in the gathered buffer
+    int64_t export_max = 1, halo_dst0 = 0;
+    std::vector<int32_t> obj_counts;         // objective terms per rank (stage order)
+    int obj_max = 1;
+    DevBuf d_export, d_halo_src, d_send, d_recv, d_obj_send, d_obj_recv, d_counts;
+    cudaStream_t halo_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_halo = nullptr, ev_gen = nullptr;
+    ~acopf_multi() {
+        if (comm) nccl().CommDestroy(comm);
+        if (halo_stream) cudaStreamDestroy(halo_stream);
+        for (cudaEvent_t e : {ev_fork, ev_halo, ev_gen}) if (e) cudaEventDestroy(e);
     }
 };
 
@@ -296,6 +361,7 @@ static void upload(acopf_batch* b) {
         for (int c = 0; c < nch; ++c) aux.push_back(DAuxItem{0, s, c, 0});
     }
     aux_first_of_stage[S] = (int)aux.size();
+    b->n_gen_items = (int)aux.size();
     // pipeline chunks for host-buffer evaluation of independent layouts: about 8
     // chunks of whole stage groups (bus items are stage-group-major)
     b->pipe.clear();
@@ -1014,6 +1080,180 @@ int acopf_batch_verify(const acopf_batch* b, int64_t* stats) {
             stats[6] = rounds; stats[7] = lane_terms; stats[8] = chain;
             stats[9] = cost[0]; stats[10] = cost[1]; stats[11] = cost[2];
         }
+    });
+}
+
+int acopf_nccl_unique_id(void* id128) {
+    return guard([&] {
+        if (!id128) throw std::runtime_error("id buffer is NULL");
+        ncclUniqueId id;
+        nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(id128, &id, sizeof id);
+    });
+}
+
+int acopf_multi_create(acopf_batch* b, int32_t rank, int32_t world, const int64_t* x_lo, const int64_t* x_hi,
+                       const int64_t* need_ptr, const int64_t* need_idx, int64_t halo_dst0,
+                       const int32_t* obj_counts, const void* nccl_id, acopf_multi** out) {
+    return guard([&] {
+        if (!b || !out || world < 1 || rank < 0 || rank >= world) throw std::runtime_error("bad arguments");
+        if (!b->laid_out) throw std::runtime_error("acopf_batch_set_layout was not called");
+        if (b->obj_mode != ACOPF_OBJ_TERMS) throw std::runtime_error("a sharded batch needs ACOPF_OBJ_TERMS");
+        std::unique_ptr<acopf_multi> M(new acopf_multi());
+        M->b = b;
+        M->rank = rank;
+        M->world = world;
+        M->halo_dst0 = halo_dst0;
+        // exports: every global index some other rank needs that lies in this rank's x range
+        const int64_t lo = x_lo[rank], hi = x_hi[rank];
+        std::vector<int64_t> ex;
+        for (int r = 0; r < world; ++r) {
+            if (r == rank) continue;
+            for (int64_t i = need_ptr[r]; i < need_ptr[r + 1]; ++i)
+                if (need_idx[i] >= lo && need_idx[i] < hi) ex.push_back(need_idx[i]);
+        }
+        std::sort(ex.begin(), ex.end());
+        ex.erase(std::unique(ex.begin(), ex.end()), ex.end());
+        // every rank's export list (derived from the same inputs), for the gathered layout
+        std::vector<std::vector<int64_t>> exports(world);
+        for (int q = 0; q < world; ++q) {
+            for (int r = 0; r < world; ++r) {
+                if (r == q) continue;
+                for (int64_t i = need_ptr[r]; i < need_ptr[r + 1]; ++i)
+                    if (need_idx[i] >= x_lo[q] && need_idx[i] < x_hi[q]) exports[q].push_back(need_idx[i]);
+            }
+            std::sort(exports[q].begin(), exports[q].end());
+            exports[q].erase(std::unique(exports[q].begin(), exports[q].end()), exports[q].end());
+            M->export_max = std::max<int64_t>(M->export_max, (int64_t)exports[q].size());
+        }
+        for (int64_t g : ex) M->export_idx.push_back(g - lo);
+        // halo: this rank's needs, each read from its owner's slot in the gathered buffer
+        for (int64_t i = need_ptr[rank]; i < need_ptr[rank + 1]; ++i) {
+            const int64_t g = need_idx[i];
+            int owner = -1;
+            for (int q = 0; q < world && owner < 0; ++q)
+                if (g >= x_lo[q] && g < x_hi[q]) owner = q;
+            if (owner < 0 || owner == rank) throw std::runtime_error("halo index not owned by another rank");
+            const auto& e = exports[owner];
+            const int64_t j = (int64_t)(std::lower_bound(e.begin(), e.end(), g) - e.begin());
+            M->halo_src.push_back((int64_t)owner * M->export_max + j);
+        }
+        M->obj_counts.assign(obj_counts, obj_counts + world);
+        for (int32_t c : M->obj_counts) M->obj_max = std::max<int>(M->obj_max, c);
+        if (M->obj_counts[rank] != (int)b->stages.size())
+            throw std::runtime_error("obj_counts[rank] must equal this rank's stage count");
+        if (nccl_id) {            // device side: communicator and buffers (collective over all ranks)
+            cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof id);
+            nccl_check(nccl().CommInitRank(&M->comm, world, id, rank), "ncclCommInitRank");
+            M->d_export.upload(M->export_idx);
+            M->d_halo_src.upload(M->halo_src);
+            M->d_counts.upload(M->obj_counts);
+            M->d_send.alloc(sizeof(double) * (size_t)M->export_max);
+            M->d_recv.alloc(sizeof(double) * (size_t)M->export_max * world);
+            M->d_obj_send.alloc(sizeof(double) * (size_t)M->obj_max);
+            M->d_obj_recv.alloc(sizeof(double) * (size_t)M->obj_max * world);
+            cuda_check(cudaStreamCreateWithFlags(&M->halo_stream, cudaStreamNonBlocking), "stream");
+            for (cudaEvent_t* e : {&M->ev_fork, &M->ev_halo, &M->ev_gen})
+                cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+        }
+        *out = M.release();
+    });
+}
+
+int acopf_multi_plan(const acopf_multi* m, int64_t* sizes3, int64_t* export_idx, int64_t* halo_src) {
+    return guard([&] {
+        if (sizes3) { sizes3[0] = (int64_t)m->export_idx.size(); sizes3[1] = m->export_max; sizes3[2] = (int64_t)m->halo_src.size(); }
+        if (export_idx) std::copy(m->export_idx.begin(), m->export_idx.end(), export_idx);
+        if (halo_src) std::copy(m->halo_src.begin(), m->halo_src.end(), halo_src);
+    });
+}
+
+int acopf_multi_destroy(acopf_multi* m) {
+    if (m) {
+        cudaSetDevice(m->b->device);
+        delete m;
+    }
+    return 0;
+}
+
+int acopf_batch_eval_multi(acopf_multi* m, double* x, double obj_factor, const double* mult, uint32_t what,
+                           double* obj, double* grad, double* cons, double* jval, double* hval, void* stream) {
+    return guard([&] {
+        if (!m->comm) throw std::runtime_error("multi handle made without a NCCL id (plan only)");
+        acopf_batch* b = m->b;
+        if (!b->uploaded) upload(b);
+        if ((what & ACOPF_ALL) && !x) throw std::runtime_error("x is NULL");
+        if ((what & ACOPF_OBJ) && !obj) throw std::runtime_error("obj is NULL");
+        if ((what & ACOPF_GRAD) && !grad) throw std::runtime_error("grad is NULL");
+        if ((what & ACOPF_CONS) && !cons) throw std::runtime_error("cons is NULL");
+        if ((what & ACOPF_JAC) && !jval) throw std::runtime_error("jval is NULL");
+        if ((what & ACOPF_HESS) && (!hval || !mult)) throw std::runtime_error("hval/mult is NULL");
+        cuda_check(cudaSetDevice(b->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        EvalParams P = b->params;
+        P.x = x; P.mult = mult; P.obj_factor = obj_factor; P.what = what;
+        P.obj = static_cast<double*>(m->d_obj_send.p);      // this rank's w_s f_s, padded to obj_max
+        P.grad = grad; P.cons = cons; P.jval = jval; P.hval = hval;
+        cuda_check(cudaEventRecord(m->ev_fork, st), "event record");
+        // halo chain on its own stream: pack -> NCCL all-gather -> unpack -> coupling rows;
+        // it overlaps the tile kernel, which never reads the halo
+        const int n_cp_items = P.n_aux_items - b->n_gen_items;
+        const bool halo = (what & (ACOPF_CONS | ACOPF_JAC)) != 0;
+        if (halo) {
+            cudaStream_t hs = m->halo_stream;
+            cuda_check(cudaStreamWaitEvent(hs, m->ev_fork, 0), "stream wait");
+            const long long ne = (long long)m->export_idx.size(), nh = (long long)m->halo_src.size();
+            acopf_halo_pack_kernel<<<(unsigned)std::max<long long>(1, std::min<long long>(1184, (m->export_max + BLOCK - 1) / BLOCK)),
+                                     BLOCK, 0, hs>>>(x, static_cast<const long long*>(m->d_export.p), ne, m->export_max,
+                                                     static_cast<double*>(m->d_send.p));
+            cuda_check(cudaGetLastError(), "acopf_halo_pack_kernel launch");
+            b->launches++;
+            nccl_check(nccl().AllGather(m->d_send.p, m->d_recv.p, (size_t)m->export_max, ncclDouble, m->comm, hs),
+                       "ncclAllGather(halo)");
+            if (nh > 0) {
+                acopf_halo_unpack_kernel<<<(unsigned)std::max<long long>(1, std::min<long long>(1184, (nh + BLOCK - 1) / BLOCK)),
+                                           BLOCK, 0, hs>>>(x, m->halo_dst0, static_cast<const long long*>(m->d_halo_src.p),
+                                                           nh, static_cast<const double*>(m->d_recv.p));
+                cuda_check(cudaGetLastError(), "acopf_halo_unpack_kernel launch");
+                b->launches++;
+            }
+            if (n_cp_items > 0) {
+                acopf_aux_kernel<<<n_cp_items, BLOCK, b->aux_smem, hs>>>(P, b->n_gen_items);
+                cuda_check(cudaGetLastError(), "acopf_aux_kernel (coupling) launch");
+                b->launches++;
+            }
+            cuda_check(cudaEventRecord(m->ev_halo, hs), "event record");
+        }
+        // generator chunks (gradient, PG Hessian diagonal, w_s f_s) beside the tile kernel
+        const bool gen = (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS)) && b->n_gen_items > 0;
+        if (gen) {
+            cuda_check(cudaStreamWaitEvent(b->aux_stream, m->ev_fork, 0), "stream wait");
+            acopf_aux_kernel<<<b->n_gen_items, BLOCK, b->aux_smem, b->aux_stream>>>(P, 0);
+            cuda_check(cudaGetLastError(), "acopf_aux_kernel (generators) launch");
+            b->launches++;
+            if (what & ACOPF_OBJ) {
+                // every rank's terms, then the stage-order sum (bit-identical to one GPU)
+                nccl_check(nccl().AllGather(m->d_obj_send.p, m->d_obj_recv.p, (size_t)m->obj_max, ncclDouble, m->comm,
+                                            b->aux_stream), "ncclAllGather(objective)");
+                acopf_objsum_multi_kernel<<<1, BLOCK, 0, b->aux_stream>>>(static_cast<const double*>(m->d_obj_recv.p),
+                                                                          static_cast<const int*>(m->d_counts.p),
+                                                                          m->world, m->obj_max, obj);
+                cuda_check(cudaGetLastError(), "acopf_objsum_multi_kernel launch");
+                b->launches++;
+            }
+            cuda_check(cudaEventRecord(m->ev_gen, b->aux_stream), "event record");
+        }
+        if ((what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) && P.n_bus_items > 0) {
+            launch_interleave(b, P, 0, (int)b->stages.size(), st);
+            if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
+            else acopf_tile_kernel<0u><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
+            cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
+            b->launches++;
+        }
+        if (halo) cuda_check(cudaStreamWaitEvent(st, m->ev_halo, 0), "stream wait");
+        if (gen) cuda_check(cudaStreamWaitEvent(st, m->ev_gen, 0), "stream wait");
     });
 }
 

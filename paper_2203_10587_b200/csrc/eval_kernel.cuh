@@ -929,6 +929,45 @@ __global__ void __launch_bounds__(BLOCK) acopf_interleave_kernel(const EvalParam
     }
 }
 
+// ---------------------------------------------------------------------------
+// multi-GPU halo and objective (acopf_batch_eval_multi)
+
+// send[j] = x[idx[j]] (the base-stage values other ranks' coupling rows read),
+// zero padding up to n_pad
+__global__ void __launch_bounds__(BLOCK) acopf_halo_pack_kernel(const double* x, const long long* idx, long long n,
+                                                               long long n_pad, double* send) {
+    for (long long j = blockIdx.x * (long long)BLOCK + threadIdx.x; j < n_pad; j += (long long)gridDim.x * BLOCK)
+        send[j] = j < n ? x[idx[j]] : 0.0;
+}
+
+// x[dst0 + i] = recv[src[i]] (the gathered [world][export_max] buffer -> this rank's halo)
+__global__ void __launch_bounds__(BLOCK) acopf_halo_unpack_kernel(double* x, long long dst0, const long long* src,
+                                                                 long long n, const double* recv) {
+    for (long long i = blockIdx.x * (long long)BLOCK + threadIdx.x; i < n; i += (long long)gridDim.x * BLOCK)
+        x[dst0 + i] = recv[src[i]];
+}
+
+// The composite objective over all ranks' w_s f_s terms, gathered rank-major
+// ([world][per_rank], rank r holding counts[r]), added in global stage order
+// ((0 + t_0) + t_1) + ... -- bit-identical to the one-GPU acopf_objsum_kernel.
+__global__ void __launch_bounds__(BLOCK) acopf_objsum_multi_kernel(const double* terms, const int* counts, int world,
+                                                                   int per_rank, double* obj) {
+    __shared__ double buf[BLOCK];
+    double acc = 0.0;
+    for (int r = 0; r < world; ++r) {
+        const int cnt = counts[r];
+        for (int i0 = 0; i0 < cnt; i0 += BLOCK) {
+            const int n = min(BLOCK, cnt - i0);
+            if ((int)threadIdx.x < n) buf[threadIdx.x] = terms[(long long)r * per_rank + i0 + threadIdx.x];
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int i = 0; i < n; ++i) acc = acc + buf[i];
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) obj[0] = acc;
+}
+
 __global__ void __launch_bounds__(BLOCK) acopf_aux_kernel(const EvalParams P, int item0) {
     extern __shared__ __align__(16) double leaves[];
     const DAuxItem it = P.aux_items[item0 + blockIdx.x];

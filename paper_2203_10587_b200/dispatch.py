@@ -7,15 +7,18 @@ the native evaluator for its stages only.  Its flat buffers hold, in the
 global order, its stage variables (plus a halo), its constraint rows
 ``[eq blocks | pins | ineq blocks | boxes]`` and the matching J / H values.
 
-Collectives (the only data exchanged):
+Collectives (the only data exchanged; both inside the C ABI's
+``acopf_batch_eval_multi``, NCCL over NVLink):
 
 * halo: coupling rows ``x[child] - x[base]`` whose base stage lives on another
-  rank read the base values from a halo filled by one ``all_gather`` of each
-  rank's exported values (base-stage Pg / VM; a period neighbour's Pg);
+  rank read the base values from a halo filled by one ``ncclAllGather`` of
+  each rank's exported values (base-stage Pg / VM; a period neighbour's Pg),
+  packed and unpacked by the library's kernels on a stream beside the tile
+  kernel;
 * objective: every rank writes its per-stage ``w_s f_s`` (ACOPF_OBJ_TERMS);
-  the terms are all-gathered and summed in global stage order, which keeps
-  the composite objective bit-identical to the single-GPU evaluation
-  (composer.py:256-258 sums left to right).
+  the terms are all-gathered and summed in global stage order on the device,
+  which keeps the composite objective bit-identical to the single-GPU
+  evaluation (composer.py:256-258 sums left to right).
 """
 
 from __future__ import annotations
@@ -104,14 +107,22 @@ class ShardedComposite:
     """One rank's evaluator for a sharded composite.
 
     ``dist`` is ``torch.distributed`` (initialised); tensors live on
-    ``device`` (CUDA for NCCL, CPU for gloo).  ``local_eval`` replaces the
-    native evaluation (CPU tests); by default the rank's BatchEvaluator runs
-    the CUDA kernels.
+    ``device``.  The exchange runs inside the C ABI: ``acopf_multi_create``
+    computes the plan (exports, halo positions, objective counts) from every
+    rank's halo needs and makes the NCCL communicator (its id is made by rank 0
+    and broadcast through ``dist``); ``acopf_batch_eval_multi`` runs the halo
+    pack -> ncclAllGather -> unpack -> coupling-row chain on a forked stream
+    beside the tile kernel and sums every rank's objective terms in stage order
+    on the device.  ``local_eval`` (CPU tests, gloo) replaces the device
+    evaluation: the native plan is then executed by this class's emulation of
+    the same exchange over ``dist``.
     """
 
     def __init__(self, spec, dist, rank: int, world: int, device="cuda", align=None, local_eval=None):
+        import ctypes
         import torch
-        self.torch, self.dist = torch, dist
+        from . import _lib as L
+        self.torch, self.dist, self.L = torch, dist, L
         self.plan = plan = ShardPlan(spec, rank, world, align)
         self.device = torch.device(device)
         dev_index = self.device.index or 0
@@ -119,75 +130,103 @@ class ShardedComposite:
                                  coupling=plan.coupling, n_pins=plan.n_pins, obj_terms=True)
         assert self.ev.n == plan.n_loc and self.ev.m_eq == plan.m_eq_loc
         self.local_eval = local_eval
-        # halo exchange plan: every rank exports the values any other rank needs from it
-        needs = [None] * world
-        dist.all_gather_object(needs, plan.halo_idx.tolist())
-        exports = sorted({g for r, lst in enumerate(needs) if r != rank for g in lst
-                          if plan.x_lo <= g < plan.x_hi})
-        self.export_local = torch.as_tensor(np.array(exports, dtype=np.int64) - plan.x_lo, device=self.device)
-        sizes = [None] * world
-        dist.all_gather_object(sizes, len(exports))
-        self.export_sizes = sizes
-        self.export_max = max(max(sizes), 1)
-        all_exports = [None] * world
-        dist.all_gather_object(all_exports, exports)
-        # where each halo value sits in the gathered [world, export_max] buffer
-        pos = {}
-        for r, lst in enumerate(all_exports):
-            for j, g in enumerate(lst):
-                pos.setdefault(g, r * self.export_max + j)
-        self.halo_src = torch.as_tensor([pos[int(g)] for g in plan.halo_idx], dtype=torch.int64,
-                                        device=self.device)
-        # objective terms of every rank, in stage order
-        counts = [None] * world
-        dist.all_gather_object(counts, plan.s1 - plan.s0)
-        self.obj_counts = counts
-        self.obj_max = max(max(counts), 1)
+        # every rank's halo needs, x range and stage count (host exchange, once)
+        info = [None] * world
+        dist.all_gather_object(info, (plan.halo_idx.tolist(), plan.x_lo, plan.x_hi, plan.s1 - plan.s0))
+        need_ptr = np.zeros(world + 1, dtype=np.int64)
+        for r, (nd, _, _, _) in enumerate(info):
+            need_ptr[r + 1] = need_ptr[r] + len(nd)
+        need_idx = L.i64(np.concatenate([np.asarray(nd, dtype=np.int64) for nd, _, _, _ in info] + [np.zeros(1)]))
+        x_lo = L.i64([a for _, a, _, _ in info])
+        x_hi = L.i64([b for _, _, b, _ in info])
+        self.obj_counts = counts = L.i32([c for _, _, _, c in info])
+        nccl_id = None
+        if local_eval is None and self.device.type == "cuda":
+            idbuf = ctypes.create_string_buffer(128)
+            if rank == 0:
+                L.check(L.lib().acopf_nccl_unique_id(idbuf))
+            box = [idbuf.raw if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            idbuf = ctypes.create_string_buffer(box[0], 128)
+            nccl_id = idbuf
+        h = ctypes.c_void_p()
+        L.check(L.lib().acopf_multi_create(self.ev._h, rank, world, L.ptr(x_lo, ctypes.c_int64),
+                                           L.ptr(x_hi, ctypes.c_int64), L.ptr(need_ptr, ctypes.c_int64),
+                                           L.ptr(need_idx, ctypes.c_int64), plan.n_loc,
+                                           L.ptr(counts, ctypes.c_int32), nccl_id, ctypes.byref(h)))
+        self._m = h
+        sizes = np.zeros(3, dtype=np.int64)
+        L.check(L.lib().acopf_multi_plan(h, L.ptr(sizes, ctypes.c_int64), None, None))
+        exp_idx = np.zeros(max(int(sizes[0]), 1), dtype=np.int64)
+        halo_src = np.zeros(max(int(sizes[2]), 1), dtype=np.int64)
+        L.check(L.lib().acopf_multi_plan(h, None, L.ptr(exp_idx, ctypes.c_int64), L.ptr(halo_src, ctypes.c_int64)))
+        self.export_local = exp_idx[:int(sizes[0])]
+        self.export_max = int(sizes[1])
+        self.halo_src = halo_src[:int(sizes[2])]
+        self.obj_max = max(int(counts.max()), 1)
         self.n_x = plan.n_loc + len(plan.halo_idx)
+        self._obj = None
+
+    def launches(self) -> int:
+        return self.ev.launches()
 
     # -- buffers -----------------------------------------------------------------
 
     def alloc_x(self):
         return self.torch.zeros(max(self.n_x, 1), dtype=self.torch.float64, device=self.device)
 
-    def exchange_halo(self, x):
-        """Fill x[n_loc:] with the base values owned by other ranks."""
-        torch = self.torch
-        send = torch.zeros(self.export_max, dtype=torch.float64, device=self.device)
-        if len(self.export_local):
-            send[:len(self.export_local)] = x[self.export_local]
-        recv = torch.empty(self.plan.world * self.export_max, dtype=torch.float64, device=self.device)
-        self.dist.all_gather_into_tensor(recv, send)
-        if len(self.halo_src):
-            x[self.plan.n_loc:self.n_x] = recv[self.halo_src]
-
-    def combine_objective(self, terms) -> float:
-        """Sum of all ranks' w_s f_s in global stage order ((0 + t_0) + t_1) + ..."""
-        torch = self.torch
-        buf = torch.zeros(self.obj_max, dtype=torch.float64, device=self.device)
-        buf[:len(terms)] = terms
-        out = torch.empty(self.plan.world * self.obj_max, dtype=torch.float64, device=self.device)
-        self.dist.all_gather_into_tensor(out, buf)
-        host = out.cpu().numpy().reshape(self.plan.world, self.obj_max)
-        acc = 0.0
-        for r, c in enumerate(self.obj_counts):
-            for v in host[r, :c]:
-                acc = acc + float(v)
-        return acc
-
     def evaluate(self, x, mult, obj_factor: float = 1.0, what: int = 31, out=None, stream=None):
-        """Halo exchange, local evaluation, objective combination.  Returns (out, objective)."""
-        from . import _lib as L
-        if what & (L.CONS | L.JAC):
-            self.exchange_halo(x)
+        """One sharded evaluation.  Returns (out, objective): the objective is a 1-element
+        tensor on the device (no host synchronisation), None unless OBJ is requested."""
+        import ctypes
+        L = self.L
         if self.local_eval is not None:
-            out = self.local_eval(x, mult, obj_factor, what)
-        else:
-            out = self.ev.eval_device(x, mult, obj_factor, what, out=out, stream=stream)
+            return self._emulated(x, mult, obj_factor, what)
+        out = out if out is not None else self.ev.alloc(what)
+        if self._obj is None:
+            self._obj = self.torch.zeros(1, dtype=self.torch.float64, device=self.device)
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
+        L.check(L.lib().acopf_batch_eval_multi(
+            self._m, ptr(x), float(obj_factor), ptr(mult), int(what), ptr(self._obj), ptr(out["grad"]),
+            ptr(out["cons"]), ptr(out["jac"]), ptr(out["hess"]), self.ev.stream_handle(stream)))
+        return out, (self._obj if what & L.OBJ else None)
+
+    # -- CPU emulation of the native exchange (tests over gloo) ----------------------
+
+    def _emulated(self, x, mult, obj_factor, what):
+        torch, L = self.torch, self.L
+        world = self.plan.world
+        if what & (L.CONS | L.JAC):
+            send = torch.zeros(self.export_max, dtype=torch.float64, device=self.device)
+            if len(self.export_local):
+                send[:len(self.export_local)] = x[torch.as_tensor(self.export_local)]
+            recv = torch.empty(world * self.export_max, dtype=torch.float64, device=self.device)
+            self.dist.all_gather_into_tensor(recv, send)
+            if len(self.halo_src):
+                x[self.plan.n_loc:self.n_x] = recv[torch.as_tensor(self.halo_src)]
+        out = self.local_eval(x, mult, obj_factor, what)
         obj = None
         if what & L.OBJ:
-            obj = self.combine_objective(out["obj"][:self.plan.s1 - self.plan.s0])
+            buf = torch.zeros(self.obj_max, dtype=torch.float64, device=self.device)
+            terms = out["obj"][:self.plan.s1 - self.plan.s0]
+            buf[:len(terms)] = terms
+            allt = torch.empty(world * self.obj_max, dtype=torch.float64, device=self.device)
+            self.dist.all_gather_into_tensor(allt, buf)
+            host = allt.cpu().numpy().reshape(world, self.obj_max)
+            acc = 0.0
+            for r, c in enumerate(self.obj_counts):            # acopf_objsum_multi_kernel's order
+                for v in host[r, :c]:
+                    acc = acc + float(v)
+            obj = torch.tensor([acc], dtype=torch.float64)
         return out, obj
+
+    def __del__(self):
+        h = getattr(self, "_m", None)
+        if h is not None:
+            try:
+                self.L.lib().acopf_multi_destroy(h)
+            except Exception:
+                pass
 
     # -- placing local results in the global vectors (tests, drop-in API) -----------
 

@@ -2,9 +2,11 @@
 
 The device evaluation is replaced by the oracle (test-only); everything else
 is the product path: stage partition, each rank's native planner (host side),
-halo exchange of base-stage values, ordered objective combination, and the
-local -> global range mapping, which is checked against the oracle's global
-CSR patterns.
+the exchange plan computed by the C ABI (acopf_multi_create, plan-only
+handle: exports, halo positions, objective counts), executed over gloo by
+ShardedComposite's emulation of acopf_batch_eval_multi's exchange, the ordered
+objective combination, and the local -> global range mapping, which is
+checked against the oracle's global CSR patterns.
 """
 
 import os
@@ -103,7 +105,7 @@ def _worker(rank, world, port, results):
                 for key in glob:
                     for gs, ls, ln in prg[key]:
                         glob[key][gs:gs + ln] = pres[key][ls:ls + ln]
-            out[name] = dict(obj=obj == o.objective(x), ok_j=bool(ok_j), ok_h=bool(ok_h),
+            out[name] = dict(obj=float(obj[0]) == o.objective(x), ok_j=bool(ok_j), ok_h=bool(ok_h),
                              cons=C.bit_diffs(glob["cons"], g_cons), grad=C.bit_diffs(glob["grad"], g_grad),
                              jac=C.bit_diffs(glob["jac"], J.data), hess=C.bit_diffs(glob["hess"], H.data),
                              halo=len(sc.plan.halo_idx))
