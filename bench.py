@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--points", type=int, default=100, help="evaluation points per step (config 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="composites through the sharded entry point (acopf_batch_eval_multi) even on one rank")
     return ap.parse_args()
 
 
@@ -111,7 +113,7 @@ class Runner:
         self.n_coupling = n_coupling          # coupling rows of this rank's evaluator
 
 
-def build_ours(cfg: int, points: int, device: int, seed0: int, dist=None, rank=0, world=1):
+def build_ours(cfg: int, points: int, device: int, seed0: int, dist=None, rank=0, world=1, sharded=False):
     """Runner for config cfg on cuda:device (sharded over ranks for composites when world > 1)."""
     from paper_2203_10587_b200 import synthetic as syn
     from paper_2203_10587_b200 import BatchEvaluator, compose_general, compose_multiperiod, compose_scopf
@@ -131,7 +133,7 @@ def build_ours(cfg: int, points: int, device: int, seed0: int, dist=None, rank=0
             ms.append(m)
         return Runner(ev, np.concatenate(xs), np.concatenate(ms), points)
     kind, args, per_scen = _composite_args(cfg)
-    if world > 1:
+    if world > 1 or sharded:
         from paper_2203_10587_b200.dispatch import ShardedComposite
         from paper_2203_10587_b200.lattice import composite_spec
         spec = composite_spec(kind, *args)
@@ -369,11 +371,15 @@ def main():
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or (args.sharded and args.config != 1):
+        if "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ.get("MASTER_PORT", "29533"),
+                              RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    run = build_ours(args.config, args.points, local, seed0=1_000_000 * (rank + 1), dist=dist if world > 1 else None,
-                     rank=rank, world=world)
+    run = build_ours(args.config, args.points, local, seed0=1_000_000 * (rank + 1),
+                     dist=dist if dist.is_initialized() else None, rank=rank, world=world,
+                     sharded=args.sharded and args.config != 1)
     ev, x_h, m_h, units, sc = run.ev, run.x_h, run.m_h, run.units, run.sharded
     x = torch.from_numpy(x_h).to(dev)
     mult = torch.from_numpy(m_h).to(dev)
@@ -508,7 +514,7 @@ def main():
             "dtype": "f64", "data": "synthetic (seeded, SURVEY §8d)",
             "config": cfg,
             "parallelism": (f"replicas x{world}" if sc is None else f"stage shards x{world} (NCCL halo + objective)")
-                           if world > 1 else "single GPU",
+                           if world > 1 or sc is not None else "single GPU",
             "units_per_step": units * (world if sc is None else 1),
             "l2": ("inputs (x + multipliers) and outputs exceed the 126 MB L2 many times over; the K steps "
                    "run back to back between one pair of CUDA events" if back_to_back else
@@ -527,7 +533,7 @@ def main():
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
