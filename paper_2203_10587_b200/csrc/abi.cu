@@ -19,6 +19,7 @@
 
 #include "../../include/acopf_b200.h"
 #include "eval_kernel.cuh"
+#include "sl_kernel.cuh"
 #include "planner.hpp"
 #include "writer.hpp"
 
@@ -126,6 +127,17 @@ struct acopf_batch {
     int64_t launches = 0;
     // host staging for eval_host
     DevBuf h_x, h_m, h_obj, h_g, h_c, h_j, h_h;
+    // stage-lane path for full evaluations (sl_kernel.cuh): SL tiles per base table
+    // (topology, tile) (empty: a bus needs more term slots; that tile stays on the tile
+    // kernel), groups of 32 stages, items, and the tile-kernel items of the rest
+    bool sl_on = false;
+    std::vector<std::vector<SLTile>> sl_tiles;     // index: topo * ntile_max + tile
+    int sl_ntile_max = 0;
+    SLParams slp{};
+    size_t sl_smem = 0;
+    int n_res_items = 0;
+    DevBuf d_sl_groups, d_sl_items, d_sl_boff, d_sl_bytes, d_sl_runoff, d_sl_tileout, d_sl_blob, d_sl_x;
+    DevBuf d_res_items, d_res_recs;
 
     // host-buffer pipeline (independent layouts): chunks of whole stage groups
     struct Pipe { int s0, s1, bus_first, bus_count, aux_first, aux_count; };
@@ -309,44 +321,184 @@ static void upload(acopf_batch* b) {
     // pay the table load per stage)
     const int G = (int)std::max<int64_t>(std::min<int64_t>(2, g_l2),
                                          std::min<int64_t>({g_max, total_recs / target_items, g_l2}));
-    std::vector<DBusItem> items;
-    std::vector<DRec> recs;
     size_t max_smem = 0;
-    std::map<int, std::vector<int>> by_table;     // table id -> stages (in order)
     std::vector<std::pair<int, int>> tiles;       // (topo, tile)
     for (size_t ti = 0; ti < b->topos.size(); ++ti)
         for (size_t t = 0; t < b->base_table[ti].size(); ++t) tiles.push_back({(int)ti, (int)t});
     std::vector<int> table_area(b->tables.size());
     for (size_t i = 0; i < b->tables.size(); ++i) table_area[i] = b->tables[i].nArea + table_shift_n[i];
-    // stage-group-major order: warps running together share one group's x/mult in L2
-    for (int g0 = 0; g0 < S; g0 += G) {
-        const int g1 = std::min(S, g0 + G);
-        for (auto [topo, t] : tiles) {
-            by_table.clear();
-            for (int s = g0; s < g1; ++s)
-                if (b->stages[s].topo == topo) by_table[b->stages[s].table[t]].push_back(s);
-            for (auto& kv : by_table) {
-                DBusItem it{};
-                it.blob_off = table_off[kv.first];
-                it.bytes = table_bytes[kv.first];
-                it.first = (int)recs.size();
-                it.count = (int)kv.second.size();
-                for (int s : kv.second) {
-                    const StageInfo& st = b->stages[s];
-                    const DStage& d = ds[s];
-                    DRec r{};
-                    r.var_off = d.var_off; r.eq_row = d.eq_row; r.ineq_row = d.ineq_row; r.pd_off = d.pd_off;
-                    r.jineq = d.jineq_base;
-                    r.oP = d.jeq_base + st.tile_off[4 * t + 0]; r.oQ = d.jeq_base + st.tile_off[4 * t + 1];
-                    r.oA = d.h_base + st.tile_off[4 * t + 2]; r.oV = d.h_base + st.tile_off[4 * t + 3];
-                    r.fl_off = d.fl_off; r.inj_off = d.inj_off; r.rem_off = d.rem_off;
-                    r.w = d.w; r.nrem = d.nrem; r.nb = d.nb; r.ng = d.ng; r.nbr = d.nbr;
-                    r.stage = s;
-                    recs.push_back(r);
+    // tile-kernel items over the (tile, stage) pairs `keep` accepts, stage-group-major
+    // (warps running together share one group's x/mult in L2)
+    auto build_items = [&](auto keep, std::vector<DBusItem>& items, std::vector<DRec>& recs) {
+        std::map<int, std::vector<int>> by_table;     // table id -> stages (in order)
+        for (int g0 = 0; g0 < S; g0 += G) {
+            const int g1 = std::min(S, g0 + G);
+            for (auto [topo, t] : tiles) {
+                by_table.clear();
+                for (int s = g0; s < g1; ++s)
+                    if (b->stages[s].topo == topo && keep(t, s)) by_table[b->stages[s].table[t]].push_back(s);
+                for (auto& kv : by_table) {
+                    DBusItem it{};
+                    it.blob_off = table_off[kv.first];
+                    it.bytes = table_bytes[kv.first];
+                    it.first = (int)recs.size();
+                    it.count = (int)kv.second.size();
+                    for (int s : kv.second) {
+                        const StageInfo& st = b->stages[s];
+                        const DStage& d = ds[s];
+                        DRec r{};
+                        r.var_off = d.var_off; r.eq_row = d.eq_row; r.ineq_row = d.ineq_row; r.pd_off = d.pd_off;
+                        r.jineq = d.jineq_base;
+                        r.oP = d.jeq_base + st.tile_off[4 * t + 0]; r.oQ = d.jeq_base + st.tile_off[4 * t + 1];
+                        r.oA = d.h_base + st.tile_off[4 * t + 2]; r.oV = d.h_base + st.tile_off[4 * t + 3];
+                        r.fl_off = d.fl_off; r.inj_off = d.inj_off; r.rem_off = d.rem_off;
+                        r.w = d.w; r.nrem = d.nrem; r.nb = d.nb; r.ng = d.ng; r.nbr = d.nbr;
+                        r.stage = s;
+                        recs.push_back(r);
+                    }
+                    items.push_back(it);
+                    max_smem = std::max(max_smem, tile_smem_bytes(table_bytes[kv.first], table_area[kv.first]));
                 }
-                items.push_back(it);
-                const TileTable& tt = b->tables[kv.first];
-                max_smem = std::max(max_smem, tile_smem_bytes(table_bytes[kv.first], table_area[kv.first]));
+            }
+        }
+    };
+    std::vector<DBusItem> items;
+    std::vector<DRec> recs;
+    build_items([](int, int) { return true; }, items, recs);
+    // ---- stage-lane path (full evaluations) ----
+    b->sl_on = false;
+    b->n_res_items = 0;
+    std::vector<DBusItem> res_items;
+    std::vector<DRec> res_recs;
+    {
+        const char* sle = getenv("ACOPF_SL");          // 0: tile kernel only (development aid / comparisons)
+        if (!sle || atoi(sle) != 0) {
+            int ntmax = 0;
+            for (size_t ti = 0; ti < b->topos.size(); ++ti) ntmax = std::max(ntmax, (int)b->base_table[ti].size());
+            if (b->sl_tiles.empty() || b->sl_ntile_max != ntmax) {
+                b->sl_ntile_max = ntmax;
+                b->sl_tiles.assign(b->topos.size() * (size_t)ntmax, {});
+                std::vector<std::pair<int, int>> jobs = tiles;
+                std::atomic<size_t> next{0};
+                auto work = [&] {
+                    for (size_t j; (j = next.fetch_add(1)) < jobs.size();) {
+                        const auto [topo, t] = jobs[j];
+                        std::vector<SLTile> v;
+                        if (!build_sl_tiles(*b->topos[topo], b->tables[b->base_table[topo][t]], t, v)) v.clear();
+                        b->sl_tiles[(size_t)topo * ntmax + t] = std::move(v);
+                    }
+                };
+                const int nt = (int)std::min<size_t>({(size_t)std::max(1u, std::thread::hardware_concurrency()),
+                                                      (size_t)32, jobs.size()});
+                std::vector<std::thread> pool;
+                for (int i = 1; i < nt; ++i) pool.emplace_back(work);
+                work();
+                for (auto& th : pool) th.join();
+            }
+            // global SL tile list
+            std::vector<int> first((size_t)b->topos.size() * ntmax, -1), count((size_t)b->topos.size() * ntmax, 0);
+            std::vector<long long> boff;
+            std::vector<int> bytes, runoff;
+            std::vector<uint8_t> sblob;
+            int table_max = 16, stride = 1;
+            for (auto [topo, t] : tiles) {
+                const auto& v = b->sl_tiles[(size_t)topo * ntmax + t];
+                if (v.empty()) continue;
+                first[(size_t)topo * ntmax + t] = (int)boff.size();
+                count[(size_t)topo * ntmax + t] = (int)v.size();
+                for (const SLTile& u : v) {
+                    boff.push_back((long long)sblob.size());
+                    bytes.push_back((int)u.blob.size());
+                    sblob.insert(sblob.end(), u.blob.begin(), u.blob.end());
+                    for (int q = 0; q < 4; ++q) runoff.push_back(u.off[q]);
+                    table_max = std::max(table_max, (int)u.blob.size());
+                    stride = std::max(stride, u.L[0] + u.L[1] + u.L[2] + u.L[3] + 4);
+                }
+            }
+            table_max = (table_max + 127) & ~127;
+            if (!(stride & 1)) ++stride;
+            // groups: stages ordered by (topology, removed branches, index), runs of <= 32 of one topology
+            std::vector<int> order(S);
+            std::iota(order.begin(), order.end(), 0);
+            std::stable_sort(order.begin(), order.end(), [&](int a, int c) {
+                const StageInfo &x = b->stages[a], &y = b->stages[c];
+                if (x.topo != y.topo) return x.topo < y.topo;
+                return x.removed < y.removed;
+            });
+            std::vector<SLGroup> groups;
+            long long xt = 0, mtt = 0, xg = 0;
+            for (int i = 0; i < S;) {
+                SLGroup G{};
+                for (int l = 0; l < 32; ++l) G.stage[l] = -1;
+                G.topo = b->stages[order[i]].topo;
+                int l = 0;
+                while (i < S && l < 32 && b->stages[order[i]].topo == G.topo) G.stage[l++] = order[i++];
+                G.nlanes = l;
+                const Topo& T = *b->topos[G.topo];
+                G.xt_off = xt; G.mt_off = mtt; G.xg_off = xg;
+                xt += 128LL * T.nb; mtt += 64LL * T.nr; xg += 64LL * T.ng;
+                groups.push_back(G);
+            }
+            const int ng_ = (int)groups.size();
+            std::vector<long long> tile_out((size_t)ng_ * ntmax * 128, -1);
+            std::vector<SLItem> sitems;
+            auto covered = [&](int t, int s) {
+                const StageInfo& st = b->stages[s];
+                return first[(size_t)st.topo * ntmax + t] >= 0 && st.table[t] == b->base_table[st.topo][t];
+            };
+            const int K = 4;                                  // SL tiles per warp item
+            for (int g = 0; g < ng_; ++g) {
+                const SLGroup& G = groups[g];
+                for (int t = 0; t < (int)b->base_table[G.topo].size(); ++t) {
+                    const int f = first[(size_t)G.topo * ntmax + t];
+                    if (f < 0) continue;
+                    bool any = false;
+                    long long* to = &tile_out[((size_t)g * ntmax + t) * 128];
+                    for (int l = 0; l < 32; ++l) {
+                        const int s2 = G.stage[l];
+                        if (s2 < 0 || !covered(t, s2)) continue;
+                        any = true;
+                        const StageInfo& st = b->stages[s2];
+                        to[l] = ds[s2].jeq_base + st.tile_off[4 * t + 0];
+                        to[32 + l] = ds[s2].jeq_base + st.tile_off[4 * t + 1];
+                        to[64 + l] = ds[s2].h_base + st.tile_off[4 * t + 2];
+                        to[96 + l] = ds[s2].h_base + st.tile_off[4 * t + 3];
+                    }
+                    if (!any) continue;
+                    const int n = count[(size_t)G.topo * ntmax + t];
+                    for (int u = 0; u < n; u += K) sitems.push_back(SLItem{g, t, f + u, f + std::min(n, u + K)});
+                }
+            }
+            if (!sitems.empty()) {
+                build_items([&](int t, int s2) { return !covered(t, s2); }, res_items, res_recs);
+                SLParams& Q = b->slp;
+                Q = SLParams{};
+                Q.groups = b->d_sl_groups.upload(groups);
+                Q.items = b->d_sl_items.upload(sitems);
+                Q.sl_blob_off = b->d_sl_boff.upload(boff);
+                Q.sl_bytes = b->d_sl_bytes.upload(bytes);
+                Q.sl_run_off = b->d_sl_runoff.upload(runoff);
+                Q.tile_out = b->d_sl_tileout.upload(tile_out);
+                Q.blob = b->d_sl_blob.upload(sblob);
+                Q.n_items = (int)sitems.size();
+                Q.n_groups = ng_;
+                Q.ntile_max = ntmax;
+                Q.stride = stride;
+                Q.table_max = table_max;
+                double* xb = static_cast<double*>(b->d_sl_x.alloc(sizeof(double) * (size_t)(xt + mtt + xg + 1)));
+                Q.xt = xb;
+                Q.mt = xb + xt;
+                Q.xg = xb + xt + mtt;
+                b->sl_smem = 2 * (size_t)table_max + 32 * (size_t)stride * 8;
+                if (b->sl_smem > (size_t)SMEM_LIMIT_BYTES) throw std::runtime_error("SL working set exceeds shared memory");
+                cuda_check(cudaFuncSetAttribute(acopf_sl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)b->sl_smem), "cudaFuncSetAttribute(sl)");
+                b->sl_on = true;
+                b->n_res_items = (int)res_items.size();
+                if (!res_items.empty()) {
+                    b->d_res_items.upload(res_items);
+                    b->d_res_recs.upload(res_recs);
+                }
             }
         }
     }
@@ -775,6 +927,37 @@ static void launch_interleave(acopf_batch* b, const EvalParams& P, int s0, int s
     }
 }
 
+// The bus-side work of one evaluation on st: for full evaluations with the
+// stage-lane path, the transposition pre-pass, the SL kernel and the tile kernel
+// for the (tile, stage) pairs SL does not cover; else the interleave pre-pass
+// (large networks) and the tile kernel over every item.
+static void launch_bus_work(acopf_batch* b, const EvalParams& P, cudaStream_t st) {
+    if (P.what == ACOPF_ALL && b->sl_on) {
+        const SLParams& Q = b->slp;
+        acopf_sl_transpose_kernel<<<dim3(64, (unsigned)Q.n_groups), 256, 0, st>>>(P, Q);
+        cuda_check(cudaGetLastError(), "acopf_sl_transpose_kernel launch");
+        acopf_sl_kernel<<<Q.n_items, 32, b->sl_smem, st>>>(P, Q);
+        cuda_check(cudaGetLastError(), "acopf_sl_kernel launch");
+        b->launches += 2;
+        if (b->n_res_items > 0) {
+            EvalParams R = P;
+            R.bus_items = static_cast<const DBusItem*>(b->d_res_items.p);
+            R.bus_recs = static_cast<const DRec*>(b->d_res_recs.p);
+            R.n_bus_items = b->n_res_items;
+            R.xi = nullptr;                   // direct gathers for the few leftover pairs
+            acopf_tile_kernel<ACOPF_ALL><<<R.n_bus_items, TILE_THREADS, b->smem, st>>>(R, 0);
+            cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
+            b->launches++;
+        }
+        return;
+    }
+    launch_interleave(b, P, 0, (int)b->stages.size(), st);
+    if (P.what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
+    else acopf_tile_kernel<0u><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
+    cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
+    b->launches++;
+}
+
 int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const double* mult, uint32_t what,
                      double* obj, double* grad, double* cons, double* jval, double* hval, void* stream) {
     return guard([&] {
@@ -811,13 +994,7 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
                 b->launches++;
             }
         }
-        if (bus) {
-            launch_interleave(b, P, 0, (int)b->stages.size(), st);
-            if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
-            else acopf_tile_kernel<0u><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
-            cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
-            b->launches++;
-        }
+        if (bus) launch_bus_work(b, P, st);
         if (fork) {
             cuda_check(cudaEventRecord(b->ev_join, b->aux_stream), "event record");
             cuda_check(cudaStreamWaitEvent(st, b->ev_join, 0), "stream wait");
@@ -1245,13 +1422,7 @@ int acopf_batch_eval_multi(acopf_multi* m, double* x, double obj_factor, const d
             }
             cuda_check(cudaEventRecord(m->ev_gen, b->aux_stream), "event record");
         }
-        if ((what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) && P.n_bus_items > 0) {
-            launch_interleave(b, P, 0, (int)b->stages.size(), st);
-            if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
-            else acopf_tile_kernel<0u><<<P.n_bus_items, TILE_THREADS, b->smem, st>>>(P, 0);
-            cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
-            b->launches++;
-        }
+        if ((what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) && P.n_bus_items > 0) launch_bus_work(b, P, st);
         if (halo) cuda_check(cudaStreamWaitEvent(st, m->ev_halo, 0), "stream wait");
         if (gen) cuda_check(cudaStreamWaitEvent(st, m->ev_gen, 0), "stream wait");
     });
