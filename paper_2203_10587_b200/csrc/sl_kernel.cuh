@@ -155,10 +155,26 @@ struct SLLane {
     }
 };
 
-template <int N>
-struct SLTerms {
-    double t[N];
+// One end's stage inputs (lane = stage): the far bus's (VA, VM, muP, muQ) and the
+// branch's flow-limit multipliers, read from the transposed copies.
+struct SLIn {
+    double va, vm, mp, mq, sf, st;
 };
+
+__device__ __forceinline__ void sl_load_end(const SLEnd& E, const double* xt, const double* mt, int lane, SLIn& in) {
+    const double* xf = xt + (long long)E.far * 128 + lane;
+    in.va = xf[0];
+    in.vm = xf[32];
+    in.mp = xf[64];
+    in.mq = xf[96];
+    in.sf = 0.0;
+    in.st = 0.0;
+    if (E.ridx >= 0) {
+        const double* m2 = mt + (long long)E.ridx * 64 + lane;
+        in.sf = m2[0];
+        in.st = m2[32];
+    }
+}
 
 __global__ void __launch_bounds__(32, 12) acopf_sl_kernel(const EvalParams P, const SLParams Q) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -168,8 +184,7 @@ __global__ void __launch_bounds__(32, 12) acopf_sl_kernel(const EvalParams P, co
     const SLGroup& G = Q.groups[it.group];
     const int st = G.stage[lane];
     unsigned char* tab[2] = {smem, smem + Q.table_max};
-    double* stage_area = reinterpret_cast<double*>(smem + 2 * Q.table_max);
-    double* A = stage_area + lane * Q.stride;
+    double* A = reinterpret_cast<double*>(smem + 2 * Q.table_max) + lane * Q.stride;
     const unsigned mb[2] = {smem_u32(&bars[0]), smem_u32(&bars[1])};
     if (lane == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb[0]));
@@ -178,15 +193,23 @@ __global__ void __launch_bounds__(32, 12) acopf_sl_kernel(const EvalParams P, co
     }
     __syncwarp();
     if (lane == 0) sl_table_load(mb[0], tab[0], Q.blob + Q.sl_blob_off[it.u0], Q.sl_bytes[it.u0]);
-    // this lane's stage
-    DStage S{};
-    if (st >= 0) S = P.stages[st];
+    // this lane's stage: only the fields the bus side needs
+    long long eq_row = 0, ineq_row = 0, jineq = 0, pd_off = 0, rem_off = 0;
+    int nrem = 0, snb = 0;
+    if (st >= 0) {
+        const DStage* S = P.stages + st;
+        eq_row = S->eq_row; ineq_row = S->ineq_row; jineq = S->jineq_base; pd_off = S->pd_off;
+        rem_off = S->rem_off; nrem = S->nrem; snb = S->nb;
+    }
     const long long* to = Q.tile_out + ((long long)it.group * Q.ntile_max + it.tile) * 128;
     const long long oP = to[lane], oQ = to[32 + lane], oA = to[64 + lane], oV = to[96 + lane];
     const bool on = st >= 0 && oP >= 0;
     const double* xt = Q.xt + G.xt_off;
     const double* mt = Q.mt + G.mt_off;
     const double* xg = Q.xg + G.xg_off;
+    const unsigned long long j8 = reinterpret_cast<uintptr_t>(P.jval) >> 3;
+    const unsigned long long h8 = reinterpret_cast<uintptr_t>(P.hval) >> 3;
+    const unsigned a8 = smem_u32(A) >> 3;
     double T[SL_MAXT];
     for (int u = it.u0; u < it.u1; ++u) {
         const int k = u - it.u0, buf = k & 1;
@@ -204,22 +227,26 @@ __global__ void __launch_bounds__(32, 12) acopf_sl_kernel(const EvalParams P, co
         const unsigned short* cpos = reinterpret_cast<const unsigned short*>(tb + H->o_const);
         const int* gl = reinterpret_cast<const int*>(tb + H->o_gen);
         const int* ro = Q.sl_run_off + 4 * u;
-        // this lane's output runs and their staging segments (16-byte parity matched)
         const int L0 = H->L[0], L1 = H->L[1], L2 = H->L[2], L3 = H->L[3];
         const long long d0 = oP + ro[0], d1 = oQ + ro[1], d2 = oA + ro[2], d3 = oV + ro[3];
-        // (segment s starts at slot s0..s3, plus one slot when the staging and the
-        // output run differ in 16-byte parity)
+        // this lane's staging segments: slot s0..s3, plus one slot when the staging and
+        // the output run differ in 16-byte parity (TMA bulk stores need equal parity)
         SLLane W;
         W.A = A;
         {
-            const unsigned a8 = smem_u32(A) >> 3;
             const int s0 = 0, s1 = L0 + 1, s2 = s1 + L1 + 1, s3 = s2 + L2 + 1;
-            const unsigned long long j8 = reinterpret_cast<uintptr_t>(P.jval) >> 3;
-            const unsigned long long h8 = reinterpret_cast<uintptr_t>(P.hval) >> 3;
             W.sb0 = s0 + (int)((j8 + d0 - a8 - s0) & 1);
             W.sb1 = s1 + (int)((j8 + d1 - a8 - s1) & 1);
             W.sb2 = s2 + (int)((h8 + d2 - a8 - s2) & 1);
             W.sb3 = s3 + (int)((h8 + d3 - a8 - s3) & 1);
+        }
+        // inputs of the first bus and end (the next ones are loaded one step ahead)
+        SLIn nx;
+        if (nE > 0) sl_load_end(en[0], xt, mt, lane, nx);
+        double own_va, own_vm, own_mp, own_mq;
+        {
+            const double* xb = xt + (long long)b0 * 128 + lane;
+            own_va = xb[0]; own_vm = xb[32]; own_mp = xb[64]; own_mq = xb[96];
         }
         // the staging is free once this lane's previous bulk stores have read it
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -227,18 +254,24 @@ __global__ void __launch_bounds__(32, 12) acopf_sl_kernel(const EvalParams P, co
         for (int bl = 0; bl < nB; ++bl) {
             const SLBus& B = bus[bl];
             const int ib = b0 + bl;
-            const double* xb = xt + (long long)ib * 128 + lane;
-            const double vai = xb[0], vmi = xb[32], mpi = xb[64], mqi = xb[96];
+            const double vai = own_va, vmi = own_vm, mpi = own_mp, mqi = own_mq;
+            if (bl + 1 < nB) {
+                const double* xb = xt + (long long)(ib + 1) * 128 + lane;
+                own_va = xb[0]; own_vm = xb[32]; own_mp = xb[64]; own_mq = xb[96];
+            }
+            const bool canon = B.canon;
             double pacc = 0.0, qacc = 0.0;
+            // streaming diagonal sums (np.add.at order; -0.0 is the exact additive identity)
+            double a0 = -0.0, a1 = -0.0, a2 = -0.0, a3 = -0.0, a4 = -0.0, a5 = -0.0, a6 = -0.0, a7 = -0.0;
             for (int e = B.end0; e < B.end0 + B.nend; ++e) {
                 const SLEnd E = en[e];
+                const SLIn cur = nx;
+                if (e + 1 < nE) sl_load_end(en[e + 1], xt, mt, lane, nx);
                 const bool sd = E.flags & 1;
-                const double* xf = xt + (long long)E.far * 128 + lane;
-                const double vaj = xf[0], vmj = xf[32], mpj = xf[64], mqj = xf[96];
-                const double vaf = sd ? vaj : vai, vat = sd ? vai : vaj;
-                const double vf = sd ? vmj : vmi, vt = sd ? vmi : vmj;
-                const double mpf = sd ? mpj : mpi, mqf = sd ? mqj : mqi;
-                const double mpt = sd ? mpi : mpj, mqt = sd ? mqi : mqj;
+                const double vaf = sd ? cur.va : vai, vat = sd ? vai : cur.va;
+                const double vf = sd ? cur.vm : vmi, vt = sd ? vmi : cur.vm;
+                const double mpf = sd ? cur.mp : mpi, mqf = sd ? cur.mq : mqi;
+                const double mpt = sd ? mpi : cur.mp, mqt = sd ? mqi : cur.mq;
                 const double gff = adm[e], bff = adm[nE + e], gft = adm[2 * nE + e], bft = adm[3 * nE + e];
                 const double gtf = adm[4 * nE + e], btf = adm[5 * nE + e], gtt = adm[6 * nE + e], btt = adm[7 * nE + e];
                 const double g2ff = gff + gff, m2bff = -(bff + bff), g2tt = gtt + gtt, m2btt = -(btt + btt);
@@ -263,46 +296,40 @@ __global__ void __launch_bounds__(32, 12) acopf_sl_kernel(const EvalParams P, co
                 const double gqt0 = (-vv) * u2, gqt2 = vt * w2, gqt3 = m2btt * vt + vf * w2;
                 const double gp0 = sd ? gpt0 : gpf0, gp2 = sd ? gpt2 : gpf2, gp3 = sd ? gpt3 : gpf3;
                 const double gq0 = sd ? gqt0 : gqf0, gq2 = sd ? gqt2 : gqf2, gq3 = sd ? gqt3 : gqf3;
-                double sfv = 0.0, stv = 0.0;
-                if (E.ridx >= 0) {
-                    const double* m2 = mt + (long long)E.ridx * 64 + lane;
-                    sfv = m2[0];
-                    stv = m2[32];
-                }
                 // flow-limit rows and |S|^2 (acopf.py:284-288, 302-307), direct per lane
                 if (E.ridx >= 0 && on) {
                     int rs = E.ridx;
                     long long fo = E.foff;
-                    for (int i = 0; i < S.nrem; ++i) {
-                        const int rr = __ldg(P.rem_ridx + S.rem_off + i);
-                        if (rr < E.ridx) { rs--; fo -= __ldg(P.rem_rowsz + S.rem_off + i); }
+                    for (int r = 0; r < nrem; ++r) {
+                        const int rr = __ldg(P.rem_ridx + rem_off + r);
+                        if (rr < E.ridx) { rs--; fo -= __ldg(P.rem_rowsz + rem_off + r); }
                     }
-                    P.cons[S.ineq_row + 2 * (long long)rs + (int)sd] = fp * fp + fq * fq;
+                    P.cons[ineq_row + 2 * (long long)rs + (int)sd] = fp * fp + fq * fq;
                     const double tp = 2.0 * fp, tq = 2.0 * fq;
                     const double r0 = (0.0 + tp * gp0) + tq * gq0, r1 = (0.0 + tp * (-gp0)) + tq * (-gq0);
                     const double r2 = (0.0 + tp * gp2) + tq * gq2, r3 = (0.0 + tp * gp3) + tq * gq3;
                     const bool loop = E.flags & 2;
-                    double* out = P.jval + S.jineq_base + fo + (loop ? 2 : 4) * (int)sd;
+                    double* out = P.jval + jineq + fo + (loop ? 2 : 4) * (int)sd;
                     if (!loop) {
                         const bool fl = sd ? (E.far < ib) : (ib < E.far);     // f < t
-                        const double a0 = fl ? r0 : r1, a1 = fl ? r1 : r0, a2 = fl ? r2 : r3, a3 = fl ? r3 : r2;
+                        const double c0 = fl ? r0 : r1, c1 = fl ? r1 : r0, c2 = fl ? r2 : r3, c3 = fl ? r3 : r2;
                         if ((reinterpret_cast<uintptr_t>(out) & 31) == 0) {
                             unsigned long long pol;
                             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
                             asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(out),
-                                         "d"(a0), "d"(a1), "d"(a2), "d"(a3), "l"(pol)
+                                         "d"(c0), "d"(c1), "d"(c2), "d"(c3), "l"(pol)
                                          : "memory");
                         } else if ((reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-                            reinterpret_cast<double2*>(out)[0] = make_double2(a0, a1);
-                            reinterpret_cast<double2*>(out)[1] = make_double2(a2, a3);
-                        } else { out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3; }
+                            reinterpret_cast<double2*>(out)[0] = make_double2(c0, c1);
+                            reinterpret_cast<double2*>(out)[1] = make_double2(c2, c3);
+                        } else { out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3; }
                     } else {
                         out[0] = r0 + r1;
                         out[1] = r2 + r3;
                     }
                 }
                 // Hessian positions (eval_kernel.cuh end_eval)
-                const double s2f = 2.0 * sfv, s2t = 2.0 * stv;
+                const double s2f = 2.0 * cur.sf, s2t = 2.0 * cur.st;
                 const double cpf = (-mpf) + s2f * pf, cqf = (-mqf) + s2f * qf;
                 const double cpt = (-mpt) + s2t * pt, cqt = (-mqt) + s2t * qt;
                 const double vvu = vv * u_, vvw = vv * w_, vvu2 = vv * u2, vvw2 = vv * w2;
@@ -315,12 +342,22 @@ __global__ void __launch_bounds__(32, 12) acopf_sl_kernel(const EvalParams P, co
                                        gqf0, gqf3, gpt0, gpt3, gqt0, gqt3);
                 const double v8 = hval(cpf, cqf, cpt, cqt, s2f, s2t, u_, w_, u2, w2, gpf2, gpf3, gqf2, gqf3, gpt2, gpt3,
                                        gqt2, gqt3);
-                const double a0 = sd ? gpf3 : gpf2, a1 = sd ? gqf3 : gqf2, a2 = sd ? gpt3 : gpt2, a3 = sd ? gqt3 : gqt2;
+                const double e0 = sd ? gpf3 : gpf2, e1 = sd ? gqf3 : gqf2, e2 = sd ? gpt3 : gpt2, e3 = sd ? gqt3 : gqt2;
                 const double v79 = hval(cpf, cqf, cpt, cqt, s2f, s2t, sd ? z : g2ff, sd ? z : m2bff, sd ? g2tt : z,
-                                        sd ? m2btt : z, a0, a0, a1, a1, a2, a2, a3, a3);
+                                        sd ? m2btt : z, e0, e0, e1, e1, e2, e2, e3, e3);
                 const double v5s = sd ? -v3 : v2;
                 const double vals[SL_NV] = {-gp0, gp0, -gp2, -gp3, -gq0, gq0, -gq2, -gq3,
                                             v0,   -v0, v3,   -v2,  v8,   v5s, v79,  v5s};
+                if (canon) {
+                    a0 = a0 + (sd ? gp0 : -gp0);
+                    a1 = a1 + (sd ? -gp3 : -gp2);
+                    a2 = a2 + (sd ? gq0 : -gq0);
+                    a3 = a3 + (sd ? -gq3 : -gq2);
+                    a4 = a4 + v0;
+                    a5 = a5 + v5s;
+                    a6 = a6 + v5s;
+                    a7 = a7 + v79;
+                }
 #pragma unroll
                 for (int q = 0; q < SL_NV; ++q) {
                     const unsigned d = dst[q * nE + e];
@@ -330,18 +367,25 @@ __global__ void __launch_bounds__(32, 12) acopf_sl_kernel(const EvalParams P, co
                 }
             }
             // the bus's own terms (acopf.py:262-263, 283, 296-297, 366)
-            {
-                const double gsb = B.gs, bsb = B.bs;
-                const double t0 = (-2.0 * gsb) * vmi, t1 = (2.0 * bsb) * vmi;
-                const double t2 = 2.0 * ((-mpi) * gsb - (-mqi) * bsb);
+            const double gsb = B.gs, bsb = B.bs;
+            const double t0 = (-2.0 * gsb) * vmi, t1 = (2.0 * bsb) * vmi;
+            const double t2 = 2.0 * ((-mpi) * gsb - (-mqi) * bsb);
+            pacc = pacc + (gsb * vmi) * vmi;
+            qacc = qacc + (-((bsb * vmi) * vmi));
+            if (canon) {
+                W.put(B.diag[0], a0);
+                W.put(B.diag[1], a1 + t0);
+                W.put(B.diag[2], a2);
+                W.put(B.diag[3], a3 + t1);
+                W.put(B.diag[4], a4);
+                W.put(B.diag[5], a5);
+                W.put(B.diag[6], a6);
+                W.put(B.diag[7], a7 + t2);
+            } else {
                 if (B.sh_jp != SL_NONE) { if (B.sh_jp & SL_T) T[B.sh_jp & 0x7fffu] = t0; else W.put(B.sh_jp, t0); }
                 if (B.sh_jq != SL_NONE) { if (B.sh_jq & SL_T) T[B.sh_jq & 0x7fffu] = t1; else W.put(B.sh_jq, t1); }
                 if (B.sh_h != SL_NONE) { if (B.sh_h & SL_T) T[B.sh_h & 0x7fffu] = t2; else W.put(B.sh_h, t2); }
-                pacc = pacc + (gsb * vmi) * vmi;
-                qacc = qacc + (-((bsb * vmi) * vmi));
-            }
-            // multi-term entries: scipy's duplicate order (planner.hpp canonicalise)
-            {
+                // multi-term entries: scipy's duplicate order (planner.hpp canonicalise)
                 const unsigned short* pr = prog + B.prog0;
                 for (int j = 0; j < B.nprog; ++j) {
                     const unsigned d = pr[0];
@@ -354,15 +398,15 @@ __global__ void __launch_bounds__(32, 12) acopf_sl_kernel(const EvalParams P, co
             }
             // balance rows: -(pd + p) + generators in order (acopf.py:277-283)
             if (on) {
-                const double pd = P.pd[S.pd_off + ib], qd = P.qd[S.pd_off + ib];
+                const double pd = P.pd[pd_off + ib], qd = P.qd[pd_off + ib];
                 double cP = -(pd + pacc), cQ = -(qd + qacc);
                 for (int j = B.gen0; j < B.gen0 + B.ngen; ++j) {
                     const double* gv = xg + (long long)gl[j] * 64 + lane;
                     cP = cP + gv[0];
                     cQ = cQ + gv[32];
                 }
-                P.cons[S.eq_row + ib] = cP;
-                P.cons[S.eq_row + S.nb + ib] = cQ;
+                P.cons[eq_row + ib] = cP;
+                P.cons[eq_row + snb + ib] = cQ;
             }
         }
         __syncwarp();

@@ -35,6 +35,10 @@ constexpr int SL_MAXT = 160;         // term-buffer slots per bus (a bus needing
 #endif
 constexpr int SL_MAX_BUSES = ACOPF_SL_BUSES;      // buses per SL tile
 constexpr int SL_MAX_ENDS = 16;      // branch ends per SL tile (soft: a single bus may exceed it)
+#ifndef ACOPF_SL_MAX_L
+#define ACOPF_SL_MAX_L 60
+#endif
+constexpr int SL_MAX_L = ACOPF_SL_MAX_L;   // staged doubles per lane (a bus needing more stays on the tile kernel)
 constexpr uint16_t SL_NONE = 0xffff;
 constexpr uint16_t SL_T = 0x8000;    // destination flag: term-buffer slot (else staging: seg << 13 | pos)
 
@@ -53,13 +57,26 @@ struct SLEnd {                       // 16 bytes
     int32_t flags;                   // bit 0: to-end; bit 1: self-loop (f == t)
 };
 
-struct SLBus {                       // 40 bytes
+struct SLBus {                       // 64 bytes
     double gs, bs;
     uint16_t end0, nend, prog0, nprog;   // ends [end0, end0 + nend); program entries
     uint16_t gen0, ngen, sh_jp, sh_jq;   // generators; shunt J (P, VM_i), (Q, VM_i) destinations
-    uint16_t sh_h, nT, pad0, pad1;       // shunt H (VM_i, VM_i) destination; term slots used
+    uint16_t sh_h, nT, canon, pad0;      // shunt H (VM_i, VM_i) destination; term slots used; streaming bus
+    uint16_t diag[8];                    // streaming bus: staging positions of its 8 diagonal entries
+    uint16_t pad1[4];
 };
-static_assert(sizeof(SLBus) == 40, "SLBus layout");
+static_assert(sizeof(SLBus) == 64, "SLBus layout");
+
+// Diagonal entries of a bus, in SLBus::diag order: J (P_i, VA_i), (P_i, VM_i),
+// (Q_i, VA_i), (Q_i, VM_i); H (VA_i, VA_i), (VA_i, VM_i), (VM_i, VA_i), (VM_i, VM_i).
+// sl_diag_q[k][side]: the end quantity each contributes; sl_diag_row / _vm: its row
+// (0..3 = P, Q, VA, VM) and whether its column is VM_i (else VA_i); the VM-column
+// entries of rows P, Q and VM end with the bus's shunt term.
+constexpr int sl_diag_q[8][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7},
+                                 {Q_H + 0, Q_H + 0}, {Q_H + 5, Q_H + 5}, {Q_H + 5, Q_H + 5}, {Q_H + 6, Q_H + 6}};
+constexpr int sl_diag_row[8] = {0, 0, 1, 1, 2, 2, 3, 3};
+constexpr int sl_diag_vm[8] = {0, 1, 0, 1, 0, 1, 0, 1};
+constexpr int sl_diag_shunt[8] = {-1, 0, -1, 1, -1, -1, -1, 2};      // bus quantity of the trailing shunt term
 
 struct SLTile {
     int old_tile = 0, c0 = 0, c1 = 0;  // buses [c0, c1) of planner tile old_tile (tile-local)
@@ -121,6 +138,43 @@ inline bool build_sl_tile(const Topo& T, const TileTable& tt, int old_tile, int 
         B.ngen = (uint16_t)(gens.size() - B.gen0);
         Row rows[4];
         build_bus_rows(T, i, Live{}, rows);
+        // streaming bus: its only multi-term entries are the 8 diagonal ones, each summing
+        // the bus's ends in np.add.at order (one term each, the quantity sl_diag_q names)
+        // and, for the VM columns of rows P, Q and VM, the shunt term last -- then the kernel
+        // accumulates them in registers as the ends are evaluated
+        bool canon = B.nend > 0;
+        int diag_pos[8];
+        for (int s = 0; s < 4 && canon; ++s) {
+            int pos = 0;
+            for (int r = c0; r < c0 + bl; ++r) pos += tt.rowlen[s * nB + r];
+            const Row& row = rows[s];
+            for (size_t c = 0; c < row.cols.size() && canon; ++c, ++pos) {
+                const int t0 = row.tptr[c], t1 = row.tptr[c + 1];
+                const int col = row.cols[c];
+                int k = -1;
+                for (int d = 0; d < 8; ++d)
+                    if (sl_diag_row[d] == s && col == (sl_diag_vm[d] ? T.nb + i : i)) k = d;
+                if (k < 0) {
+                    if (t1 - t0 != 1) canon = false;
+                    continue;
+                }
+                const int want = B.nend + (sl_diag_shunt[k] >= 0 ? 1 : 0);
+                if (t1 - t0 != want) { canon = false; continue; }
+                for (int j = 0; j < B.nend && canon; ++j) {
+                    const Sym& y = row.terms[t0 + j];
+                    const int ek = ends[bus_end0[bl] + j];
+                    canon = y.kind == 0 && y.a == ek && y.q == sl_diag_q[k][ek & 1];
+                }
+                if (canon && sl_diag_shunt[k] >= 0) {
+                    const Sym& y = row.terms[t1 - 1];
+                    canon = y.kind == 1 && y.q == sl_diag_shunt[k];
+                }
+                diag_pos[k] = (s << 13) | pos;
+            }
+        }
+        B.canon = canon ? 1 : 0;
+        if (canon)
+            for (int d = 0; d < 8; ++d) B.diag[d] = (uint16_t)diag_pos[d];
         int nT = 0, nprog = 0;
         for (int s = 0; s < 4; ++s) {
             // position of this bus's row inside the chunk's run s
@@ -149,6 +203,7 @@ inline bool build_sl_tile(const Topo& T, const TileTable& tt, int old_tile, int 
                         cpos.push_back(d);
                     }
                 };
+                if (canon && (row.cols[c] == i || row.cols[c] == T.nb + i)) continue;   // accumulated in registers
                 if (t1 - t0 == 1) {
                     use_of(row.terms[t0], stg);
                     continue;
@@ -167,6 +222,7 @@ inline bool build_sl_tile(const Topo& T, const TileTable& tt, int old_tile, int 
         B.nprog = (uint16_t)nprog;
         B.nT = (uint16_t)nT;
     }
+    if (out.L[0] + out.L[1] + out.L[2] + out.L[3] > SL_MAX_L) return false;
     // serialise
     SLHdr h{};
     h.b0 = b0;
@@ -216,10 +272,14 @@ inline bool build_sl_tiles(const Topo& T, const TileTable& tt, int tile, std::ve
     int c = 0;
     while (c < tt.nB) {
         int c1 = c, ne = 0;
+        int nl = 0;
         while (c1 < tt.nB) {
             const int d = tt.busptr[c1 + 1] - tt.busptr[c1];
-            if (c1 > c && (c1 - c >= SL_MAX_BUSES || ne + d > SL_MAX_ENDS)) break;
+            int l = 0;
+            for (int s = 0; s < 4; ++s) l += tt.rowlen[s * tt.nB + c1];
+            if (c1 > c && (c1 - c >= SL_MAX_BUSES || ne + d > SL_MAX_ENDS || nl + l > SL_MAX_L)) break;
             ne += d;
+            nl += l;
             ++c1;
         }
         SLTile st;
