@@ -371,8 +371,10 @@ static void upload(acopf_batch* b) {
     std::vector<DBusItem> res_items;
     std::vector<DRec> res_recs;
     {
-        const char* sle = getenv("ACOPF_SL");          // 0: tile kernel only (development aid / comparisons)
-        if (!sle || atoi(sle) != 0) {
+        // ACOPF_SL=1 enables the stage-lane path (measured slower than the tile kernel on
+        // every configuration so far; kept behind the switch with its tests)
+        const char* sle = getenv("ACOPF_SL");
+        if (sle && atoi(sle) != 0) {
             int ntmax = 0;
             for (size_t ti = 0; ti < b->topos.size(); ++ti) ntmax = std::max(ntmax, (int)b->base_table[ti].size());
             if (b->sl_tiles.empty() || b->sl_ntile_max != ntmax) {

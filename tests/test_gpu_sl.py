@@ -20,6 +20,12 @@ from paper_2203_10587_b200.types import CouplingMode
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _sl_on(monkeypatch):
+    """The stage-lane path is opt-in (ACOPF_SL=1, read when a batch is first uploaded)."""
+    monkeypatch.setenv("ACOPF_SL", "1")
+
+
 def _per_callback(ev, x, mult, of):
     """The five outputs from five single-callback evaluations (tile kernel only)."""
     out = {}
