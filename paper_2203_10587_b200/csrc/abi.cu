@@ -142,10 +142,14 @@ struct acopf_batch {
     // host-buffer pipeline (independent layouts): chunks of whole stage groups
     struct Pipe { int s0, s1, bus_first, bus_count, aux_first, aux_count; };
     std::vector<Pipe> pipe;
+    std::vector<Pipe> il_chunks;     // device evaluation with interleaved inputs: chunks whose pre-pass
+                                     // overlaps the previous chunk's tile kernel (two streams)
     cudaStream_t pipe_streams[3] = {nullptr, nullptr, nullptr};
     cudaStream_t aux_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_il = nullptr, ev_ilj[2] = {nullptr, nullptr};
     ~acopf_batch() {
+        for (cudaEvent_t e : {ev_il, ev_ilj[0], ev_ilj[1]}) if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
         if (aux_stream) cudaStreamDestroy(aux_stream);
         for (auto& ps : pipe_streams) if (ps) cudaStreamDestroy(ps);
@@ -225,6 +229,8 @@ static void upload(acopf_batch* b) {
     if (!b->aux_stream) cuda_check(cudaStreamCreateWithFlags(&b->aux_stream, cudaStreamNonBlocking), "stream");
     if (!b->ev_fork) cuda_check(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming), "event");
     if (!b->ev_join) cuda_check(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming), "event");
+    for (cudaEvent_t* e : {&b->ev_il, &b->ev_ilj[0], &b->ev_ilj[1]})
+        if (!*e) cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
 
     // topologies (only what the aux kernel needs; the bus kernel reads tile tables)
     std::vector<DTopo> dt;
@@ -552,6 +558,36 @@ static void upload(acopf_batch* b) {
         }
         for (auto& ps : b->pipe_streams)
             if (!ps) cuda_check(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking), "stream");
+    }
+    // interleave overlap: when the interleaved inputs exceed L2 (cfg4: 0.8 GB), the
+    // pre-pass of stage chunk c + 1 runs beside the tile kernel of chunk c
+    b->il_chunks.clear();
+    {
+        int64_t il_bytes = 0;
+        int nbmax = 0;
+        for (const StageInfo& st : b->stages) nbmax = std::max(nbmax, b->topos[st.topo]->nb);
+        for (const StageInfo& st : b->stages) il_bytes += 32LL * b->topos[st.topo]->nb;
+        const char* ie = getenv("ACOPF_INTERLEAVE");
+        const bool il = ie ? atoi(ie) != 0 : nbmax >= INTERLEAVE_MIN_BUSES;
+        const char* ce = getenv("ACOPF_IL_CHUNKS");                // development aid
+        const int nch = ce ? std::max(1, atoi(ce)) : 4;
+        if (il && il_bytes > 256LL * 1048576 && nch > 1) {
+            const int ngroups = (S + G - 1) / G;
+            const int per = std::max(1, (ngroups + nch - 1) / nch);
+            int item = 0;
+            for (int g0 = 0; g0 < ngroups; g0 += per) {
+                acopf_batch::Pipe pc{};
+                pc.s0 = g0 * G;
+                pc.s1 = std::min(S, (g0 + per) * G);
+                pc.bus_first = item;
+                while (item < (int)items.size() && recs[items[item].first].stage < pc.s1) ++item;
+                pc.bus_count = item - pc.bus_first;
+                b->il_chunks.push_back(pc);
+            }
+            if (item != (int)items.size()) b->il_chunks.clear();      // items not stage-group-major: no chunks
+            for (auto& ps : b->pipe_streams)
+                if (!ps) cuda_check(cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking), "stream");
+        }
     }
     // coupling rows as runs (row, J position, child and base columns advancing
     // together), packed into items of at most CP_CHUNK rows
@@ -950,6 +986,28 @@ static void launch_bus_work(acopf_batch* b, const EvalParams& P, cudaStream_t st
             acopf_tile_kernel<ACOPF_ALL><<<R.n_bus_items, TILE_THREADS, b->smem, st>>>(R, 0);
             cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
             b->launches++;
+        }
+        return;
+    }
+    if (P.xi && b->il_chunks.size() > 1) {
+        // chunk c on stream c % 2: its interleave pre-pass, then its tile kernel; the
+        // pre-pass of chunk c + 1 (HBM streaming) overlaps chunk c's tile kernel (L1-bound)
+        cuda_check(cudaEventRecord(b->ev_il, st), "event record");
+        for (int k = 0; k < 2; ++k) cuda_check(cudaStreamWaitEvent(b->pipe_streams[k], b->ev_il, 0), "stream wait");
+        for (size_t c = 0; c < b->il_chunks.size(); ++c) {
+            const auto& pc = b->il_chunks[c];
+            cudaStream_t cs = b->pipe_streams[c & 1];
+            launch_interleave(b, P, pc.s0, pc.s1, cs);
+            if (pc.bus_count == 0) continue;
+            if (P.what == ACOPF_ALL)
+                acopf_tile_kernel<ACOPF_ALL><<<pc.bus_count, TILE_THREADS, b->smem, cs>>>(P, pc.bus_first);
+            else acopf_tile_kernel<0u><<<pc.bus_count, TILE_THREADS, b->smem, cs>>>(P, pc.bus_first);
+            cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
+            b->launches++;
+        }
+        for (int k = 0; k < 2; ++k) {
+            cuda_check(cudaEventRecord(b->ev_ilj[k], b->pipe_streams[k]), "event record");
+            cuda_check(cudaStreamWaitEvent(st, b->ev_ilj[k], 0), "stream wait");
         }
         return;
     }

@@ -215,7 +215,7 @@ struct EndIn {
 // its bus's loads and its generator's set-points with cp.async into its
 // column of the gather buffer (G[q * TILE_THREADS + tid]).
 __device__ __forceinline__ void prefetch(const EvalParams& P, const DRec& R, const TileView& V, int e, int gi,
-                                         unsigned sG, bool need_h, bool need_c, EndIn& in) {
+                                         unsigned sG, bool need_h, bool need_c, bool loads, EndIn& in) {
     const int nE = V.H->nE;
     const double* x = opaque(P.x + R.var_off);
     const unsigned st = 8u * TILE_THREADS;
@@ -227,7 +227,7 @@ __device__ __forceinline__ void prefetch(const EvalParams& P, const DRec& R, con
     }
     if (e >= nE) return;
     const int rb = V.rep[e];
-    if (need_c && rb >= 0) {
+    if (need_c && loads && rb >= 0) {          // (a stage with the previous stage's load set reuses them)
         const int i = V.H->b0 + rb;
         cp_async8s(sG, P.pd + R.pd_off + i);
         cp_async8s(sG + st, P.qd + R.pd_off + i);
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
     mbar_wait(rb_, 0);
     __syncthreads();
     EndIn pre;
-    prefetch(P, ctx[0], V, my_e, tid, sG, need_h, need_c, pre);
+    prefetch(P, ctx[0], V, my_e, tid, sG, need_h, need_c, true, pre);
     cp_commit();
 
     for (int ri = 0; ri < it.count; ++ri) {
@@ -675,7 +675,8 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         __syncthreads();
         // the gather buffer is free again: prefetch the next stage's inputs
 #ifndef ACOPF_DIAG_NO_PF
-        if (more) prefetch(P, ctx[(ri + 1) & 1], V, my_e, tid, sG, need_h, need_c, pre);
+        if (more) prefetch(P, ctx[(ri + 1) & 1], V, my_e, tid, sG, need_h, need_c, ctx[(ri + 1) & 1].pd_off != R.pd_off,
+                           pre);
 #endif
         cp_commit();
         // ---- B: balance rounds, next gathers, sum rounds -------------------------
