@@ -353,6 +353,46 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def callback_latency(device: int, calls: int = 20) -> dict:
+    """Per-callback latency of the drop-in NlpProblem on the config-1 network (batch = 1, the
+    way the reference's IPM calls it, ipm.py:389-578): pageable numpy in, fresh numpy / scipy
+    CSR out, host wall time per call (median of `calls`), next to the oracle port's (1 core)."""
+    from paper_2203_10587_b200 import build_acopf, synthetic as syn
+    from oracle.stage import StageOracle
+    case = syn.config_case(1)
+    p, _ = build_acopf(case, device=device)
+    o = StageOracle(case)
+    kinds = syn.variable_kinds([(o.nb, o.ng)])
+    x, mult = syn.random_point(kinds, p.xl, p.xu, p.m_eq + p.m_ineq, 4242)
+    calls_of = lambda q: dict(objective=lambda: q.objective(x), gradient=lambda: q.gradient(x),
+                              constraints=lambda: q.constraints(x), jacobian=lambda: q.jacobian(x),
+                              lagrangian_hessian=lambda: q.lagrangian_hessian(x, 1.0, mult))
+    out = {}
+    for name, fn in calls_of(p).items():
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(calls):
+            t = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t)
+        out[name + "_ms"] = 1000 * statistics.median(ts)
+    ref = {}
+    for name, fn in calls_of(o).items():
+        fn()
+        ts = []
+        for _ in range(3):
+            t = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t)
+        ref[name + "_ms"] = 1000 * min(ts)
+    out["all_five_ms"] = sum(v for k, v in out.items() if k.endswith("_ms"))
+    out["reference_port_1core_ms"] = ref
+    out["path"] = ("paper_2203_10587_b200.build_acopf(cfg1 network) NlpProblem callbacks; pageable numpy in, "
+                   f"new numpy / scipy CSR out; host wall time, median of {calls} calls per callback")
+    return out
+
+
 def workload_config(cfg: int) -> dict:
     """The `config` object of both arms (identical for the same workload)."""
     d = workload_desc(cfg, 0)
@@ -504,6 +544,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_single(args.config)
+    cbl = None
+    if rank == 0 and not args.no_e2e:
+        cbl = callback_latency(local)
 
     if rank == 0:
         cfg = workload_config(args.config)
@@ -529,6 +572,7 @@ def main():
                          "kernel_ms": kernel_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_callbacks": cbl,
             "gpu_launches": int(gpu_launches),
             "clocks": clk.summary(),
         }
