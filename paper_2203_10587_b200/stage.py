@@ -33,13 +33,21 @@ def csr_index_arrays(indptr: np.ndarray, indices: np.ndarray):
 
 
 class CallbackSet:
-    """The five NlpProblem callbacks over one BatchEvaluator (host buffers)."""
+    """The five NlpProblem callbacks over one BatchEvaluator (host buffers).
+
+    Latency path (the reference's IPM calls one callback at a time, ipm.py:389-578): the
+    point is copied into a persistent pinned buffer, every output is written by an
+    asynchronous D2H copy straight into a FRESH pinned array from torch's caching host
+    allocator (so each call returns new arrays the caller owns, as the reference does,
+    without a pageable copy), and the C ABI call itself is one ctypes call
+    (acopf_batch_eval_host: H2D, the requested kernels only, D2H, synchronise)."""
 
     def __init__(self, ev: BatchEvaluator, obj_index: int = 0):
         self.ev = ev
         self._lock = threading.Lock()
         self._jp = self._hp = None
         self.obj_index = obj_index
+        self._pin_x = self._pin_m = None
 
     def _patterns(self, which):
         if which == "J":
@@ -50,27 +58,60 @@ class CallbackSet:
             self._hp = csr_index_arrays(*self.ev.pattern("H"))
         return self._hp
 
+    @staticmethod
+    def _pinned(n):
+        import torch
+        return torch.empty(max(int(n), 1), dtype=torch.float64, pin_memory=True)
+
     def _eval(self, x, mult, of, what):
+        """One evaluation of `what` (a single output) into a fresh pinned array."""
+        import ctypes
+        ev = self.ev
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape != (ev.n,):
+            raise ValueError(f"x must have shape ({ev.n},)")
         with self._lock:
-            return self.ev.eval_host(np.asarray(x, dtype=np.float64), mult, of, what)
+            if self._pin_x is None:
+                self._pin_x = self._pinned(ev.n)
+                self._pin_m = self._pinned(ev.m)
+            px = self._pin_x.numpy()[:ev.n]
+            np.copyto(px, x)
+            pm = 0
+            if mult is not None:
+                mult = np.asarray(mult, dtype=np.float64)
+                if mult.shape != (ev.m,):
+                    raise ValueError(f"mult must have shape ({ev.m},)")
+                np.copyto(self._pin_m.numpy()[:ev.m], mult)
+                pm = self._pin_m.data_ptr()
+            size = {L.OBJ: ev.n_obj, L.GRAD: ev.n, L.CONS: ev.m, L.JAC: ev.nnz_j, L.HESS: ev.nnz_h}[what]
+            out = self._pinned(size)
+            ptrs = [None] * 5
+            ptrs[{L.OBJ: 0, L.GRAD: 1, L.CONS: 2, L.JAC: 3, L.HESS: 4}[what]] = out
+            v = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
+            nn = lambda t: 0 if t is None else size
+            L.check(L.lib().acopf_batch_eval_host(
+                ev._h, ctypes.c_void_p(self._pin_x.data_ptr()), ev.n, float(of), ctypes.c_void_p(pm or None),
+                ev.m if pm else 0, int(what), v(ptrs[0]), nn(ptrs[0]), v(ptrs[1]), nn(ptrs[1]), v(ptrs[2]),
+                nn(ptrs[2]), v(ptrs[3]), nn(ptrs[3]), v(ptrs[4]), nn(ptrs[4]), None))
+            return out.numpy()[:size]
 
     def objective(self, x) -> float:
-        return float(self._eval(x, None, 1.0, L.OBJ)["obj"][self.obj_index])
+        return float(self._eval(x, None, 1.0, L.OBJ)[self.obj_index])
 
     def gradient(self, x) -> np.ndarray:
-        return self._eval(x, None, 1.0, L.GRAD)["grad"]
+        return self._eval(x, None, 1.0, L.GRAD)
 
     def constraints(self, x) -> np.ndarray:
-        return self._eval(x, None, 1.0, L.CONS)["cons"]
+        return self._eval(x, None, 1.0, L.CONS)
 
     def jacobian(self, x) -> sp.csr_matrix:
-        vals = self._eval(x, None, 1.0, L.JAC)["jac"]
+        vals = self._eval(x, None, 1.0, L.JAC)
         indptr, indices = self._patterns("J")
         return sp.csr_matrix((vals, indices.copy(), indptr.copy()), shape=(self.ev.m, self.ev.n))
 
     def lagrangian_hessian(self, x, obj_factor, mult) -> sp.csr_matrix:
         mult = np.asarray(mult, dtype=np.float64)
-        vals = self._eval(x, mult, float(obj_factor), L.HESS)["hess"]
+        vals = self._eval(x, mult, float(obj_factor), L.HESS)
         indptr, indices = self._patterns("H")
         return sp.csr_matrix((vals, indices.copy(), indptr.copy()), shape=(self.ev.n, self.ev.n))
 
