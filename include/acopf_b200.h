@@ -181,6 +181,21 @@ int acopf_multi_destroy(acopf_multi* m);
 int acopf_batch_eval_multi(acopf_multi* m, double* x, double obj_factor, const double* mult, uint32_t what,
                            double* obj, double* grad, double* cons, double* jval, double* hval, void* stream);
 
+/* Host graph utilities of the composite builder (network.py:232-262, 339-344):
+ * islands of the in-service network over buses with alive[v] != 0 (edges with an
+ * endpoint not alive are ignored; edge_live may be NULL = all), labels in the
+ * order of their first bus, -1 for buses not alive; and the bridges of the live
+ * multigraph (a parallel twin is not a bridge), is_bridge[k] per edge. */
+int acopf_graph_islands(int32_t nbus, const uint8_t* alive, int64_t nedge, const int32_t* ea, const int32_t* eb,
+                        const uint8_t* edge_live, int32_t* n_islands, int32_t* label);
+int acopf_graph_bridges(int32_t nbus, int64_t nedge, const int32_t* ea, const int32_t* eb, const uint8_t* edge_live,
+                        uint8_t* is_bridge);
+
+/* Host utility of the composite builder: dst[dst_off[i] ..+ len[i]) = src[src_off[i] ..+ len[i])
+ * for i < n, on the host cores (the per-stage bound blocks of composer.py:244-251). */
+int acopf_copy_runs(int64_t n, double* dst, const int64_t* dst_off, const double* src, const int64_t* src_off,
+                    const int64_t* len);
+
 /* MATPOWER text of one matrix section of a solved stage (the reference's
  * matpower._fmt_matrix, matpower.py:151-157): "mpc.<section> = [", one line
  * per row ("\t" + the row's values as "%.10g" joined by "\t" + ";"), "];",

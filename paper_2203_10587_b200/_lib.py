@@ -57,6 +57,10 @@ _SIGNATURES = {
     "acopf_multi_destroy": (c_int32, [c_void_p]),
     "acopf_batch_eval_multi": (c_int32, [c_void_p, c_void_p, c_double, c_void_p, c_uint32, c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_void_p, c_void_p]),
+    "acopf_graph_islands": (c_int32, [c_int32, POINTER(c_uint8), c_int64, _i32p, _i32p, POINTER(c_uint8),
+                                      _i32p, _i32p]),
+    "acopf_graph_bridges": (c_int32, [c_int32, c_int64, _i32p, _i32p, POINTER(c_uint8), POINTER(c_uint8)]),
+    "acopf_copy_runs": (c_int32, [c_int64, _f64p, _i64p, _f64p, _i64p, _i64p]),
     "acopf_format_matrix": (c_int32, [c_char_p, c_int64, _i64p, _f64p, c_void_p, c_int64, _i64p]),
 }
 

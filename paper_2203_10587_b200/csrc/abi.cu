@@ -1488,6 +1488,122 @@ int acopf_batch_eval_multi(acopf_multi* m, double* x, double obj_factor, const d
     });
 }
 
+int acopf_graph_islands(int32_t nbus, const uint8_t* alive, int64_t nedge, const int32_t* ea, const int32_t* eb,
+                        const uint8_t* edge_live, int32_t* n_islands, int32_t* label) {
+    return guard([&] {
+        std::vector<int32_t> parent(nbus);
+        std::iota(parent.begin(), parent.end(), 0);
+        auto find = [&](int32_t v) {
+            while (parent[v] != v) { parent[v] = parent[parent[v]]; v = parent[v]; }
+            return v;
+        };
+        for (int64_t k = 0; k < nedge; ++k) {
+            if (edge_live && !edge_live[k]) continue;
+            const int32_t a = ea[k], b = eb[k];
+            if (a < 0 || a >= nbus || b < 0 || b >= nbus) throw std::runtime_error("edge endpoint out of range");
+            if (!alive[a] || !alive[b]) continue;
+            const int32_t ra = find(a), rb = find(b);
+            if (ra != rb) parent[std::max(ra, rb)] = std::min(ra, rb);
+        }
+        // labels in order of first bus (the order of check_connectivity's DFS roots)
+        std::vector<int32_t> lab(nbus, -1);
+        int32_t count = 0;
+        for (int32_t v = 0; v < nbus; ++v) {
+            if (!alive[v]) continue;
+            const int32_t r = find(v);
+            if (lab[r] < 0) lab[r] = count++;
+            if (label) label[v] = lab[r];
+        }
+        if (label)
+            for (int32_t v = 0; v < nbus; ++v) if (!alive[v]) label[v] = -1;
+        *n_islands = count;
+    });
+}
+
+int acopf_graph_bridges(int32_t nbus, int64_t nedge, const int32_t* ea, const int32_t* eb, const uint8_t* edge_live,
+                        uint8_t* is_bridge) {
+    return guard([&] {
+        // iterative Tarjan over the live multigraph: a parallel twin is a back edge
+        std::vector<int64_t> ptr(nbus + 1, 0), adj_e;
+        std::vector<int32_t> adj_v;
+        for (int64_t k = 0; k < nedge; ++k) {
+            is_bridge[k] = 0;
+            if (edge_live && !edge_live[k]) continue;
+            if (ea[k] < 0 || ea[k] >= nbus || eb[k] < 0 || eb[k] >= nbus) throw std::runtime_error("edge endpoint out of range");
+            ptr[ea[k] + 1]++;
+            ptr[eb[k] + 1]++;
+        }
+        for (int32_t v = 0; v < nbus; ++v) ptr[v + 1] += ptr[v];
+        adj_e.resize(ptr[nbus]);
+        adj_v.resize(ptr[nbus]);
+        std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+        for (int64_t k = 0; k < nedge; ++k) {
+            if (edge_live && !edge_live[k]) continue;
+            adj_v[fill[ea[k]]] = eb[k]; adj_e[fill[ea[k]]++] = k;
+            adj_v[fill[eb[k]]] = ea[k]; adj_e[fill[eb[k]]++] = k;
+        }
+        std::vector<int32_t> disc(nbus, -1), low(nbus, 0);
+        std::vector<int64_t> it(nbus, 0), via(nbus, -1);
+        std::vector<int32_t> stack;
+        int32_t t = 0;
+        for (int32_t root = 0; root < nbus; ++root) {
+            if (disc[root] >= 0 || ptr[root] == ptr[root + 1]) continue;
+            disc[root] = low[root] = t++;
+            it[root] = ptr[root];
+            via[root] = -1;
+            stack.push_back(root);
+            while (!stack.empty()) {
+                const int32_t u = stack.back();
+                bool pushed = false;
+                while (it[u] < ptr[u + 1]) {
+                    const int64_t j = it[u]++;
+                    const int32_t v = adj_v[j];
+                    const int64_t k = adj_e[j];
+                    if (k == via[u]) continue;
+                    if (disc[v] < 0) {
+                        disc[v] = low[v] = t++;
+                        it[v] = ptr[v];
+                        via[v] = k;
+                        stack.push_back(v);
+                        pushed = true;
+                        break;
+                    }
+                    low[u] = std::min(low[u], disc[v]);
+                }
+                if (pushed) continue;
+                stack.pop_back();
+                if (!stack.empty()) {
+                    const int32_t p = stack.back();
+                    low[p] = std::min(low[p], low[u]);
+                    if (low[u] > disc[p]) is_bridge[via[u]] = 1;
+                }
+            }
+        }
+    });
+}
+
+int acopf_copy_runs(int64_t n, double* dst, const int64_t* dst_off, const double* src, const int64_t* src_off,
+                    const int64_t* len) {
+    return guard([&] {
+        int64_t total = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            if (len[i] < 0 || dst_off[i] < 0 || src_off[i] < 0) throw std::runtime_error("negative run");
+            total += len[i];
+        }
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const int nt = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)hw, 16, total / (1 << 20) + 1}));
+        std::atomic<int64_t> next{0};
+        auto work = [&] {
+            for (int64_t i; (i = next.fetch_add(1)) < n;)
+                if (len[i]) std::memcpy(dst + dst_off[i], src + src_off[i], sizeof(double) * (size_t)len[i]);
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+        work();
+        for (auto& th : pool) th.join();
+    });
+}
+
 int acopf_format_matrix(const char* section, int64_t rows, const int64_t* row_ptr, const double* values,
                         char* out, int64_t cap, int64_t* len) {
     return guard([&] {

@@ -179,10 +179,9 @@ class BatchEvaluator:
             rows = L.i64(cp.row)
             # J position of a coupling row: pins follow the eq blocks, boxes the ineq blocks
             me_st = int(meq.sum())
-            jpos = np.where(rows < self.m_eq,
-                            int(jeq.sum()) + 2 * (rows - me_st),
-                            int(jeq.sum()) + 2 * n_pins + int(jin.sum()) + 2 * (rows - self.m_eq - int(mineq.sum())))
-            jpos = L.i64(jpos)
+            jpos = 2 * rows
+            jpos += np.where(rows < self.m_eq, int(jeq.sum()) - 2 * me_st,
+                             int(jeq.sum()) + 2 * n_pins + int(jin.sum()) - 2 * (self.m_eq + int(mineq.sum())))
             ca, cb = L.i64(cp.col_a), L.i64(cp.col_b)
             first = np.ascontiguousarray(cb < ca if cp.base_first is None else cp.base_first, dtype=np.int8)
         else:

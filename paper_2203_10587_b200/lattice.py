@@ -28,8 +28,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import EmptyScenarioSet, InvalidPlan, IslandingDetected, TopologyMismatch
+from . import _lib as L
 from .evaluator import BatchEvaluator, Coupling, StagePlan
-from .grid import REF, apply_contingency, apply_scenario, check_connectivity, resolve_outages, scenario_targets
+from .grid import ISOLATED, REF, apply_contingency, apply_scenario, check_connectivity, resolve_outages, scenario_targets
 from .packer import PackedCase, Topology
 from .stage import CallbackSet
 from .types import (
@@ -96,44 +97,31 @@ def _check_topology(ref, other) -> None:
 
 
 def _bridges(pc: PackedCase) -> set:
-    """Case positions of live branches whose outage islands the network."""
-    nbus = len(pc.bus_id)
-    adj: list = [[] for _ in range(nbus)]
-    for k in pc.live_br:
-        a, b = int(pc.br_f[k]), int(pc.br_t[k])
-        adj[a].append((b, int(k)))
-        adj[b].append((a, int(k)))
-    disc = [-1] * nbus
-    low = [0] * nbus
-    out = set()
-    t = 0
-    for root in range(nbus):
-        if disc[root] >= 0 or not adj[root]:
-            continue
-        disc[root] = low[root] = t
-        t += 1
-        stack = [(root, -1, iter(adj[root]))]
-        while stack:
-            u, via, it = stack[-1]
-            pushed = False
-            for v, k in it:
-                if k == via:
-                    continue
-                if disc[v] < 0:
-                    disc[v] = low[v] = t
-                    t += 1
-                    stack.append((v, k, iter(adj[v])))
-                    pushed = True
-                    break
-                low[u] = min(low[u], disc[v])
-            if not pushed:
-                stack.pop()
-                if stack:
-                    p = stack[-1][0]
-                    low[p] = min(low[p], low[u])
-                    if low[u] > disc[p]:
-                        out.add(via)
-    return out
+    """Case positions of live branches whose outage islands the network (native Tarjan,
+    acopf_graph_bridges, over the live multigraph)."""
+    import ctypes
+    ea = L.i32(pc.br_f[pc.live_br])
+    eb = L.i32(pc.br_t[pc.live_br])
+    out = np.zeros(max(len(ea), 1), dtype=np.uint8)
+    if len(ea):
+        L.check(L.lib().acopf_graph_bridges(len(pc.bus_id), len(ea), L.ptr(ea, ctypes.c_int32),
+                                            L.ptr(eb, ctypes.c_int32), None, L.ptr(out, ctypes.c_uint8)))
+    return set(int(k) for k in np.asarray(pc.live_br)[out[:len(ea)].astype(bool)])
+
+
+def _islands_without(pc: PackedCase, removed_case_branches) -> int:
+    """Island count of the in-service network minus some branches (check_connectivity, native)."""
+    import ctypes
+    live = np.asarray(pc.live_br)
+    keep = ~np.isin(live, np.asarray(removed_case_branches, dtype=np.int64))
+    ea, eb = L.i32(pc.br_f[live]), L.i32(pc.br_t[live])
+    el = np.ascontiguousarray(keep, dtype=np.uint8)
+    alive = np.ascontiguousarray(pc.btype != ISOLATED, dtype=np.uint8)
+    n = ctypes.c_int32()
+    L.check(L.lib().acopf_graph_islands(len(alive), L.ptr(alive, ctypes.c_uint8), len(ea), L.ptr(ea, ctypes.c_int32),
+                                        L.ptr(eb, ctypes.c_int32), L.ptr(el, ctypes.c_uint8) if len(el) else None,
+                                        ctypes.byref(n), None))
+    return int(n.value)
 
 
 @dataclass
@@ -202,8 +190,9 @@ class _Lattice:
             if int(case_branches[0]) in self._bridges[rep]:
                 raise IslandingDetected(f"contingency {ctg.id} splits the network into 2 islands")
             return
-        out = apply_contingency(self.periods[rep], ctg)   # raises IslandingDetected
-        del out
+        n = _islands_without(self.pcs[rep], case_branches)      # one native check per contingency
+        if n != 1:
+            raise IslandingDetected(f"contingency {ctg.id} splits the network into {n} islands")
 
     def add_stage(self, s_pos, c_pos, t, scen, ctg, weight, targets, outages) -> int:
         rep = self.period_topo[t]
@@ -269,10 +258,16 @@ class _Lattice:
         n_s = np.array([s.topo.n for s in st], dtype=np.int64)
         meq_s = np.array([2 * s.topo.nb for s in st], dtype=np.int64)
         rated_live = []
+        rated_mask = {}                # topology -> per local branch: 1 when rated
         for s in st:
-            keep = np.ones(s.topo.nbr, dtype=bool)
-            keep[s.removed.astype(np.int64)] = False
-            rated_live.append(int(np.count_nonzero(keep[s.topo.rated_pos])))
+            key = id(s.topo)
+            if key not in rated_mask:
+                m = np.zeros(s.topo.nbr, dtype=bool)
+                m[s.topo.rated_pos] = True
+                rated_mask[key] = m
+            nr = len(s.topo.rated_pos)
+            gone = int(np.count_nonzero(rated_mask[key][s.removed])) if len(s.removed) else 0
+            rated_live.append(nr - gone)
         mineq_s = 2 * np.array(rated_live, dtype=np.int64)
         var_off = np.concatenate([[0], np.cumsum(n_s)[:-1]]).astype(np.int64)
         eq_off = np.concatenate([[0], np.cumsum(meq_s)[:-1]]).astype(np.int64)
@@ -294,31 +289,49 @@ class _Lattice:
                 return var_off[stage] + 2 * s.topo.nb + pos
             return var_off[stage] + s.topo.nb + s.topo.pc.slot[buses]
 
-        kind_code, sa, sb, gen, bus, bound, row, col_a, col_b = ([] for _ in range(9))
+        # one preallocated array per field, filled group by group (6.1 M rows for cfg4)
+        total = sum(len(r[5]) for r in pins) + sum(len(r[5]) for r in boxes)
+        cp = dict(kind=np.empty(total, dtype=np.int8), stage_a=np.empty(total, dtype=np.int64),
+                  stage_b=np.empty(total, dtype=np.int64), gen=np.empty(total, dtype=np.int64),
+                  bus=np.empty(total, dtype=np.int64), bound=np.empty(total, dtype=np.float64),
+                  row=np.empty(total, dtype=np.int64), col_a=np.empty(total, dtype=np.int64),
+                  col_b=np.empty(total, dtype=np.int64))
+        gen_pos = {}                   # topology -> variable position of each case generator (-1: off)
+
+        def var_cols_fast(stage, gens, buses):
+            s = st[stage]
+            if gens is not None:
+                key = id(s.topo)
+                if key not in gen_pos:
+                    m = np.full(int(s.topo.live_gens.max()) + 1 if len(s.topo.live_gens) else 1, -1, dtype=np.int64)
+                    m[s.topo.live_gens] = np.arange(len(s.topo.live_gens))
+                    gen_pos[key] = m
+                return var_off[stage] + 2 * s.topo.nb + gen_pos[key][gens]
+            return var_cols(stage, gens, buses)
+
+        at = 0
         nxt_pin, nxt_box = me_st, m_eq + mi_st
         for group in (pins, boxes):
             for kind, child, base, gens, buses, bnd, is_eq in group:
                 k = len(bnd)
                 if k == 0:
                     continue
+                sl = slice(at, at + k)
                 start = nxt_pin if is_eq else nxt_box
-                row.append(np.arange(start, start + k, dtype=np.int64))
+                cp["row"][sl] = np.arange(start, start + k, dtype=np.int64)
                 if is_eq:
                     nxt_pin += k
                 else:
                     nxt_box += k
-                kind_code.append(np.full(k, KINDS.index(kind), dtype=np.int8))
-                sa.append(np.full(k, child, dtype=np.int64))
-                sb.append(np.full(k, base, dtype=np.int64))
-                gen.append(gens if gens is not None else np.full(k, -1, dtype=np.int64))
-                bus.append(buses if buses is not None else np.full(k, -1, dtype=np.int64))
-                bound.append(np.asarray(bnd, dtype=np.float64))
-                col_a.append(var_cols(child, gens, buses))
-                col_b.append(var_cols(base, gens, buses))
-        cat = lambda parts, dt: np.concatenate(parts).astype(dt) if parts else np.zeros(0, dtype=dt)
-        cp = dict(kind=cat(kind_code, np.int8), stage_a=cat(sa, np.int64), stage_b=cat(sb, np.int64),
-                  gen=cat(gen, np.int64), bus=cat(bus, np.int64), bound=cat(bound, np.float64),
-                  row=cat(row, np.int64), col_a=cat(col_a, np.int64), col_b=cat(col_b, np.int64))
+                cp["kind"][sl] = KINDS.index(kind)
+                cp["stage_a"][sl] = child
+                cp["stage_b"][sl] = base
+                cp["gen"][sl] = gens if gens is not None else -1
+                cp["bus"][sl] = buses if buses is not None else -1
+                cp["bound"][sl] = bnd
+                cp["col_a"][sl] = var_cols_fast(child, gens, buses)
+                cp["col_b"][sl] = var_cols_fast(base, gens, buses)
+                at += k
         return CompositeSpec(plans=plans, cp=cp, n_pins=n_pins, n_s=n_s, meq_s=meq_s, mineq_s=mineq_s,
                              var_off=var_off, eq_off=eq_off, ineq_off=ineq_off, m_eq=m_eq, m_ineq=m_ineq,
                              stage_dims=[(s.topo.nb, s.topo.ng) for s in st])
@@ -338,21 +351,41 @@ class _Lattice:
         if (ev.n, ev.m_eq, ev.m_ineq) != (nv, m_eq, m_ineq):
             raise RuntimeError("native planner sizes disagree with the lattice")
 
-        # bounds
-        xl = np.empty(nv)
-        xu = np.empty(nv)
-        x0 = np.empty(nv)
-        gls, gus = [], []
-        for k, s in enumerate(st):
-            a = var_off[k]
-            lo, hi, start = stage_bounds(s.topo, s.pt, s.pmin, s.pmax)
-            xl[a:a + s.topo.n], xu[a:a + s.topo.n], x0[a:a + s.topo.n] = lo, hi, start
-            gl, gu = s.topo.ineq_bounds(s.removed)
-            gls.append(gl)
-            gus.append(gu)
+        # bounds: one (xl, xu, x0) per distinct (topology, period, scenario limits) and one
+        # (gl, gu) per distinct (topology, removed branches); the flat vectors are filled by
+        # the library's threaded run copy (acopf_copy_runs)
+        xl, xu, x0 = (np.empty(nv) for _ in range(3))
         is_box = cp["row"] >= m_eq
-        gl = np.concatenate(gls + [-cp["bound"][is_box]])
-        gu = np.concatenate(gus + [cp["bound"][is_box]])
+        n_box = int(np.count_nonzero(is_box))
+        mi_st = int(mineq_s.sum())
+        gl, gu = np.empty(mi_st + n_box), np.empty(mi_st + n_box)
+        xkeys, gkeys = {}, {}
+        xsrc, gsrc = [], []
+        x_src_off = np.empty(ns, dtype=np.int64)
+        g_src_off = np.empty(ns, dtype=np.int64)
+        xo = go = 0
+        for k, s in enumerate(st):
+            kx = (id(s.topo), s.t, s.s_pos if s.pmin is not None else -1)
+            if kx not in xkeys:
+                xkeys[kx] = xo
+                xsrc.append(stage_bounds(s.topo, s.pt, s.pmin, s.pmax))
+                xo += s.topo.n
+            x_src_off[k] = xkeys[kx]
+            kg = (id(s.topo), s.removed.tobytes())
+            if kg not in gkeys:
+                gkeys[kg] = go
+                gsrc.append(s.topo.ineq_bounds(s.removed))
+                go += len(gsrc[-1][0])
+            g_src_off[k] = gkeys[kg]
+        lens = n_s.astype(np.int64)
+        for dst, j in ((xl, 0), (xu, 1), (x0, 2)):
+            copy_runs(dst, var_off, np.concatenate([b[j] for b in xsrc]), x_src_off, lens)
+        glens = mineq_s.astype(np.int64)
+        for dst, j in ((gl, 0), (gu, 1)):
+            src = np.concatenate([b[j] for b in gsrc]) if gsrc else np.zeros(0)
+            copy_runs(dst, ineq_off, src, g_src_off, glens)
+        gl[mi_st:] = -cp["bound"][is_box]
+        gu[mi_st:] = cp["bound"][is_box]
 
         cbk = CallbackSet(ev)
         problem = NlpProblem(n=nv, m_eq=m_eq, m_ineq=m_ineq, xl=xl, xu=xu, gl=gl, gu=gu, x0=x0,
@@ -392,6 +425,18 @@ class _Lattice:
         # stage_a, stage_b, gen, bus (-1 = none), bound, row, and the x columns col_a / col_b
         object.__setattr__(index, "coupling_arrays", cp)
         return problem, index
+
+
+def copy_runs(dst: np.ndarray, dst_off, src: np.ndarray, src_off, lens) -> None:
+    """dst[dst_off[i]:+lens[i]] = src[src_off[i]:+lens[i]] for every run (acopf_copy_runs, threaded)."""
+    import ctypes
+    n = len(lens)
+    if n == 0:
+        return
+    do, so, ln = L.i64(dst_off), L.i64(src_off), L.i64(lens)
+    src = L.f64(src) if len(src) else np.zeros(1)
+    L.check(L.lib().acopf_copy_runs(n, dst.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), L.ptr(do, ctypes.c_int64),
+                                    L.ptr(src, ctypes.c_double), L.ptr(so, ctypes.c_int64), L.ptr(ln, ctypes.c_int64)))
 
 
 def stage_bounds(topo: Topology, pc: PackedCase, pmin=None, pmax=None):

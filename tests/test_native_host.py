@@ -254,3 +254,27 @@ def test_reference_fixture_composite_structure(name):
     assert np.array_equal(ip, g["jindptr"]) and np.array_equal(ix, g["jindices"])
     ip, ix = p.evaluator.pattern("H")
     assert np.array_equal(ip, g["hindptr"]) and np.array_equal(ix, g["hindices"])
+
+
+def test_native_graph_checks_match_the_python_restatements():
+    """acopf_graph_bridges / acopf_graph_islands (the lattice's islanding checks) against
+    grid.check_connectivity (network.py:232-262) and a Python Tarjan, incl. parallel twins."""
+    from dataclasses import replace
+    from paper_2203_10587_b200 import lattice as Lt
+    from paper_2203_10587_b200 import synthetic as syn
+    from paper_2203_10587_b200.grid import check_connectivity
+    from paper_2203_10587_b200.packer import PackedCase
+    for case in (syn.make_case(300, 60, 40, seed=5, features=True), C.hub_case(), syn.config_case(2)):
+        pc = PackedCase(case)
+        nb = set(syn.non_bridge_branches(case))
+        br = Lt._bridges(pc)
+        for k in pc.live_br:
+            if case.branches[int(k)].fbus != case.branches[int(k)].tbus:
+                assert (int(k) in br) == (int(k) not in nb)
+        rng = np.random.default_rng(1)
+        live = sorted(int(k) for k in pc.live_br)
+        for _ in range(10):
+            rem = set(rng.choice(live, size=4, replace=False).tolist())
+            c2 = replace(case, branches=tuple(replace(b, status=0) if i in rem else b
+                                              for i, b in enumerate(case.branches)))
+            assert Lt._islands_without(pc, sorted(rem)) == check_connectivity(c2)[0]
