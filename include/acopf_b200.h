@@ -181,6 +181,23 @@ int acopf_multi_destroy(acopf_multi* m);
 int acopf_batch_eval_multi(acopf_multi* m, double* x, double obj_factor, const double* mult, uint32_t what,
                            double* obj, double* grad, double* cons, double* jval, double* hval, void* stream);
 
+/* The reference IPM's Newton matrix on the device (ipm.py:463-477, 173-189), dense,
+ * K = [[0.5 (Hfull + Hfull^T) + reg I, Je^T], [Je, -delta I]]
+ * with Hfull = H + diag(dx) + Ji^T diag(ds) Ji over the nf free variables, from
+ * device J / H value arrays (jval / hval of acopf_batch_eval) and device index
+ * structures: H as CSR over free rows (h_ptr nf+1, free column h_col, value index
+ * h_vi), Ji as CSC over free columns (jt_*: inequality row, value index) and as CSR
+ * over inequality rows (ji_*: free column, value index), Je as CSR over equality
+ * rows (je_*); sc_e / sc_i: the reference view's row scales s_c of the equality and
+ * inequality rows (NULL = 1).  K must hold (nf+me)^2 zeros; both triangles are
+ * written.  Deterministic (no atomics). */
+int acopf_kkt_assemble(int64_t nf, int64_t me, double* K, const int64_t* h_ptr, const int32_t* h_col,
+                       const int64_t* h_vi, const double* hval, const double* dx, const int64_t* jt_ptr,
+                       const int32_t* jt_row, const int64_t* jt_vi, const int64_t* ji_ptr, const int32_t* ji_col,
+                       const int64_t* ji_vi, const double* jval, const double* ds, const int64_t* je_ptr,
+                       const int32_t* je_col, const int64_t* je_vi, const double* sc_e, const double* sc_i,
+                       double reg, double delta, void* stream);
+
 /* Host graph utilities of the composite builder (network.py:232-262, 339-344):
  * islands of the in-service network over buses with alive[v] != 0 (edges with an
  * endpoint not alive are ignored; edge_live may be NULL = all), labels in the

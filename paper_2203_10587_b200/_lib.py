@@ -57,6 +57,7 @@ _SIGNATURES = {
     "acopf_multi_destroy": (c_int32, [c_void_p]),
     "acopf_batch_eval_multi": (c_int32, [c_void_p, c_void_p, c_double, c_void_p, c_uint32, c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_void_p, c_void_p]),
+    "acopf_kkt_assemble": (c_int32, [c_int64, c_int64] + [c_void_p] * 19 + [c_double, c_double, c_void_p]),
     "acopf_graph_islands": (c_int32, [c_int32, POINTER(c_uint8), c_int64, _i32p, _i32p, POINTER(c_uint8),
                                       _i32p, _i32p]),
     "acopf_graph_bridges": (c_int32, [c_int32, c_int64, _i32p, _i32p, POINTER(c_uint8), POINTER(c_uint8)]),

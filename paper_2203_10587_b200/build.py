@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libacopf_b200.so")
 SOURCES = ["abi.cu"]
-DEPS = ["abi.cu", "eval_kernel.cuh", "planner.hpp", "sincos.cuh", "writer.hpp", "sl_planner.hpp", "sl_kernel.cuh", "gen_sincos_table.py",
+DEPS = ["abi.cu", "eval_kernel.cuh", "planner.hpp", "sincos.cuh", "writer.hpp", "sl_planner.hpp", "sl_kernel.cuh", "kkt.cuh", "gen_sincos_table.py",
         os.path.join("..", "..", "include", "acopf_b200.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -20,6 +20,7 @@
 #include "../../include/acopf_b200.h"
 #include "eval_kernel.cuh"
 #include "sl_kernel.cuh"
+#include "kkt.cuh"
 #include "planner.hpp"
 #include "writer.hpp"
 
@@ -1485,6 +1486,37 @@ int acopf_batch_eval_multi(acopf_multi* m, double* x, double obj_factor, const d
         if ((what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) && P.n_bus_items > 0) launch_bus_work(b, P, st);
         if (halo) cuda_check(cudaStreamWaitEvent(st, m->ev_halo, 0), "stream wait");
         if (gen) cuda_check(cudaStreamWaitEvent(st, m->ev_gen, 0), "stream wait");
+    });
+}
+
+int acopf_kkt_assemble(int64_t nf, int64_t me, double* K, const int64_t* h_ptr, const int32_t* h_col,
+                       const int64_t* h_vi, const double* hval, const double* dx, const int64_t* jt_ptr,
+                       const int32_t* jt_row, const int64_t* jt_vi, const int64_t* ji_ptr, const int32_t* ji_col,
+                       const int64_t* ji_vi, const double* jval, const double* ds, const int64_t* je_ptr,
+                       const int32_t* je_col, const int64_t* je_vi, const double* sc_e, const double* sc_i,
+                       double reg, double delta, void* stream) {
+    return guard([&] {
+        if (nf < 0 || me < 0 || !K) throw std::runtime_error("bad arguments");
+        KKTParams Q{};
+        Q.nf = nf; Q.me = me; Q.dim = nf + me; Q.K = K;
+        Q.h_ptr = h_ptr; Q.h_col = h_col; Q.h_vi = h_vi; Q.hval = hval; Q.dx = dx;
+        Q.jt_ptr = jt_ptr; Q.jt_row = jt_row; Q.jt_vi = jt_vi;
+        Q.ji_ptr = ji_ptr; Q.ji_col = ji_col; Q.ji_vi = ji_vi; Q.jval = jval; Q.ds = ds;
+        Q.je_ptr = je_ptr; Q.je_col = je_col; Q.je_vi = je_vi; Q.sc_e = sc_e; Q.sc_i = sc_i;
+        Q.reg = reg; Q.delta = delta;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (nf > 0) {
+            acopf_kkt_hfull_kernel<<<(unsigned)((nf + 127) / 128), 128, 0, st>>>(Q);
+            cuda_check(cudaGetLastError(), "acopf_kkt_hfull_kernel launch");
+            const unsigned gx = (unsigned)std::min<int64_t>(64, (nf + 255) / 256);
+            acopf_kkt_finish_kernel<<<dim3(gx, (unsigned)std::min<int64_t>(nf, 65535)), 256, 0, st>>>(Q);
+            cuda_check(cudaGetLastError(), "acopf_kkt_finish_kernel launch");
+        }
+        const int64_t nd = std::max(nf, me);
+        if (nd > 0) {
+            acopf_kkt_diag_je_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, st>>>(Q);
+            cuda_check(cudaGetLastError(), "acopf_kkt_diag_je_kernel launch");
+        }
     });
 }
 
