@@ -315,7 +315,12 @@ static void upload(acopf_batch* b) {
     // enough that the inputs (x, multipliers) of the stage groups in flight stay
     // L2-resident (ACOPF_L2_INPUT_MB per group; gathers otherwise re-read HBM)
     const char* wenv = getenv("ACOPF_ITEM_WAVES");     // development aid: items per resident CTA slot
-    const int64_t target_items = 148LL * (WARP_MINB / TILE_WARPS) * (wenv ? std::max(1, atoi(wenv)) : 6);
+    int n_sm = 148;                                     // B200; the device's own count when it is visible
+    if (cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, b->device) != cudaSuccess || n_sm <= 0) {
+        cudaGetLastError();
+        n_sm = 148;
+    }
+    const int64_t target_items = (int64_t)n_sm * (WARP_MINB / TILE_WARPS) * (wenv ? std::max(1, atoi(wenv)) : 6);
     double in_bytes = 0.0;
     for (const StageInfo& st : b->stages) in_bytes += 8.0 * (double)(st.n + st.m_eq + st.m_ineq);
     const double per_stage = in_bytes / std::max(1, S);

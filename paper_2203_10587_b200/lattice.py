@@ -73,6 +73,30 @@ class LazySeq:
         except TypeError:
             return NotImplemented
 
+    def __contains__(self, item):
+        return any(item == v for v in self)
+
+    def index(self, item):
+        for i, v in enumerate(self):
+            if v == item:
+                return i
+        raise ValueError(f"{item!r} is not in the sequence")
+
+    def count(self, item):
+        return sum(1 for v in self if v == item)
+
+    def __reversed__(self):
+        return (self[i] for i in range(self._n - 1, -1, -1))
+
+    def __repr__(self):
+        return f"LazySeq(len={self._n})"
+
+
+# a read-only sequence for isinstance checks (collections.abc.Sequence), like the
+# reference's tuples; items are built on first access (cfg4: 6.1 M coupling rows)
+import collections.abc as _abc  # noqa: E402
+_abc.Sequence.register(LazySeq)
+
 
 def _same_topology(a: PackedCase, b: PackedCase) -> bool:
     """Everything but loads equal (composer.py:112-126 checks a subset)."""

@@ -86,11 +86,25 @@ def _host_flows(ev: BatchEvaluator, x: np.ndarray):
     return out
 
 
+_SINGLE_CACHE: "dict" = {}
+
+
 def _single(case):
-    """(PackedCase, Topology, one-stage evaluator) of a case, as _Engine(case) (acopf.py:77-149)."""
+    """(PackedCase, Topology, one-stage evaluator) of a case, as _Engine(case) (acopf.py:77-149).
+
+    Cached per case object (cases are frozen dataclasses): repeated extract_solution /
+    residuals_at calls on one case reuse the packing, the planner's tables and the device
+    upload instead of rebuilding them (a few most recent cases are kept)."""
+    key = id(case)
+    hit = _SINGLE_CACHE.get(key)
+    if hit is not None and hit[0] is case:
+        return hit[1]
     pc = PackedCase(case)
     topo = Topology(pc)
     ev = BatchEvaluator([stage_plan(topo)], layout="independent")
+    if len(_SINGLE_CACHE) >= 8:
+        _SINGLE_CACHE.pop(next(iter(_SINGLE_CACHE)))
+    _SINGLE_CACHE[key] = (case, (pc, topo, ev))
     return pc, topo, ev
 
 
