@@ -119,7 +119,7 @@ struct acopf_batch {
     // device
     cudaStream_t stream = nullptr;
     DevBuf d_topo, d_stage, d_items, d_recs, d_aux, d_blob, d_pd, d_qd, d_ca, d_cb, d_cc, d_rem, d_remsz;
-    DevBuf d_cpruns, d_objterms, d_xi;
+    DevBuf d_cpruns, d_objterms, d_xi, d_auxdone;
     int max_nb = 0;
     int n_gen_items = 0;             // aux items [0, n_gen_items) are generator chunks, the rest coupling runs
     std::vector<std::unique_ptr<DevBuf>> topo_bufs;
@@ -639,6 +639,7 @@ static void upload(acopf_batch* b) {
     P.n_obj = S;
     P.obj_mode = b->obj_mode;
     P.obj_terms = static_cast<double*>(b->d_objterms.alloc(sizeof(double) * std::max(S, 1)));
+    P.aux_done = static_cast<unsigned*>(b->d_auxdone.alloc(sizeof(unsigned)));
     // interleaved (VA, VM, muP, muQ) per stage and bus, indexed 4 (var_off + bus)
     {
         int64_t xi_len = 4;
@@ -1044,6 +1045,20 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) && P.n_bus_items > 0;
         static const bool no_aux = getenv("ACOPF_EXP_NO_AUX") != nullptr;   // development aid: tile kernel alone
         const bool aux = !no_aux && (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
+        // full evaluations on the tile kernel path: the generator/coupling items run as the
+        // last blocks of the tile kernel's own grid (one launch, no fork / join)
+        static const bool fuse_env = !getenv("ACOPF_FUSED_AUX") || atoi(getenv("ACOPF_FUSED_AUX")) != 0;
+        if (fuse_env && aux && bus && !(what == ACOPF_ALL && b->sl_on) && !(P.xi && b->il_chunks.size() > 1)) {
+            P.aux_in_tile = 1;
+            P.n_bus_launch = P.n_bus_items;
+            launch_interleave(b, P, 0, (int)b->stages.size(), st);
+            const int grid = P.n_bus_items + P.n_aux_items;
+            if (what == ACOPF_ALL) acopf_tile_kernel<ACOPF_ALL><<<grid, TILE_THREADS, b->smem, st>>>(P, 0);
+            else acopf_tile_kernel<0u><<<grid, TILE_THREADS, b->smem, st>>>(P, 0);
+            cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
+            b->launches++;
+            return;
+        }
         // the generator/coupling kernel runs concurrently on a forked stream
         const bool fork = aux && bus;
         if (fork) {

@@ -99,6 +99,9 @@ struct EvalParams {
     double* flows;            // W_FLOWS: per stage pf, qf, pt, qt by topology branch (pu)
     double* inj;              // W_FLOWS: per stage p, q network injections by bus (pu)
     double* xi;               // per stage and bus (VA, VM, muP, muQ) at 4 (var_off + bus): acopf_interleave_kernel
+    int aux_in_tile;          // 1: the tile kernel's grid also runs the generator / coupling items
+    int n_bus_launch;         // (then blocks >= n_bus_launch are aux items)
+    unsigned* aux_done;       // finished aux items (the last one sums the composite objective)
 };
 
 #ifndef ACOPF_WARP_MINB
@@ -549,6 +552,33 @@ __device__ __forceinline__ void copy_seg16(double* g, const double* s, int L, in
     }
 }
 
+__device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q);
+__device__ void coupling_runs(const EvalParams& P, int first, int count);
+__device__ void objsum_block(const EvalParams& P, double* buf);
+
+// A generator / coupling item run by a block of the tile kernel's grid (after the
+// tile items, so these blocks fill the tile kernel's last wave): one launch per
+// evaluation, no fork / join.  The block that finishes the last item sums the
+// composite objective in stage order (a ticket counter; the sum itself is the
+// fixed-order acopf_objsum_kernel loop, so the result is deterministic).
+__device__ __forceinline__ void aux_in_tile(const EvalParams& P, int k, double* Q) {
+    __shared__ int last;
+    const DAuxItem it = P.aux_items[k];
+    if (it.kind == 0) gen_chunk(P, it.stage, it.chunk, Q);
+    else coupling_runs(P, it.stage, it.chunk);
+    if (!(P.obj_mode == 1 && (P.what & W_OBJ))) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(P.aux_done, 1u) == (unsigned)(P.n_aux_items - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    objsum_block(P, Q);
+    if (threadIdx.x == 0) atomicExch(P.aux_done, 0u);
+}
+
 // ---------------------------------------------------------------------------
 // Tile kernel: one CTA (one thread per branch end) evaluates one tile for a run of stages.
 //
@@ -571,6 +601,10 @@ template <unsigned WHAT>
 __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_tile_kernel(const EvalParams P, int item0) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar, rbar;      // table load; stage records
+    if (P.aux_in_tile && (int)blockIdx.x >= P.n_bus_launch) {
+        aux_in_tile(P, blockIdx.x - P.n_bus_launch, reinterpret_cast<double*>(smem));
+        return;
+    }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const DBusItem it = P.bus_items[item0 + blockIdx.x];
     const unsigned rb_ = smem_u32(&rbar);
@@ -802,7 +836,6 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
     const DStage S = P.stages[s];
     const int nb = S.nb, ng = S.ng;
     const double* pg = P.x + S.var_off + 2 * nb;
-    const int g = chunk * GEN_CHUNK + threadIdx.x;
     if (P.what & W_GRAD) {
         // the angle and magnitude entries (acopf.py:271-275: w * 0.0), spread
         // over the stage's generator chunks
@@ -810,7 +843,8 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
         const int span = (2 * nb + nch - 1) / nch, v1 = min(2 * nb, (chunk + 1) * span);
         for (int v = chunk * span + threadIdx.x; v < v1; v += blockDim.x) P.grad[S.var_off + v] = S.w * 0.0;
     }
-    if (g < ng) {
+    const int g_end = min(ng, (chunk + 1) * GEN_CHUNK);
+    for (int g = chunk * GEN_CHUNK + threadIdx.x; g < g_end; g += blockDim.x) {
         if (P.what & W_GRAD) {
             const double ca = P.ca[S.cost_off + g], cb = P.cb[S.cost_off + g];
             P.grad[S.var_off + 2 * nb + g] = S.w * ((2.0 * ca) * pg[g] + cb);
@@ -867,19 +901,24 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
 }
 
 // The composite objective (composer.py:256-258): the weighted stage terms in
-// stage order.  One block stages them 256 at a time; one thread adds them.
-__global__ void __launch_bounds__(BLOCK) acopf_objsum_kernel(const EvalParams P) {
-    __shared__ double buf[BLOCK];
+// stage order.  One block stages them blockDim.x at a time; one thread adds them
+// (L2 reads: the terms were written by other blocks).
+__device__ void objsum_block(const EvalParams& P, double* buf) {
     double acc = 0.0;
-    for (int i0 = 0; i0 < P.n_obj; i0 += BLOCK) {
-        const int n = min(BLOCK, P.n_obj - i0);
-        if ((int)threadIdx.x < n) buf[threadIdx.x] = P.obj_terms[i0 + threadIdx.x];
+    for (int i0 = 0; i0 < P.n_obj; i0 += blockDim.x) {
+        const int n = min((int)blockDim.x, P.n_obj - i0);
+        if ((int)threadIdx.x < n) buf[threadIdx.x] = __ldcg(P.obj_terms + i0 + threadIdx.x);
         __syncthreads();
         if (threadIdx.x == 0)
             for (int i = 0; i < n; ++i) acc = acc + buf[i];
         __syncthreads();
     }
     if (threadIdx.x == 0) P.obj[0] = acc;
+}
+
+__global__ void __launch_bounds__(BLOCK) acopf_objsum_kernel(const EvalParams P) {
+    __shared__ double buf[BLOCK];
+    objsum_block(P, buf);
 }
 
 __device__ void coupling_runs(const EvalParams& P, int first, int count) {
