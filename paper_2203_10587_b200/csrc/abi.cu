@@ -1045,10 +1045,12 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
         const bool bus = (what & (ACOPF_CONS | ACOPF_JAC | ACOPF_HESS)) && P.n_bus_items > 0;
         static const bool no_aux = getenv("ACOPF_EXP_NO_AUX") != nullptr;   // development aid: tile kernel alone
         const bool aux = !no_aux && (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS | ACOPF_CONS | ACOPF_JAC)) && P.n_aux_items > 0;
-        // full evaluations on the tile kernel path: the generator/coupling items run as the
-        // last blocks of the tile kernel's own grid (one launch, no fork / join)
-        static const bool fuse_env = !getenv("ACOPF_FUSED_AUX") || atoi(getenv("ACOPF_FUSED_AUX")) != 0;
-        if (fuse_env && aux && bus && !(what == ACOPF_ALL && b->sl_on) && !(P.xi && b->il_chunks.size() > 1)) {
+        // the generator/coupling items run as the last blocks of the tile kernel's own grid (one
+        // launch, no fork / join) when they are a small share of it: measured cfg3 -5%; with
+        // many aux items (cfg1/2/4) their 128-thread blocks in the tail cost 2-4% instead
+        const char* fe = getenv("ACOPF_FUSED_AUX");      // 0 / 1 force it (development aid)
+        const bool fuse_ok = fe ? atoi(fe) != 0 : (int64_t)P.n_aux_items * 100 <= (int64_t)P.n_bus_items * 15;
+        if (fuse_ok && aux && bus && !(what == ACOPF_ALL && b->sl_on) && !(P.xi && b->il_chunks.size() > 1)) {
             P.aux_in_tile = 1;
             P.n_bus_launch = P.n_bus_items;
             launch_interleave(b, P, 0, (int)b->stages.size(), st);
