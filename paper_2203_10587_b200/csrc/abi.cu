@@ -143,6 +143,8 @@ struct acopf_batch {
     // host-buffer pipeline (independent layouts): chunks of whole stage groups
     struct Pipe { int s0, s1, bus_first, bus_count, aux_first, aux_count; };
     std::vector<Pipe> pipe;
+    int pipe_mode = 0;               // 1: independent stages ([eq; ineq] per stage); 2: composite
+                                     // (stage blocks in order in every region, coupling rows after)
     std::vector<Pipe> il_chunks;     // device evaluation with interleaved inputs: chunks whose pre-pass
                                      // overlaps the previous chunk's tile kernel (two streams)
     cudaStream_t pipe_streams[3] = {nullptr, nullptr, nullptr};
@@ -534,7 +536,7 @@ static void upload(acopf_batch* b) {
     // the chunked copies move [off6(s0), off6(s1)) ranges: only valid when every
     // stage's blocks are contiguous and in stage order ([eq; ineq] rows, [Jeq; Jineq]
     // values, x, H values, objective slot s)
-    bool contiguous = true;
+    bool contiguous = true, composite = S >= 2;
     for (int s = 0; s < S && contiguous; ++s) {
         const StageInfo& st = b->stages[s];
         const int64_t* o = &b->off6[6 * s];
@@ -546,7 +548,19 @@ static void upload(acopf_batch* b) {
             contiguous = contiguous && q[0] == nx[0] && q[1] == nx[1] && q[3] == nx[3] && q[5] == nx[5];
         }
     }
-    if (b->obj_mode == 0 && n_coupling == 0 && S >= 2 && contiguous) {
+    // composite layouts: every region (x, eq rows, ineq rows, J eq, J ineq, H) holds the stage
+    // blocks in stage order; coupling rows / J entries lie outside them
+    for (int s = 0; s + 1 < S && composite; ++s) {
+        const StageInfo& st = b->stages[s];
+        const int64_t *o = &b->off6[6 * s], *q = &b->off6[6 * (s + 1)];
+        composite = q[0] == o[0] + st.n && q[1] == o[1] + st.m_eq && q[2] == o[2] + st.m_ineq &&
+                    q[3] == o[3] + st.nnz_jeq && q[4] == o[4] + st.nnz_jin && q[5] == o[5] + st.nnz_h &&
+                    b->obj_slot[s] == s && b->obj_slot[s + 1] == s + 1;
+    }
+    composite = composite && b->obj_mode != 0 && !contiguous;
+    b->pipe_mode = 0;
+    if ((b->obj_mode == 0 && n_coupling == 0 && S >= 2 && contiguous) || composite) {
+        b->pipe_mode = composite ? 2 : 1;
         const int ngroups = (S + G - 1) / G;
         const int nchunks = getenv("ACOPF_PIPE_CHUNKS") ? std::max(1, atoi(getenv("ACOPF_PIPE_CHUNKS"))) : 8;   // development aid
         const int per = std::max(1, (ngroups + nchunks - 1) / nchunks);
@@ -1148,27 +1162,52 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
         if (b->pipe.size() > 1 && x && nx) {
             // chunk c: H2D of its inputs, its kernels, D2H of its outputs, on stream c % 3;
-            // copies of one chunk overlap the kernels and copies of the others
+            // copies of one chunk overlap the kernels and copies of the others.  Composite
+            // layouts then run the coupling rows and the stage-order objective (they read every
+            // chunk's x / objective terms) and copy out the coupling regions.
             const EvalParams base = b->params;
             EvalParams P = base;
             P.x = dx; P.mult = mult ? dm : nullptr; P.obj_factor = obj_factor; P.what = what;
             P.obj = dobj; P.grad = dg; P.cons = dc; P.jval = dj; P.hval = dh;
+            const bool comp = b->pipe_mode == 2;
             cudaEvent_t start;
             cuda_check(cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
             cuda_check(cudaEventRecord(start, st), "event record");
             const int S = (int)b->stages.size();
+            // start of stage s in region k (s == S: the end of the last stage's block)
+            auto rlo = [&](int s, int k) -> int64_t {
+                if (s < S) return b->off6[6 * s + k];
+                const StageInfo& L = b->stages[S - 1];
+                const int64_t sz[6] = {L.n, L.m_eq, L.m_ineq, L.nnz_jeq, L.nnz_jin, L.nnz_h};
+                return b->off6[6 * (S - 1) + k] + sz[k];
+            };
             auto lo = [&](int s, int k, int64_t total) -> int64_t { return s >= S ? total : b->off6[6 * s + k]; };
             auto m_lo = [&](int s) -> int64_t { return s >= S ? nm : b->off6[6 * s + 1]; };
+            auto h2d = [&](double* d, const double* h, int64_t a, int64_t e, cudaStream_t cs, const char* w) {
+                if (e > a) cuda_check(cudaMemcpyAsync(d + a, h + a, 8 * (e - a), cudaMemcpyHostToDevice, cs), w);
+            };
+            auto d2h = [&](double* h, const double* d, int64_t a, int64_t e, cudaStream_t cs, const char* w) {
+                if (e > a) cuda_check(cudaMemcpyAsync(h + a, d + a, 8 * (e - a), cudaMemcpyDeviceToHost, cs), w);
+            };
             for (size_t c = 0; c < b->pipe.size(); ++c) {
                 const auto& pc = b->pipe[c];
                 cudaStream_t cs = b->pipe_streams[c % 3];
                 cuda_check(cudaStreamWaitEvent(cs, start, 0), "stream wait");
-                const int64_t x0 = lo(pc.s0, 0, nx), x1 = lo(pc.s1, 0, nx);
-                const int64_t m0 = m_lo(pc.s0), m1 = m_lo(pc.s1);
-                const int64_t j0 = lo(pc.s0, 3, nj), j1 = lo(pc.s1, 3, nj);
-                const int64_t h0 = lo(pc.s0, 5, nh), h1 = lo(pc.s1, 5, nh);
-                cuda_check(cudaMemcpyAsync(dx + x0, x + x0, 8 * (x1 - x0), cudaMemcpyHostToDevice, cs), "H2D x");
-                if (mult && nm) cuda_check(cudaMemcpyAsync(dm + m0, mult + m0, 8 * (m1 - m0), cudaMemcpyHostToDevice, cs), "H2D mult");
+                int64_t x0, x1, r0[2], r1[2], j0[2], j1[2], h0, h1;
+                if (comp) {
+                    x0 = rlo(pc.s0, 0); x1 = rlo(pc.s1, 0);
+                    r0[0] = rlo(pc.s0, 1); r1[0] = rlo(pc.s1, 1); r0[1] = rlo(pc.s0, 2); r1[1] = rlo(pc.s1, 2);
+                    j0[0] = rlo(pc.s0, 3); j1[0] = rlo(pc.s1, 3); j0[1] = rlo(pc.s0, 4); j1[1] = rlo(pc.s1, 4);
+                    h0 = rlo(pc.s0, 5); h1 = rlo(pc.s1, 5);
+                } else {
+                    x0 = lo(pc.s0, 0, nx); x1 = lo(pc.s1, 0, nx);
+                    r0[0] = m_lo(pc.s0); r1[0] = m_lo(pc.s1); r0[1] = r1[1] = 0;
+                    j0[0] = lo(pc.s0, 3, nj); j1[0] = lo(pc.s1, 3, nj); j0[1] = j1[1] = 0;
+                    h0 = lo(pc.s0, 5, nh); h1 = lo(pc.s1, 5, nh);
+                }
+                h2d(dx, x, x0, x1, cs, "H2D x");
+                if (mult && nm)
+                    for (int q = 0; q < 2; ++q) h2d(dm, mult, r0[q], r1[q], cs, "H2D mult");
                 if (pc.aux_count) {
                     acopf_aux_kernel<<<pc.aux_count, BLOCK, b->aux_smem, cs>>>(P, pc.aux_first);
                     cuda_check(cudaGetLastError(), ("acopf_aux_kernel launch (" + std::to_string(b->aux_smem) + " B shared)").c_str());
@@ -1181,19 +1220,45 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
                     cuda_check(cudaGetLastError(), "acopf_tile_kernel launch");
                     b->launches++;
                 }
-                if ((what & ACOPF_OBJ) && obj) cuda_check(cudaMemcpyAsync(obj + pc.s0, dobj + pc.s0, 8 * (pc.s1 - pc.s0), cudaMemcpyDeviceToHost, cs), "D2H obj");
-                if ((what & ACOPF_GRAD) && grad) cuda_check(cudaMemcpyAsync(grad + x0, dg + x0, 8 * (x1 - x0), cudaMemcpyDeviceToHost, cs), "D2H grad");
-                if ((what & ACOPF_CONS) && cons) cuda_check(cudaMemcpyAsync(cons + m0, dc + m0, 8 * (m1 - m0), cudaMemcpyDeviceToHost, cs), "D2H cons");
-                if ((what & ACOPF_JAC) && jval) cuda_check(cudaMemcpyAsync(jval + j0, dj + j0, 8 * (j1 - j0), cudaMemcpyDeviceToHost, cs), "D2H jac");
-                if ((what & ACOPF_HESS) && hval) cuda_check(cudaMemcpyAsync(hval + h0, dh + h0, 8 * (h1 - h0), cudaMemcpyDeviceToHost, cs), "D2H hess");
+                if ((what & ACOPF_OBJ) && obj && b->obj_mode != 1) d2h(obj, dobj, pc.s0, pc.s1, cs, "D2H obj");
+                if ((what & ACOPF_GRAD) && grad) d2h(grad, dg, x0, x1, cs, "D2H grad");
+                for (int q = 0; q < 2; ++q) {
+                    if ((what & ACOPF_CONS) && cons) d2h(cons, dc, r0[q], r1[q], cs, "D2H cons");
+                    if ((what & ACOPF_JAC) && jval) d2h(jval, dj, j0[q], j1[q], cs, "D2H jac");
+                }
+                if ((what & ACOPF_HESS) && hval) d2h(hval, dh, h0, h1, cs, "D2H hess");
             }
-            // join the pipeline back into the caller's stream, then wait
+            // join the pipeline back into the caller's stream
             for (int k = 0; k < 3 && k < (int)b->pipe.size(); ++k) {
                 cudaEvent_t done;
                 cuda_check(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
                 cuda_check(cudaEventRecord(done, b->pipe_streams[k]), "event record");
                 cuda_check(cudaStreamWaitEvent(st, done, 0), "stream wait");
                 cudaEventDestroy(done);
+            }
+            if (comp) {
+                h2d(dx, x, rlo(S, 0), nx, st, "H2D x (halo)");     // values past the stage blocks (sharded halo)
+                const int n_cp = P.n_aux_items - b->n_gen_items;
+                if (n_cp > 0 && (what & (ACOPF_CONS | ACOPF_JAC))) {
+                    acopf_aux_kernel<<<n_cp, BLOCK, b->aux_smem, st>>>(P, b->n_gen_items);
+                    cuda_check(cudaGetLastError(), "acopf_aux_kernel (coupling) launch");
+                    b->launches++;
+                }
+                if (b->obj_mode == 1 && (what & ACOPF_OBJ)) {
+                    acopf_objsum_kernel<<<1, BLOCK, 0, st>>>(P);
+                    cuda_check(cudaGetLastError(), "acopf_objsum_kernel launch");
+                    b->launches++;
+                    if (obj) d2h(obj, dobj, 0, 1, st, "D2H obj");
+                }
+                // the coupling regions: pins after the eq blocks, boxes after the ineq blocks
+                if ((what & ACOPF_CONS) && cons) {
+                    d2h(cons, dc, rlo(S, 1), rlo(0, 2), st, "D2H cons (pins)");
+                    d2h(cons, dc, rlo(S, 2), ncons, st, "D2H cons (boxes)");
+                }
+                if ((what & ACOPF_JAC) && jval) {
+                    d2h(jval, dj, rlo(S, 3), rlo(0, 4), st, "D2H jac (pins)");
+                    d2h(jval, dj, rlo(S, 4), nj, st, "D2H jac (boxes)");
+                }
             }
             cudaEventDestroy(start);
             cuda_check(cudaStreamSynchronize(st), "stream sync");
