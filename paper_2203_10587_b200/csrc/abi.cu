@@ -558,6 +558,11 @@ static void upload(acopf_batch* b) {
                     b->obj_slot[s] == s && b->obj_slot[s + 1] == s + 1;
     }
     composite = composite && b->obj_mode != 0 && !contiguous;
+    {   // small composites gain nothing from chunked copies (cfg3, 73 MB of outputs: -5%)
+        double out_bytes = 0.0;
+        for (const StageInfo& st : b->stages) out_bytes += 8.0 * (st.n + st.m_eq + st.m_ineq + st.nnz_jeq + st.nnz_jin + st.nnz_h);
+        composite = composite && out_bytes > 256.0 * 1048576.0;
+    }
     b->pipe_mode = 0;
     if ((b->obj_mode == 0 && n_coupling == 0 && S >= 2 && contiguous) || composite) {
         b->pipe_mode = composite ? 2 : 1;
