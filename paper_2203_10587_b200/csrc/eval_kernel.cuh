@@ -146,12 +146,8 @@ __host__ __device__ __forceinline__ size_t tile_gather_off(int table_bytes, int 
 __host__ __device__ __forceinline__ size_t tile_rec_off(int table_bytes, int n_area) {
     return tile_gather_off(table_bytes, n_area) + 8 * (size_t)GQ * TILE_THREADS;
 }
-// own-bus inputs of the tile (interleaved path): 2 stage buffers of (VA, VM, muP, muQ) per bus
-__host__ __device__ __forceinline__ size_t tile_xib_off(int table_bytes, int n_area) {
-    return tile_rec_off(table_bytes, n_area) + 2 * sizeof(DRec);
-}
 __host__ __device__ __forceinline__ size_t tile_smem_bytes(int table_bytes, int n_area) {
-    return tile_xib_off(table_bytes, n_area) + 2 * 32 * (size_t)TILE_MAX_BUSES;
+    return tile_rec_off(table_bytes, n_area) + 2 * sizeof(DRec);
 }
 
 __device__ __forceinline__ void cp_async8s(unsigned dst, const void* src) {
@@ -241,16 +237,16 @@ __device__ __forceinline__ void prefetch(const EvalParams& P, const DRec& R, con
     }
     const int f = V.f[e], t = V.t[e], r = V.ridx[e];
     if (P.xi) {
-        // the far bus's (VA, VM, muP, muQ): one 256-bit load from the interleaved copy
-        // (the multipliers are zeros unless the Hessian is asked), cached in L2 only
-        // (scattered, little L1 reuse); the own bus's come from the tile's shared copy
-        // at phase A (own_bus_inputs)
-        const bool sd = e >= V.H->nF;
+        // both buses' (VA, VM, muP, muQ): one 256-bit load each from the
+        // interleaved copy (the multipliers are zeros unless the Hessian is asked),
+        // cached in L2 only (scattered, little L1 reuse)
         const double* xi = opaque(static_cast<const double*>(P.xi) + 4 * R.var_off);
-        double a, v, mp, mq;
-        asm("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(v), "=d"(mp), "=d"(mq) : "l"(xi + 4 * (sd ? f : t)));
-        in.vaf = a; in.vf = v; in.mpf = mp; in.mqf = mq;     // far values, placed by own_bus_inputs
-        in.vat = a; in.vt = v; in.mpt = mp; in.mqt = mq;
+        asm("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(in.vaf), "=d"(in.vf), "=d"(in.mpf), "=d"(in.mqf)
+            : "l"(xi + 4 * f));
+        asm("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(in.vat), "=d"(in.vt), "=d"(in.mpt), "=d"(in.mqt)
+            : "l"(xi + 4 * t));
     } else {
         // small networks: the stage's inputs stay L1-resident, gather directly
         const double* xm = x + R.nb;
@@ -494,27 +490,11 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
     }
 }
 
-// Interleaved path: the own bus's (VA, VM, muP, muQ) from the tile's shared copy
-// (two 128-bit loads; the ends of one bus read the same entry), completing the
-// far values prefetched into `in`.
-__device__ __forceinline__ void own_bus_inputs(const TileView& V, int e, const double* xib, EndIn& in) {
-    const bool sd = e >= V.H->nF;
-    const int own = (sd ? V.t[e] : V.f[e]) - V.H->b0;
-    const double2 a = reinterpret_cast<const double2*>(xib)[2 * own];
-    const double2 b = reinterpret_cast<const double2*>(xib)[2 * own + 1];
-    if (sd) { in.vat = a.x; in.vt = a.y; in.mpt = b.x; in.mqt = b.y; }
-    else { in.vaf = a.x; in.vf = a.y; in.mpf = b.x; in.mqf = b.y; }
-}
-
 __device__ __forceinline__ void ends_phase(const EvalParams& P, const DRec& R, const TileView& V, int tid,
-                                           const EndIn& pre, const double* G, const double* xib, unsigned char* sA,
-                                           bool need_j, bool need_h, bool need_c, bool need_f) {
+                                           const EndIn& pre, const double* G, unsigned char* sA, bool need_j,
+                                           bool need_h, bool need_c, bool need_f) {
     const int nE = V.H->nE;
-    if (tid < nE) {
-        EndIn in = pre;
-        if (xib) own_bus_inputs(V, tid, xib, in);
-        end_eval(P, R, V, tid, in, G, sA, need_j, need_h, need_c, need_f);
-    }
+    if (tid < nE) end_eval(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f);
     for (int e = tid + TILE_THREADS; e < nE; e += TILE_THREADS) {     // beyond one end per thread: unprefetched
         EndIn in;
         load_end(P, R, V, e, need_h, need_c, in);
@@ -621,7 +601,6 @@ template <unsigned WHAT>
 __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_tile_kernel(const EvalParams P, int item0) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar, rbar;      // table load; stage records
-    __shared__ __align__(8) unsigned long long xbar[2];        // own-bus input copies (interleaved path)
     if (P.aux_in_tile && (int)blockIdx.x >= P.n_bus_launch) {
         aux_in_tile(P, blockIdx.x - P.n_bus_launch, reinterpret_cast<double*>(smem));
         return;
@@ -633,8 +612,6 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         const unsigned b = smem_u32(&bar);
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rb_));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&xbar[0])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&xbar[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(it.bytes) : "memory");
         // tile tables are read by every item of their tile: evict-last in L2
@@ -667,18 +644,6 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
     unsigned char* const sA = reinterpret_cast<unsigned char*>(A);
     DRec* ctx = reinterpret_cast<DRec*>(smem + tile_rec_off(H->bytes, H->nArea));
     const double* G = reinterpret_cast<const double*>(smem + tile_gather_off(H->bytes, H->nArea)) + tid;
-    double* XIB = reinterpret_cast<double*>(smem + tile_xib_off(H->bytes, H->nArea));     // 2 x 4 doubles per bus
-    // one bulk copy of the tile's contiguous (VA, VM, muP, muQ) records of stage record rr into buffer k
-    auto own_copy = [&](const DRec& rr, int k) {
-        const unsigned xb = smem_u32(&xbar[k]);
-        const unsigned bytes = 32u * (unsigned)H->nB;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(xb), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(XIB + k * 4 * TILE_MAX_BUSES)),
-                     "l"(P.xi + 4 * (rr.var_off + H->b0)), "r"(bytes), "r"(xb)
-                     : "memory");
-    };
     const unsigned sG = smem_u32(G);
     TileView V;
     V.H = H;
@@ -711,7 +676,6 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
     if (tid == 0) record_load(rb_, ctx, P.bus_recs + it.first);
     mbar_wait(rb_, 0);
     __syncthreads();
-    if (P.xi && tid == 0) own_copy(ctx[0], 0);
     EndIn pre;
     prefetch(P, ctx[0], V, my_e, tid, sG, need_h, need_c, true, pre);
     cp_commit();
@@ -726,14 +690,9 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         const long long eq_row = R.eq_row;
         const int nb = R.nb;
         // ---- A: branch ends (one side per warp), generator set-points ----------
-        const double* xib = nullptr;
-        if (P.xi) {                                   // this stage's own-bus inputs
-            mbar_wait(smem_u32(&xbar[ri & 1]), (ri >> 1) & 1);
-            xib = XIB + (ri & 1) * 4 * TILE_MAX_BUSES;
-        }
 #ifndef ACOPF_DIAG_NO_A
         if (any_a) {
-            ends_phase(P, R, V, tid, pre, G, xib, sA, need_j, need_h, need_c, need_f);
+            ends_phase(P, R, V, tid, pre, G, sA, need_j, need_h, need_c, need_f);
         }
 #endif
         if (need_c) gens_phase(P, R, V, tid, G, sA);
@@ -748,7 +707,6 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
             }
         if (more) mbar_wait(rb_, (ri + 1) & 1);       // the next record
         __syncthreads();
-        if (more && P.xi && tid == 0) own_copy(ctx[(ri + 1) & 1], (ri + 1) & 1);
         // the gather buffer is free again: prefetch the next stage's inputs
 #ifndef ACOPF_DIAG_NO_PF
         if (more) prefetch(P, ctx[(ri + 1) & 1], V, my_e, tid, sG, need_h, need_c, ctx[(ri + 1) & 1].pd_off != R.pd_off,
