@@ -680,8 +680,8 @@ static void upload(acopf_batch* b) {
     // (up to 16 KB: larger aux blocks crowd the tile kernel's CTAs off the SMs;
     // a full carve-out preference for both kernels costs the tile kernel its L1)
     const char* se = getenv("ACOPF_OBJ_STAGE_KB");          // development aid
-    P.obj_staged = sizeof(double) * (max_leaf + max_ng) <= 1024 * (size_t)(se ? atoi(se) : 16) ? 1 : 0;
-    b->aux_smem = sizeof(double) * (max_leaf + (P.obj_staged ? max_ng : 0));
+    P.obj_staged = sizeof(double) * (9 * max_leaf + max_ng) <= 1024 * (size_t)(se ? atoi(se) : 16) ? 1 : 0;
+    b->aux_smem = sizeof(double) * (9 * max_leaf + (P.obj_staged ? max_ng : 0));
     // the dynamic shared-memory limits only grow (per device): every live batch
     // keeps launching with its own size
     {

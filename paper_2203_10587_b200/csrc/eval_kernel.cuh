@@ -860,13 +860,25 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
     // stage objective: numpy's pairwise sum over the ng cost terms (acopf.py:266-269).
     // The block first computes every term in parallel into shared memory (after
     // the leaves), so a leaf's sequential sum does not wait on global loads.
-    const double* tq = Q + T.nleaf;
+    // Q = [leaf sums | 8 partial sums per leaf | the staged cost terms]
+    double* R8 = Q + T.nleaf;
+    const double* tq = R8 + 8 * T.nleaf;
     if (P.obj_staged) {
-        double* tw = Q + T.nleaf;
+        double* tw = R8 + 8 * T.nleaf;
         for (int i = threadIdx.x; i < ng; i += blockDim.x) tw[i] = cost_term(P, S, pg, i);
         __syncthreads();
     }
     auto term = [&](int i) { return P.obj_staged ? tq[i] : cost_term(P, S, pg, i); };
+    // numpy's 8 accumulators of a leaf (r[j] over terms j, j + 8, ...) run on 8 threads
+    for (int l8 = threadIdx.x; l8 < 8 * T.nleaf; l8 += blockDim.x) {
+        const int l = l8 >> 3, j = l8 & 7;
+        const int st = T.leaf[2 * l], n = T.leaf[2 * l + 1];
+        if (n < 8) continue;
+        double r = term(st + j);
+        for (int i = 8; i < n - (n % 8); i += 8) r = r + term(st + i + j);
+        R8[l8] = r;
+    }
+    __syncthreads();
     for (int l = threadIdx.x; l < T.nleaf; l += blockDim.x) {
         const int st = T.leaf[2 * l], n = T.leaf[2 * l + 1];
         double res;
@@ -874,16 +886,9 @@ __device__ void gen_chunk(const EvalParams& P, int s, int chunk, double* Q) {
             res = 0.0;
             for (int i = 0; i < n; ++i) res = res + term(st + i);
         } else {
-            double r[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = term(st + j);
-            int i = 8;
-            for (; i < n - (n % 8); i += 8) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) r[j] = r[j] + term(st + i + j);
-            }
+            const double* r = R8 + 8 * l;
             res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-            for (; i < n; ++i) res = res + term(st + i);
+            for (int i = n - (n % 8); i < n; ++i) res = res + term(st + i);
         }
         Q[l] = res;
     }
