@@ -596,7 +596,7 @@ static void upload(acopf_batch* b) {
         const bool il = ie ? atoi(ie) != 0 : nbmax >= INTERLEAVE_MIN_BUSES;
         const char* ce = getenv("ACOPF_IL_CHUNKS");                // development aid
         const int nch = ce ? std::max(1, atoi(ce)) : 1;   // measured no gain: off by default
-        if (il && il_bytes > 256LL * 1048576 && nch > 1) {
+        if (il && (il_bytes > 256LL * 1048576 || ce) && nch > 1) {
             const int ngroups = (S + G - 1) / G;
             const int per = std::max(1, (ngroups + nch - 1) / nch);
             int item = 0;
