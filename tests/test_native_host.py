@@ -278,3 +278,28 @@ def test_native_graph_checks_match_the_python_restatements():
             c2 = replace(case, branches=tuple(replace(b, status=0) if i in rem else b
                                               for i, b in enumerate(case.branches)))
             assert Lt._islands_without(pc, sorted(rem)) == check_connectivity(c2)[0]
+
+
+def test_eval_host_rejects_short_or_missing_buffers_before_device_work():
+    """acopf_batch_eval_host validates every requested output against the layout:
+    a short buffer or a missing multiplier vector fails with a message, before any copy."""
+    import ctypes
+    from paper_2203_10587_b200 import _lib as L
+    p, _ = pkg.build_acopf(stage_case(STAGE_SPECS["stage_feat30"]))
+    ev = p.evaluator
+    x = np.zeros(ev.n)
+    short = np.zeros(max(ev.nnz_h - 1, 1))
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+    def call(what, nx=ev.n, mult=None, nm=0, h=None, nh=0, j=None, nj=0):
+        return L.lib().acopf_batch_eval_host(ev._h, vp(x), nx, 1.0, vp(mult), nm, what, None, 0, None, 0, None, 0,
+                                             vp(j), nj, vp(h), nh, None)
+
+    assert call(L.HESS, h=short, nh=len(short), mult=np.zeros(ev.m), nm=ev.m) != 0
+    assert b"hval" in L.lib().acopf_last_error()
+    assert call(L.HESS, h=np.zeros(ev.nnz_h), nh=ev.nnz_h) != 0
+    assert b"mult" in L.lib().acopf_last_error()
+    assert call(L.JAC, j=np.zeros(3), nj=3) != 0
+    assert b"jval" in L.lib().acopf_last_error()
+    assert call(L.JAC, nx=ev.n - 1, j=np.zeros(ev.nnz_j), nj=ev.nnz_j) != 0
+    assert b"x has" in L.lib().acopf_last_error()
