@@ -367,6 +367,8 @@ static void upload(acopf_batch* b) {
                         r.oA = d.h_base + st.tile_off[4 * t + 2]; r.oV = d.h_base + st.tile_off[4 * t + 3];
                         r.fl_off = d.fl_off; r.inj_off = d.inj_off; r.rem_off = d.rem_off;
                         r.w = d.w; r.nrem = d.nrem; r.nb = d.nb; r.ng = d.ng; r.nbr = d.nbr;
+                        if (d.nrem > 0) { r.rr0 = st.removed_rated[0]; r.rz0 = st.removed_rowsz[0]; }
+                        if (d.nrem > 1) { r.rr1 = st.removed_rated[1]; r.rz1 = st.removed_rowsz[1]; }
                         r.stage = s;
                         recs.push_back(r);
                     }

@@ -44,7 +44,9 @@ struct DBusItem {             // one warp (CTA) of the tile kernel: a table and 
 };
 
 // (stage, tile) record: everything the tile warp needs about one stage, with
-// absolute offsets; 128 bytes, prefetched into shared memory with cp.async
+// absolute offsets; 144 bytes, prefetched into shared memory by a TMA bulk copy.
+// The first two removed rated branches (index, flow-row size) are inline, so
+// the rated-row shifts of N-1 stages need no dependent global loads.
 struct alignas(16) DRec {
     long long var_off, eq_row, ineq_row, pd_off;
     long long jineq, oP, oQ, oA;          // J inequality block base; absolute segment offsets
@@ -52,8 +54,9 @@ struct alignas(16) DRec {
     double w;
     int nrem, nb, ng, nbr;
     int stage, pad;
+    int rr0, rz0, rr1, rz1;               // removed rated branches 0 and 1 (nrem <= 2)
 };
-static_assert(sizeof(DRec) == 128, "DRec layout");
+static_assert(sizeof(DRec) == 144, "DRec layout");
 
 struct DAuxItem {
     int kind;                 // 0 generator chunk (stage, chunk); 1 coupling runs [stage, stage + chunk)
@@ -160,10 +163,10 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 // (issued by one thread; generic-proxy reads of dst finished before a barrier).
 __device__ __forceinline__ void record_load(unsigned mb, void* dst, const void* src) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 128;" ::"r"(mb) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];" ::"r"(
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "n"((int)sizeof(DRec)) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
-                 "l"(src), "r"(mb)
+                 "l"(src), "n"((int)sizeof(DRec)), "r"(mb)
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned mb, unsigned parity) {
@@ -192,7 +195,13 @@ __device__ __forceinline__ void rated_shift(const EvalParams& P, const DRec& R, 
                                             long long& fo) {
     rs = r;
     fo = foff;
-    for (int i = 0; i < R.nrem; ++i) {
+    const int nrem = R.nrem;
+    if (nrem <= 2) {                          // inline in the record (N-1 and double outages)
+        if (nrem > 0 && R.rr0 < r) { rs--; fo -= R.rz0; }
+        if (nrem > 1 && R.rr1 < r) { rs--; fo -= R.rz1; }
+        return;
+    }
+    for (int i = 0; i < nrem; ++i) {
         if (__ldg(P.rem_ridx + R.rem_off + i) < r) { rs--; fo -= __ldg(P.rem_rowsz + R.rem_off + i); }
     }
 }
