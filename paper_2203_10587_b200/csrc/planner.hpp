@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -706,6 +707,56 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         }
         tt.nRJ = (int)rr.size();
         tt.nRH = 0;
+        // balance the rounds over the warps: the kernel's warp w runs positions w, w + W,
+        // ... two at a time (chains a and b of iteration i: w + 2iW and w + (2i+1)W), so an
+        // iteration costs its longer round.  Give each iteration's 2W positions the next 2W
+        // longest rounds, paired by length (similar chains), heaviest pair to the warp with
+        // the least work so far.
+        static const bool lpt = !getenv("ACOPF_ROUND_LPT") || atoi(getenv("ACOPF_ROUND_LPT")) != 0;
+        const int R = tt.nRJ, W = ACOPF_TILE_WARPS;
+        if (lpt && R > 2) {
+            std::vector<int> order(R);
+            for (int r = 0; r < R; ++r) order[r] = r;
+            std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tt.sround[4 * a + 1] > tt.sround[4 * b + 1]; });
+            std::vector<int> pos_of(R, -1);
+            std::vector<long long> load(W, 0);
+            int next_round = 0;
+            for (int it = 0; 2 * it * W < R; ++it) {
+                // positions of this iteration per warp: chain a p = w + 2 it W, chain b p + W
+                std::vector<std::pair<int, int>> slots;       // (warp, number of positions 1 or 2)
+                for (int w = 0; w < W; ++w) {
+                    const int pa = w + 2 * it * W, pb = pa + W;
+                    if (pa < R) slots.push_back({w, pb < R ? 2 : 1});
+                }
+                // pairs of rounds by length for the 2-position slots, singles for the rest
+                std::vector<std::vector<int>> jobs;
+                int n2 = 0, n1 = 0;
+                for (auto& sl : slots) (sl.second == 2 ? n2 : n1)++;
+                for (int k = 0; k < n2; ++k) { jobs.push_back({order[next_round], order[next_round + 1]}); next_round += 2; }
+                for (int k = 0; k < n1; ++k) jobs.push_back({order[next_round++]});
+                // heaviest job to the lightest warp among the slots that fit it
+                std::vector<char> used(slots.size(), 0);
+                for (auto& job : jobs) {
+                    int best = -1;
+                    for (size_t q = 0; q < slots.size(); ++q)
+                        if (!used[q] && slots[q].second == (int)job.size() && (best < 0 || load[slots[q].first] < load[slots[best].first]))
+                            best = (int)q;
+                    used[best] = 1;
+                    const int w = slots[best].first;
+                    pos_of[job[0]] = w + 2 * it * W;
+                    if (job.size() == 2) pos_of[job[1]] = w + (2 * it + 1) * W;
+                    load[w] += tt.sround[4 * job[0] + 1];
+                }
+            }
+            std::vector<uint16_t> sr(tt.sround.size()), sd(tt.sdst.size());
+            for (int r = 0; r < R; ++r) {
+                const int p = pos_of[r];
+                for (int k = 0; k < 4; ++k) sr[4 * p + k] = tt.sround[4 * r + k];
+                for (int l = 0; l < 32; ++l) sd[32 * p + l] = tt.sdst[32 * r + l];
+            }
+            tt.sround.swap(sr);
+            tt.sdst.swap(sd);
+        }
     }
     // generator set-points: Pg at gbase + g, Qg at gbase + ngl + g (tile order)
     for (int i = b0; i < b1; ++i) tt.ngl += T.gen_ptr[i + 1] - T.gen_ptr[i];
