@@ -403,7 +403,9 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
         flw[R.nbr] = fq;
     }
     const bool rated = in.rs >= 0;
+#ifndef ACOPF_DIAG_NO_GST
     if (rated && need_c) P.cons[R.ineq_row + 2 * in.rs + (int)sd] = fp * fp + fq * fq;
+#endif
     const int rb = V.rep[e];
     if (rb >= 0) {
         double pdv = 0.0, qdv = 0.0;
@@ -436,7 +438,11 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
         sts64(sA + (d2 >> 16), gq0);
         sts64(sA + (d3 & 0xffffu), -gq2);
         sts64(sA + (d3 >> 16), -gq3);
+#ifdef ACOPF_DIAG_NO_GST
+        if (false) {
+#else
         if (rated) {
+#endif
             const double tp = 2.0 * fp, tq = 2.0 * fq;
             const double r0 = (0.0 + tp * gp0) + tq * gq0, r1 = (0.0 + tp * (-gp0)) + tq * (-gq0);
             const double r2 = (0.0 + tp * gp2) + tq * gq2, r3 = (0.0 + tp * gp3) + tq * gq3;
@@ -463,7 +469,11 @@ __device__ __forceinline__ void end_eval(const EvalParams& P, const DRec& R, con
             }
         }
     }
+#ifdef ACOPF_DIAG_NO_H
+    if (false) {
+#else
     if (need_h) {
+#endif
         const double s2f = 2.0 * in.sf, s2t = 2.0 * in.st;
         const double cpf = (-in.mpf) + s2f * pf, cqf = (-in.mqf) + s2f * qf;
         const double cpt = (-in.mpt) + s2t * pt, cqt = (-in.mqt) + s2t * qt;
@@ -732,6 +742,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
 #else
             const int r1 = (need_j || need_h || need_c || need_f) ? H->nRJ + H->nRH : 0;
 #endif
+#if ACOPF_ROUND_CHAINS == 2
             for (int r = r0 + warp; r < r1; r += 2 * TILE_WARPS) {
                 const bool two = r + TILE_WARPS < r1;
                 const int rb = two ? r + TILE_WARPS : r;
@@ -753,6 +764,37 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
                 A[oa] = va;
                 if (two) A[ob] = vb;
             }
+#else
+            constexpr int NC = ACOPF_ROUND_CHAINS;
+            for (int r = r0 + warp; r < r1; r += NC * TILE_WARPS) {
+                const double* rp[NC];
+                double v[NC];
+                unsigned o[NC];
+                int c[NC], w[NC], n = 0;
+#pragma unroll
+                for (int k = 0; k < NC; ++k) {
+                    const int rk = r + k * TILE_WARPS;
+                    const bool on = rk < r1;
+                    const uint2 d = *reinterpret_cast<const uint2*>(sround + 4 * (on ? rk : r));
+                    o[k] = sdst[32 * (on ? rk : r) + lane];
+                    c[k] = on ? (int)(d.x >> 16) : 0;
+                    rp[k] = A + (d.x & 0xffffu) + lane;
+                    w[k] = d.y & 0xffffu;
+                    n = c[k] > n ? c[k] : n;
+                }
+#pragma unroll
+                for (int k = 0; k < NC; ++k) v[k] = rp[k][0];
+#pragma unroll 2
+                for (int j = 1; j < n; ++j) {
+#pragma unroll
+                    for (int k = 0; k < NC; ++k)
+                        if (j < c[k]) v[k] = v[k] + rp[k][j * w[k]];
+                }
+#pragma unroll
+                for (int k = 0; k < NC; ++k)
+                    if (c[k] > 0) A[o[k]] = v[k];
+            }
+#endif
         }
         // staging writes (generic proxy) before the bulk stores read them (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -65,6 +65,10 @@ constexpr int HSLOT_T[10] = {-1, 1, -1, 2, 0, 3, 5, -1, 4, 6};
 #ifndef ACOPF_TILE_ENDS
 #define ACOPF_TILE_ENDS (32 * ACOPF_TILE_WARPS)
 #endif
+// sum rounds a warp runs together (independent add chains per lane)
+#ifndef ACOPF_ROUND_CHAINS
+#define ACOPF_ROUND_CHAINS 2
+#endif
 #ifndef ACOPF_TILE_BUSES
 #define ACOPF_TILE_BUSES 64
 #endif
@@ -708,12 +712,12 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
         tt.nRJ = (int)rr.size();
         tt.nRH = 0;
         // balance the rounds over the warps: the kernel's warp w runs positions w, w + W,
-        // ... two at a time (chains a and b of iteration i: w + 2iW and w + (2i+1)W), so an
-        // iteration costs its longer round.  Give each iteration's 2W positions the next 2W
-        // longest rounds, paired by length (similar chains), heaviest pair to the warp with
-        // the least work so far.
+        // ... C at a time (chain c of iteration i: w + (Ci + c)W), so an iteration costs
+        // its longest round.  Give each iteration's CW positions the next CW longest
+        // rounds, grouped by length (similar chains), heaviest group to the warp with the
+        // least work so far.
         static const bool lpt = !getenv("ACOPF_ROUND_LPT") || atoi(getenv("ACOPF_ROUND_LPT")) != 0;
-        const int R = tt.nRJ, W = ACOPF_TILE_WARPS;
+        const int R = tt.nRJ, W = ACOPF_TILE_WARPS, C = ACOPF_ROUND_CHAINS;
         if (lpt && R > 2) {
             std::vector<int> order(R);
             for (int r = 0; r < R; ++r) order[r] = r;
@@ -721,19 +725,24 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
             std::vector<int> pos_of(R, -1);
             std::vector<long long> load(W, 0);
             int next_round = 0;
-            for (int it = 0; 2 * it * W < R; ++it) {
-                // positions of this iteration per warp: chain a p = w + 2 it W, chain b p + W
-                std::vector<std::pair<int, int>> slots;       // (warp, number of positions 1 or 2)
+            for (int it = 0; C * it * W < R; ++it) {
+                // positions of this iteration per warp: w + (C it + c) W for c < C inside [0, R)
+                std::vector<std::pair<int, int>> slots;       // (warp, number of positions)
                 for (int w = 0; w < W; ++w) {
-                    const int pa = w + 2 * it * W, pb = pa + W;
-                    if (pa < R) slots.push_back({w, pb < R ? 2 : 1});
+                    int k = 0;
+                    while (k < C && w + (C * it + k) * W < R) ++k;
+                    if (k > 0) slots.push_back({w, k});
                 }
-                // pairs of rounds by length for the 2-position slots, singles for the rest
+                // groups of consecutive (by length) rounds, the larger slots first
+                std::vector<int> sizes;
+                for (auto& sl : slots) sizes.push_back(sl.second);
+                std::sort(sizes.rbegin(), sizes.rend());
                 std::vector<std::vector<int>> jobs;
-                int n2 = 0, n1 = 0;
-                for (auto& sl : slots) (sl.second == 2 ? n2 : n1)++;
-                for (int k = 0; k < n2; ++k) { jobs.push_back({order[next_round], order[next_round + 1]}); next_round += 2; }
-                for (int k = 0; k < n1; ++k) jobs.push_back({order[next_round++]});
+                for (int sz : sizes) {
+                    std::vector<int> job;
+                    for (int k = 0; k < sz; ++k) job.push_back(order[next_round++]);
+                    jobs.push_back(job);
+                }
                 // heaviest job to the lightest warp among the slots that fit it
                 std::vector<char> used(slots.size(), 0);
                 for (auto& job : jobs) {
@@ -743,8 +752,7 @@ inline TileTable build_tile(const Topo& T, int tile, const Live& live) {
                             best = (int)q;
                     used[best] = 1;
                     const int w = slots[best].first;
-                    pos_of[job[0]] = w + 2 * it * W;
-                    if (job.size() == 2) pos_of[job[1]] = w + (2 * it + 1) * W;
+                    for (size_t k = 0; k < job.size(); ++k) pos_of[job[k]] = w + (C * it + (int)k) * W;
                     load[w] += tt.sround[4 * job[0] + 1];
                 }
             }
