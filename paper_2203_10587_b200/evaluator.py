@@ -189,11 +189,11 @@ class BatchEvaluator:
             first = np.zeros(1, dtype=np.int8)
             ncp = 0
         slots = L.i32(obj_slot)
-        self._keep = (rows, jpos, ca, cb, first)
         L.check(L.lib().acopf_batch_set_layout(
             self._h, L.ptr(off6, ctypes.c_int64), obj_mode, L.ptr(slots, ctypes.c_int32), ncp,
             L.ptr(rows, ctypes.c_int64), L.ptr(jpos, ctypes.c_int64), L.ptr(ca, ctypes.c_int64),
             L.ptr(cb, ctypes.c_int64), L.ptr(first, ctypes.c_int8)))
+        # (the library keeps its own copies of the coupling arrays)
 
     # -- patterns ---------------------------------------------------------------
 
