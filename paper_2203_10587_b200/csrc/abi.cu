@@ -1558,13 +1558,17 @@ int acopf_batch_eval_multi(acopf_multi* m, double* x, double obj_factor, const d
             }
             cuda_check(cudaEventRecord(m->ev_halo, hs), "event record");
         }
-        // generator chunks (gradient, PG Hessian diagonal, w_s f_s) beside the tile kernel
-        const bool gen = (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS)) && b->n_gen_items > 0;
+        // generator chunks (gradient, PG Hessian diagonal, w_s f_s) beside the tile kernel;
+        // the objective all-gather is issued by every rank whenever the objective is asked
+        // (collectives must match across ranks, even for a rank without generator items)
+        const bool gen = (what & (ACOPF_OBJ | ACOPF_GRAD | ACOPF_HESS)) && (b->n_gen_items > 0 || (what & ACOPF_OBJ));
         if (gen) {
             cuda_check(cudaStreamWaitEvent(b->aux_stream, m->ev_fork, 0), "stream wait");
-            acopf_aux_kernel<<<b->n_gen_items, BLOCK, b->aux_smem, b->aux_stream>>>(P, 0);
-            cuda_check(cudaGetLastError(), "acopf_aux_kernel (generators) launch");
-            b->launches++;
+            if (b->n_gen_items > 0) {
+                acopf_aux_kernel<<<b->n_gen_items, BLOCK, b->aux_smem, b->aux_stream>>>(P, 0);
+                cuda_check(cudaGetLastError(), "acopf_aux_kernel (generators) launch");
+                b->launches++;
+            }
             if (what & ACOPF_OBJ) {
                 // every rank's terms, then the stage-order sum (bit-identical to one GPU)
                 nccl_check(nccl().AllGather(m->d_obj_send.p, m->d_obj_recv.p, (size_t)m->obj_max, ncclDouble, m->comm,
