@@ -344,7 +344,13 @@ static void upload(acopf_batch* b) {
     // item, instead of several short items paying the table load and the first gathers
     // each (measured cfg3 0.0594 -> 0.0534 ms; larger workloads keep the waves above, whose
     // dynamic scheduling balances the unequal tiles)
-    const int64_t slots = (int64_t)n_sm * (WARP_MINB / TILE_WARPS);
+    // resident tile CTAs per SM: the register budget's WARP_MINB / TILE_WARPS, fewer when the
+    // largest table's shared memory (+1 KB reserved per CTA) does not fit that many
+    size_t smem_all = 0;
+    for (size_t i = 0; i < b->tables.size(); ++i)
+        smem_all = std::max(smem_all, tile_smem_bytes(table_bytes[i], b->tables[i].nArea + table_shift_n[i]));
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(WARP_MINB / TILE_WARPS, 233472 / (int64_t)(smem_all + 1024 + 256)));
+    const int64_t slots = (int64_t)n_sm * per_sm;
     if (total_recs > 0 && total_recs <= 12 * slots) {
         auto count_items = [&](int g) {
             int64_t n = 0;
