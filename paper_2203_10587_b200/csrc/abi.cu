@@ -151,7 +151,30 @@ struct acopf_batch {
     cudaStream_t aux_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_il = nullptr, ev_ilj[2] = {nullptr, nullptr};
+    // CUDA graphs of single-stream host evaluations (acopf_batch_eval_host without the
+    // chunked pipeline, on the library's stream, pinned host buffers): one per (what,
+    // multipliers given, sizes, staging buffers); the host ends of its copies are patched
+    // per call, so a batch-1 callback is one graph launch instead of 4-6 API calls
+    struct HostGraph {
+        uint32_t what = 0;
+        bool mult = false;
+        double obj_factor = 0.0;
+        int64_t sz[7] = {};                       // x, mult, obj, grad, cons, jac, hess (doubles)
+        const void* dev[7] = {};                  // the device staging buffers captured
+        const void* host[7] = {};                 // host pointers the copies currently use
+        cudaGraphNode_t node[7] = {};
+        cudaMemcpy3DParms parm[7] = {};           // the captured copy parameters (host end patched)
+        cudaGraph_t graph = nullptr;             // kept: its node handles address the exec's copies
+        cudaGraphExec_t exec = nullptr;
+        int64_t n_launches = 0;
+    };
+    std::vector<HostGraph> host_graphs;
+    bool host_graphs_off = false;
     ~acopf_batch() {
+        for (auto& g : host_graphs) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            if (g.graph) cudaGraphDestroy(g.graph);
+        }
         for (cudaEvent_t e : {ev_il, ev_ilj[0], ev_ilj[1]}) if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
         if (aux_stream) cudaStreamDestroy(aux_stream);
@@ -1009,6 +1032,11 @@ int acopf_batch_set_layout(acopf_batch* b, const int64_t* offsets6, int32_t obj_
         b->tot_n = tn; b->tot_m = tm; b->tot_j = tj; b->tot_h = th; b->tot_obj = to;
         b->laid_out = true;
         b->uploaded = false;
+        for (auto& g : b->host_graphs) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            if (g.graph) cudaGraphDestroy(g.graph);
+        }
+        b->host_graphs.clear();
     });
 }
 
@@ -1302,15 +1330,112 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
             cuda_check(cudaStreamSynchronize(st), "stream sync");
             return;
         }
-        if (x && nx) cuda_check(cudaMemcpyAsync(dx, x, 8 * nx, cudaMemcpyHostToDevice, st), "H2D x");
-        if (mult && nm) cuda_check(cudaMemcpyAsync(dm, mult, 8 * nm, cudaMemcpyHostToDevice, st), "H2D mult");
-        if (acopf_batch_eval(b, dx, obj_factor, mult ? dm : nullptr, what, dobj, dg, dc, dj, dh, st) != 0)
-            throw std::runtime_error(g_err);
-        if ((what & ACOPF_OBJ) && obj) cuda_check(cudaMemcpyAsync(obj, dobj, 8 * nobj, cudaMemcpyDeviceToHost, st), "D2H obj");
-        if ((what & ACOPF_GRAD) && grad) cuda_check(cudaMemcpyAsync(grad, dg, 8 * ngrad, cudaMemcpyDeviceToHost, st), "D2H grad");
-        if ((what & ACOPF_CONS) && cons) cuda_check(cudaMemcpyAsync(cons, dc, 8 * ncons, cudaMemcpyDeviceToHost, st), "D2H cons");
-        if ((what & ACOPF_JAC) && jval) cuda_check(cudaMemcpyAsync(jval, dj, 8 * nj, cudaMemcpyDeviceToHost, st), "D2H jac");
-        if ((what & ACOPF_HESS) && hval) cuda_check(cudaMemcpyAsync(hval, dh, 8 * nh, cudaMemcpyDeviceToHost, st), "D2H hess");
+        // the copies and kernels of one evaluation; slot k of `hp` / `dp` / `nb` / `dir` is
+        // x, mult, obj, grad, cons, jac, hess
+        const void* hp[7] = {x, mult, obj, grad, cons, jval, hval};
+        const void* dp[7] = {dx, dm, dobj, dg, dc, dj, dh};
+        const int64_t sz[7] = {nx, nm, nobj, ngrad, ncons, nj, nh};
+        const bool on[7] = {x && nx > 0, mult && nm > 0, (what & ACOPF_OBJ) && obj, (what & ACOPF_GRAD) && grad,
+                            (what & ACOPF_CONS) && cons, (what & ACOPF_JAC) && jval, (what & ACOPF_HESS) && hval};
+        auto issue = [&]() {
+            for (int k = 0; k < 2; ++k)
+                if (on[k]) cuda_check(cudaMemcpyAsync(const_cast<void*>(dp[k]), hp[k], 8 * sz[k], cudaMemcpyHostToDevice, st), "H2D");
+            if (acopf_batch_eval(b, dx, obj_factor, mult ? dm : nullptr, what, dobj, dg, dc, dj, dh, st) != 0)
+                throw std::runtime_error(g_err);
+            for (int k = 2; k < 7; ++k)
+                if (on[k]) cuda_check(cudaMemcpyAsync(const_cast<void*>(hp[k]), dp[k], 8 * sz[k], cudaMemcpyDeviceToHost, st), "D2H");
+        };
+        static const bool graphs_env = !getenv("ACOPF_HOST_GRAPHS") || atoi(getenv("ACOPF_HOST_GRAPHS")) != 0;
+        bool use_graph = graphs_env && !b->host_graphs_off && st == b->stream;
+        for (int k = 0; k < 7 && use_graph; ++k) {      // graph copies need pinned host memory
+            if (!on[k]) continue;
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, hp[k]) != cudaSuccess || a.type != cudaMemoryTypeHost) {
+                cudaGetLastError();
+                use_graph = false;
+            }
+        }
+        if (!use_graph) {
+            issue();
+            cuda_check(cudaStreamSynchronize(st), "stream sync");
+            return;
+        }
+        acopf_batch::HostGraph* g = nullptr;
+        for (auto& h : b->host_graphs) {
+            bool same = h.what == what && h.mult == (mult != nullptr) && h.obj_factor == obj_factor;
+            for (int k = 0; k < 7 && same; ++k) same = h.sz[k] == (on[k] ? sz[k] : 0) && h.dev[k] == (on[k] ? dp[k] : nullptr);
+            if (same) { g = &h; break; }
+        }
+        if (!g) {
+            if (b->host_graphs.size() >= 16) {     // bounded cache (e.g. a varying obj_factor)
+                for (auto& o : b->host_graphs) {
+                    if (o.exec) cudaGraphExecDestroy(o.exec);
+                    if (o.graph) cudaGraphDestroy(o.graph);
+                }
+                b->host_graphs.clear();
+            }
+            acopf_batch::HostGraph h;
+            h.what = what; h.mult = mult != nullptr; h.obj_factor = obj_factor;
+            for (int k = 0; k < 7; ++k) { h.sz[k] = on[k] ? sz[k] : 0; h.dev[k] = on[k] ? dp[k] : nullptr; h.host[k] = on[k] ? hp[k] : nullptr; }
+            const int64_t l0 = b->launches;
+            cudaGraph_t graph = nullptr;
+            bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                try { issue(); } catch (...) { ok = false; }
+                ok = cudaStreamEndCapture(st, &graph) == cudaSuccess && ok;
+            }
+            h.n_launches = b->launches - l0;
+            b->launches = l0;
+            if (ok) {       // the memcpy nodes, by their device ends
+                size_t n = 0;
+                ok = cudaGraphGetNodes(graph, nullptr, &n) == cudaSuccess;
+                std::vector<cudaGraphNode_t> nodes(n);
+                if (ok && n) ok = cudaGraphGetNodes(graph, nodes.data(), &n) == cudaSuccess;
+                for (size_t i = 0; i < n && ok; ++i) {
+                    cudaGraphNodeType t;
+                    if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess) { ok = false; break; }
+                    if (t != cudaGraphNodeTypeMemcpy) continue;
+                    cudaMemcpy3DParms mp{};
+                    if (cudaGraphMemcpyNodeGetParams(nodes[i], &mp) != cudaSuccess) { ok = false; break; }
+                    for (int k = 0; k < 7; ++k)
+                        if (on[k] && (k < 2 ? mp.dstPtr.ptr : mp.srcPtr.ptr) == dp[k]) { h.node[k] = nodes[i]; h.parm[k] = mp; }
+                }
+                for (int k = 0; k < 7 && ok; ++k) ok = !on[k] || h.node[k] != nullptr;
+                if (ok) ok = cudaGraphInstantiate(&h.exec, graph, 0) == cudaSuccess;
+            }
+            cudaGetLastError();
+            if (!ok) {          // capture not possible here: plain issue from now on
+                if (h.exec) cudaGraphExecDestroy(h.exec);
+                if (graph) cudaGraphDestroy(graph);
+                b->host_graphs_off = true;
+                issue();
+                cuda_check(cudaStreamSynchronize(st), "stream sync");
+                return;
+            }
+            h.graph = graph;
+            b->host_graphs.push_back(h);
+            g = &b->host_graphs.back();
+        }
+        for (int k = 0; k < 7; ++k) {           // patch the host ends that moved
+            if (!on[k] || g->host[k] == hp[k]) continue;
+            cudaMemcpy3DParms mp = g->parm[k];
+            if (k < 2) mp.srcPtr.ptr = const_cast<void*>(hp[k]);
+            else mp.dstPtr.ptr = const_cast<void*>(hp[k]);
+            const cudaError_t ue = cudaGraphExecMemcpyNodeSetParams(g->exec, g->node[k], &mp);
+            if (ue != cudaSuccess && getenv("ACOPF_DEBUG_GRAPHS")) {
+                cudaPointerAttributes a0{}, a1{};
+                cudaPointerGetAttributes(&a0, g->host[k]);
+                cudaPointerGetAttributes(&a1, hp[k]);
+                fprintf(stderr, "graph update k=%d %s: old %p (type %d dev %d) new %p (type %d dev %d) bytes %lld extent %zu/%zu/%zu kind %d src %p dst %p\n",
+                        k, cudaGetErrorString(ue), g->host[k], (int)a0.type, a0.device, hp[k], (int)a1.type, a1.device,
+                        (long long)(8 * sz[k]), mp.extent.width, mp.extent.height, mp.extent.depth, (int)mp.kind, mp.srcPtr.ptr,
+                        mp.dstPtr.ptr);
+            }
+            cuda_check(ue, "graph copy update");
+            g->host[k] = hp[k];
+        }
+        cuda_check(cudaGraphLaunch(g->exec, st), "cudaGraphLaunch");
+        b->launches += g->n_launches;
         cuda_check(cudaStreamSynchronize(st), "stream sync");
     });
 }
