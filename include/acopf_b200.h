@@ -112,7 +112,9 @@ int acopf_batch_eval(acopf_batch* b, const double* x, double obj_factor, const d
  * stream; its device buffers are internal), then synchronises that stream.
  * Layouts whose stages are contiguous and in order (independent points) are
  * pipelined in chunks over three streams; any other layout runs as one
- * H2D / evaluate / D2H sequence. */
+ * H2D / evaluate / D2H sequence, which on the handle's own stream with pinned
+ * host buffers is captured once per (what, sizes) as a CUDA graph and replayed
+ * with its host pointers patched (ACOPF_HOST_GRAPHS=0 disables this). */
 int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double obj_factor,
                           const double* mult, int64_t nm, uint32_t what, double* obj, int64_t nobj,
                           double* grad, int64_t ngrad, double* cons, int64_t ncons, double* jval,
