@@ -31,7 +31,9 @@
  * the handle's device.  Evaluation is stream-ordered on the given stream
  * (NULL = the legacy default stream, CUDA's convention; torch's default
  * stream is that stream); one handle must not be evaluated concurrently from
- * two streams (it owns one objective scratch buffer).
+ * two streams or two host threads (it owns one objective scratch buffer, the
+ * host-evaluation staging buffers and their graphs); callers serialise per
+ * handle (the Python layer holds a lock).
  */
 #ifndef ACOPF_B200_H
 #define ACOPF_B200_H
