@@ -1416,23 +1416,27 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
             b->host_graphs.push_back(h);
             g = &b->host_graphs.back();
         }
-        for (int k = 0; k < 7; ++k) {           // patch the host ends that moved
+        bool patched = true;
+        for (int k = 0; k < 7 && patched; ++k) {   // patch the host ends that moved
             if (!on[k] || g->host[k] == hp[k]) continue;
             cudaMemcpy3DParms mp = g->parm[k];
             if (k < 2) mp.srcPtr.ptr = const_cast<void*>(hp[k]);
             else mp.dstPtr.ptr = const_cast<void*>(hp[k]);
             const cudaError_t ue = cudaGraphExecMemcpyNodeSetParams(g->exec, g->node[k], &mp);
-            if (ue != cudaSuccess && getenv("ACOPF_DEBUG_GRAPHS")) {
-                cudaPointerAttributes a0{}, a1{};
-                cudaPointerGetAttributes(&a0, g->host[k]);
-                cudaPointerGetAttributes(&a1, hp[k]);
-                fprintf(stderr, "graph update k=%d %s: old %p (type %d dev %d) new %p (type %d dev %d) bytes %lld extent %zu/%zu/%zu kind %d src %p dst %p\n",
-                        k, cudaGetErrorString(ue), g->host[k], (int)a0.type, a0.device, hp[k], (int)a1.type, a1.device,
-                        (long long)(8 * sz[k]), mp.extent.width, mp.extent.height, mp.extent.depth, (int)mp.kind, mp.srcPtr.ptr,
-                        mp.dstPtr.ptr);
+            if (ue != cudaSuccess) {
+                if (getenv("ACOPF_DEBUG_GRAPHS"))
+                    fprintf(stderr, "acopf: graph copy update k=%d: %s; plain copies from now on\n", k, cudaGetErrorString(ue));
+                cudaGetLastError();
+                patched = false;
+                break;
             }
-            cuda_check(ue, "graph copy update");
             g->host[k] = hp[k];
+        }
+        if (!patched) {        // e.g. host memory from another allocator: the plain sequence
+            b->host_graphs_off = true;
+            issue();
+            cuda_check(cudaStreamSynchronize(st), "stream sync");
+            return;
         }
         cuda_check(cudaGraphLaunch(g->exec, st), "cudaGraphLaunch");
         b->launches += g->n_launches;
