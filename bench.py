@@ -506,20 +506,51 @@ def main():
             del out, outs               # the device outputs are not needed any more (HBM for the host path)
         hout = {k: torch.empty(max(n, 1), dtype=torch.float64).pin_memory()[:n] for k, n in sizes.items()}
 
+        if sc is not None:
+            # sharded: steps pipelined over two device buffer sets -- step k + 1's H2D (copy-in
+            # stream) and step k's D2H (copy-out stream) overlap the other's evaluation, the
+            # way the one-GPU host entry point overlaps its chunks
+            s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+            xb, mb = [x, torch.empty_like(x)], [mult, torch.empty_like(mult)]
+            ob = [out, ev.alloc()]
+            objb = [torch.empty(1, dtype=torch.float64, device=dev) for _ in range(2)]
+            ev_in, ev_cmp, ev_out = ([torch.cuda.Event() for _ in range(2)] for _ in range(3))
+            for b in range(2):
+                ev_cmp[b].record(stream)
+                ev_out[b].record(stream)
+            pstate = [0]
+
         def e2e_step():
             if sc is None:
                 ev.eval_host_ptrs(xp.data_ptr(), mp_.data_ptr(), 1.0, L.ALL, hout, stream=sptr)
                 return
-            x.copy_(xp, non_blocking=True)
-            mult.copy_(mp_, non_blocking=True)
-            _, obj = sc.evaluate(x, mult, 1.0, L.ALL, out=out, stream=sptr)
-            for k in ("grad", "cons", "jac", "hess"):
-                hout[k].copy_(out[k][:sizes[k]], non_blocking=True)
-            hout["obj"][:1].copy_(obj, non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
+            b = pstate[0] % 2
+            pstate[0] += 1
+            s_in.wait_event(ev_cmp[b])                 # step k - 2 has finished reading set b
+            with torch.cuda.stream(s_in):
+                xb[b][:len(x_h)].copy_(xp, non_blocking=True)
+                mb[b].copy_(mp_, non_blocking=True)
+            ev_in[b].record(s_in)
+            stream.wait_event(ev_in[b])
+            stream.wait_event(ev_out[b])               # step k - 2's outputs are on the host
+            _, obj = sc.evaluate(xb[b], mb[b], 1.0, L.ALL, out=ob[b], stream=sptr)
+            objb[b].copy_(obj.reshape(-1)[:1])
+            ev_cmp[b].record(stream)
+            s_out.wait_event(ev_cmp[b])
+            with torch.cuda.stream(s_out):
+                for k in ("grad", "cons", "jac", "hess"):
+                    hout[k].copy_(ob[b][k][:sizes[k]], non_blocking=True)
+                hout["obj"][:1].copy_(objb[b], non_blocking=True)
+            ev_out[b].record(s_out)
+
+        def e2e_drain():
+            if sc is not None:
+                for b in range(2):
+                    stream.wait_event(ev_out[b])
 
         for _ in range(2):
             e2e_step()
+        e2e_drain()
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -528,6 +559,7 @@ def main():
         es.record(stream)
         for k in range(e_steps):
             e2e_step()
+        e2e_drain()
         ee.record(stream)
         torch.cuda.synchronize(dev)
         e_ms = torch.tensor([es.elapsed_time(ee)], dtype=torch.float64, device=dev)
@@ -540,7 +572,8 @@ def main():
                "h2d_bytes_per_step": int(bytes_io[0].item()),
                "d2h_bytes_per_step": int(bytes_io[1].item()),
                "path": ("acopf_batch_eval_host (C ABI) on pinned host buffers" if sc is None else
-                        "per rank: pinned H2D of its shard, acopf_batch_eval_multi, pinned D2H of its outputs")
+                        "per rank: pinned H2D of its shard, acopf_batch_eval_multi, pinned D2H of its outputs, "
+                        "steps pipelined over two device buffer sets")
                        + f", {e_steps} steps back to back"}
 
     cpu = None
