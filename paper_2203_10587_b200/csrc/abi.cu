@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <queue>
 #include <mutex>
 #include <thread>
 #include <atomic>
@@ -362,11 +363,6 @@ static void upload(acopf_batch* b) {
     std::vector<std::pair<int, int>> tiles;       // (topo, tile)
     for (size_t ti = 0; ti < b->topos.size(); ++ti)
         for (size_t t = 0; t < b->base_table[ti].size(); ++t) tiles.push_back({(int)ti, (int)t});
-    // small workloads (<= 12 tile-stages per resident CTA slot, e.g. cfg3): the smallest G
-    // whose items all fit one wave -- each CTA then loads its table once and runs one long
-    // item, instead of several short items paying the table load and the first gathers
-    // each (measured cfg3 0.0594 -> 0.0534 ms; larger workloads keep the waves above, whose
-    // dynamic scheduling balances the unequal tiles)
     // resident tile CTAs per SM: the register budget's WARP_MINB / TILE_WARPS, fewer when the
     // largest table's shared memory (+1 KB reserved per CTA) does not fit that many
     size_t smem_all = 0;
@@ -374,23 +370,70 @@ static void upload(acopf_batch* b) {
         smem_all = std::max(smem_all, tile_smem_bytes(table_bytes[i], b->tables[i].nArea + table_shift_n[i]));
     const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(WARP_MINB / TILE_WARPS, 233472 / (int64_t)(smem_all + 1024 + 256)));
     const int64_t slots = (int64_t)n_sm * per_sm;
-    if (total_recs > 0 && total_recs <= 12 * slots) {
-        auto count_items = [&](int g) {
-            int64_t n = 0;
-            std::vector<int> seen;
-            for (int g0 = 0; g0 < S; g0 += g)
+    // The run length G by a list-scheduling model of the block scheduler: items in launch
+    // order (stage-group-major), each to the earliest-free CTA slot, an item costing its
+    // stage count plus a fixed 0.3 stage (table load, first gathers); G minimises the
+    // modelled makespan within the L2 cap (ties: the longer runs).  The model tracks the
+    // measured cfg1 times over G = 7..50 (correlation 0.97): wave quantisation, not the
+    // per-item cost alone, decides (cfg1 G = 20: +11%, G = 24: -3.5%); small workloads come
+    // out as one wave of long items (cfg3: 10 stages, 430 items for 444 slots).
+    {
+        const char* me = getenv("ACOPF_G_MODEL");            // development aid: 0 = the rule above
+        const bool model = me ? atoi(me) != 0 : true;
+        const int g_hi = (int)std::max<int64_t>(1, std::min<int64_t>(g_max, g_l2));
+        // items a run length makes (tile x group x distinct table)
+        int64_t n_items_g = 0;
+        auto makespan = [&](int g) {
+            n_items_g = 0;
+            std::priority_queue<double, std::vector<double>, std::greater<double>> free_at;
+            for (int64_t k = 0; k < slots; ++k) free_at.push(0.0);
+            double end = 0.0;
+            std::vector<int> tb;
+            for (int g0 = 0; g0 < S; g0 += g) {
+                const int g1 = std::min(S, g0 + g);
                 for (auto [topo, t] : tiles) {
-                    seen.clear();
-                    for (int s = g0; s < std::min(S, g0 + g); ++s)
-                        if (b->stages[s].topo == topo) seen.push_back(b->stages[s].table[t]);
-                    std::sort(seen.begin(), seen.end());
-                    n += std::unique(seen.begin(), seen.end()) - seen.begin();
+                    tb.clear();
+                    for (int s = g0; s < g1; ++s)
+                        if (b->stages[s].topo == topo) tb.push_back(b->stages[s].table[t]);
+                    std::sort(tb.begin(), tb.end());
+                    for (size_t a = 0; a < tb.size();) {
+                        size_t e = a;
+                        while (e < tb.size() && tb[e] == tb[a]) ++e;
+                        const double t0 = free_at.top() + (double)(e - a) + 0.3;
+                        free_at.pop();
+                        free_at.push(t0);
+                        ++n_items_g;
+                        end = std::max(end, t0);
+                        a = e;
+                    }
                 }
-            return n;
+            }
+            return end;
         };
-        const int g_hi = (int)std::min<int64_t>(g_max, g_l2);
-        for (int g = (int)std::max<int64_t>(1, (total_recs + slots - 1) / slots); g <= g_hi && g <= 2 * (total_recs / slots + 1); ++g)
-            if (count_items(g) <= slots) { G = g; break; }
+        if (model && total_recs > 0 && !tiles.empty()) {
+            // candidates: every G up to the cap for small workloads, else around the rule's G
+            // one wave of long items only for small workloads (<= 12 tile-stages per slot);
+            // otherwise at least two items per slot, so the dynamic scheduling can absorb the
+            // tiles' unequal stage times the model does not see (cfg1 G = 48/50: 1.4 waves, +4%)
+            const bool small = total_recs <= 64 * slots, tiny = total_recs <= 12 * slots;
+            const int lo = small ? 1 : std::max(1, G / 3), hi = small ? g_hi : std::min(g_hi, 4 * G);
+            // (the rule's G stays unless the model predicts at least 1% less: cfg2 G = 13 was
+            // modelled 0.6% faster and measured 0.3% slower)
+            const int G_rule = G;
+            const double rule = makespan(G_rule) * ((!tiny && n_items_g < 2 * slots) ? 1e9 : 1.0);
+            double best = 1e300;
+            int G_best = G_rule;
+            for (int g = lo; g <= hi; ++g) {
+                const double m = makespan(g);
+                if (!tiny && n_items_g < 2 * slots) continue;
+                if (m < best * 0.995 || (m <= best * 1.005 && g > G_best)) { best = m; G_best = g; }
+            }
+            if (best < rule * 0.99) G = G_best;
+            else best = rule;
+            if (getenv("ACOPF_DEBUG_PLAN"))
+                fprintf(stderr, "plan: run length G = %d (modelled makespan %.1f stage-times, %lld slots)\n", G, best,
+                        (long long)slots);
+        }
     }
     if (const char* ge = getenv("ACOPF_G")) G = std::max(1, atoi(ge));      // development aid: exact G
     std::vector<int> table_area(b->tables.size());
