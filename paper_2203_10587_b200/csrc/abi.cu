@@ -333,8 +333,8 @@ static void upload(acopf_batch* b) {
         fl_off += 4LL * b->topos[st.topo]->nbr;
         inj_off += 2LL * b->topos[st.topo]->nb;
     }
-    // tile work: for every tile, the stages sharing one table, in chunks of G
-    // stages; about 4 warps' worth of items per resident warp slot
+    // tile work: for every tile, the stages sharing one table, in groups of G consecutive
+    // stages (G: the starting rule below, then the makespan model further down)
     int64_t total_recs = 0;
     for (const StageInfo& st : b->stages) total_recs += (int64_t)st.table.size();
     // stages per item: enough items to fill the GPU a few times over, and few
@@ -355,8 +355,8 @@ static void upload(acopf_batch* b) {
     const int64_t g_l2 = std::max<int64_t>(1, (int64_t)(l2_budget / std::max(1.0, per_stage)));
     const char* genv = getenv("ACOPF_MAX_G");          // development aid
     const int64_t g_max = genv ? std::max(1, atoi(genv)) : 64;
-    // at least two stages per item where the L2 budget allows (one-stage items
-    // pay the table load per stage)
+    // starting rule: about 6 items per resident CTA slot, at least two stages per item where
+    // the L2 budget allows (one-stage items pay the table load per stage)
     int G = (int)std::max<int64_t>(std::min<int64_t>(2, g_l2),
                                    std::min<int64_t>({g_max, total_recs / target_items, g_l2}));
     size_t max_smem = 0;
