@@ -112,7 +112,10 @@ struct EvalParams {
 #endif
 constexpr int BLOCK = 256;                     // aux kernel
 constexpr int WARP_MINB = ACOPF_WARP_MINB;     // resident warps per SM the tile kernel is built for
-constexpr int GEN_CHUNK = 256;
+#ifndef ACOPF_GEN_CHUNK
+#define ACOPF_GEN_CHUNK 256
+#endif
+constexpr int GEN_CHUNK = ACOPF_GEN_CHUNK;
 constexpr int CP_CHUNK = 1024;
 constexpr int INTERLEAVE_MIN_BUSES = 4096;
 constexpr int IL_BUSES = 4;                     // buses per thread of acopf_interleave_kernel     // interleaved bus inputs from this network size on
