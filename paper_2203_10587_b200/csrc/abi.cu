@@ -452,6 +452,7 @@ static void upload(acopf_batch* b) {
                     DBusItem it{};
                     it.blob_off = table_off[kv.first];
                     it.bytes = table_bytes[kv.first];
+                    it.rec_off = (int)tile_rec_off(table_bytes[kv.first], table_area[kv.first]);
                     it.first = (int)recs.size();
                     it.count = (int)kv.second.size();
                     for (int s : kv.second) {

@@ -40,7 +40,8 @@ struct DStage {
 
 struct DBusItem {             // one warp (CTA) of the tile kernel: a table and a run of stage records
     long long blob_off;
-    int bytes, first, count, pad;
+    int bytes, first, count;
+    int rec_off;                // shared-memory byte offset of the stage-record buffers
 };
 
 // (stage, tile) record: everything the tile warp needs about one stage, with
@@ -644,6 +645,8 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
             "%4;" ::"r"(smem_u32(smem)),
             "l"(P.blob + it.blob_off), "r"(it.bytes), "r"(b), "l"(pol)
             : "memory");
+        // the first stage record beside the table (its own mbarrier phase 0)
+        record_load(rb_, smem + it.rec_off, P.bus_recs + it.first);
     }
     // WHAT != 0: the mask is a compile-time constant (the all-callbacks path)
     const unsigned what = WHAT ? WHAT : P.what;
@@ -695,8 +698,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
     const bool any_a = need_j || need_h || need_c || need_f;
 
     // first record (record k completes phase k of rbar) and its inputs
-    if (tid == 0) record_load(rb_, ctx, P.bus_recs + it.first);
-    mbar_wait(rb_, 0);
+    mbar_wait(rb_, 0);                    // (issued with the table copy)
     __syncthreads();
     EndIn pre;
     prefetch(P, ctx[0], V, my_e, tid, sG, need_h, need_c, true, pre);
