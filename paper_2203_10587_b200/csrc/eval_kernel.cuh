@@ -868,7 +868,9 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         }
     }
     cp_wait<0>();
-    if ((tid & 15) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // the last bulk stores must have read the staging area before the CTA (and its shared
+    // memory) retires; their global writes complete with the grid
+    if ((tid & 15) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
