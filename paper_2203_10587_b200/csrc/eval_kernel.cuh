@@ -686,6 +686,16 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
 
     const unsigned short* sround = reinterpret_cast<const unsigned short*>(smem + H->o_sround);
     const unsigned short* sdst = reinterpret_cast<const unsigned short*>(smem + H->o_sdst);
+    const int my_e = tid;
+    const bool any_a = need_j || need_h || need_c || need_f;
+
+    // first record (record k completes phase k of rbar; every thread waits on it) and its
+    // inputs; the area's constant slots are written while those gathers are in flight (the
+    // sum rounds read them after the first stage's barriers)
+    mbar_wait(rb_, 0);                    // (issued with the table copy)
+    EndIn pre;
+    prefetch(P, ctx[0], V, my_e, tid, sG, need_h, need_c, true, pre);
+    cp_commit();
     {
         const unsigned short* cpos = reinterpret_cast<const unsigned short*>(smem + H->o_const);
         const unsigned short* nega = reinterpret_cast<const unsigned short*>(smem + H->o_nega);
@@ -694,15 +704,6 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
         const unsigned short* zpos = reinterpret_cast<const unsigned short*>(smem + H->o_zero);
         for (int i = tid; i < H->nZero; i += TILE_THREADS) A[zpos[i]] = 0.0;
     }
-    const int my_e = tid;
-    const bool any_a = need_j || need_h || need_c || need_f;
-
-    // first record (record k completes phase k of rbar) and its inputs
-    mbar_wait(rb_, 0);                    // (issued with the table copy)
-    __syncthreads();
-    EndIn pre;
-    prefetch(P, ctx[0], V, my_e, tid, sG, need_h, need_c, true, pre);
-    cp_commit();
 
     for (int ri = 0; ri < it.count; ++ri) {
         const DRec& R = ctx[ri & 1];
