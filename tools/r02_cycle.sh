@@ -1,9 +1,8 @@
 #!/bin/bash
 # Round-2 GPU cycle (run under gpurun): bench lines first on a cool GPU (default cfg4, cfgs 1-3,
 # the sharded entry point, the reference arm), then every GPU test (parity report with bit
-# counts), smoke,
-# arm, the default command's launch list, and ncu --set full captures of the tile kernel
-# for every config.  Usage: tools/r02_cycle.sh TAG
+# counts), smoke, the default command's launch list, and ncu --set full captures of the
+# tile kernel for every config.  Usage: tools/r02_cycle.sh TAG
 T=${1:-r02}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1 || { echo "build failed"; tail gpurun_out/${T}_build.log; }
 timeout 900 python bench.py > gpurun_out/${T}_bench_cfg4.json 2> gpurun_out/${T}_bench_cfg4.err; tail -1 gpurun_out/${T}_bench_cfg4.json | cut -c1-300
