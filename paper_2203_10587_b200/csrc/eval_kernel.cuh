@@ -108,6 +108,10 @@ struct EvalParams {
     unsigned* aux_done;       // finished aux items (the last one sums the composite objective)
 };
 
+#ifndef ACOPF_B_UNROLL
+#define ACOPF_B_UNROLL 4
+#endif
+constexpr int B_UNROLL = ACOPF_B_UNROLL;        // sum-round chain loop unroll
 #ifndef ACOPF_WARP_MINB
 #define ACOPF_WARP_MINB 12
 #endif
@@ -762,7 +766,7 @@ __global__ void __launch_bounds__(TILE_THREADS, WARP_MINB / TILE_WARPS) acopf_ti
                 const int wa = da.y & 0xffffu, wb = db.y & 0xffffu;
                 double va = ra[0], vb = rbp[0];
                 const int n = ca > cb ? ca : cb;
-#pragma unroll 4
+#pragma unroll(B_UNROLL)
                 for (int j = 1; j < n; ++j) {
                     if (j < ca) va = va + ra[j * wa];
                     if (j < cb) vb = vb + rbp[j * wb];
