@@ -171,6 +171,8 @@ struct acopf_batch {
     };
     std::vector<HostGraph> host_graphs;
     bool host_graphs_off = false;
+    int host_graph_captures = 0;             // (a caller whose keys never repeat, e.g. a new
+                                             // obj_factor per call, gets the plain path after 32)
     ~acopf_batch() {
         for (auto& g : host_graphs) {
             if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -1409,6 +1411,12 @@ int acopf_batch_eval_host(acopf_batch* b, const double* x, int64_t nx, double ob
             bool same = h.what == what && h.mult == (mult != nullptr) && h.obj_factor == obj_factor;
             for (int k = 0; k < 7 && same; ++k) same = h.sz[k] == (on[k] ? sz[k] : 0) && h.dev[k] == (on[k] ? dp[k] : nullptr);
             if (same) { g = &h; break; }
+        }
+        if (!g && ++b->host_graph_captures > 32) {
+            b->host_graphs_off = true;
+            issue();
+            cuda_check(cudaStreamSynchronize(st), "stream sync");
+            return;
         }
         if (!g) {
             if (b->host_graphs.size() >= 16) {     // bounded cache (e.g. a varying obj_factor)
